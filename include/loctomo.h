@@ -1,0 +1,163 @@
+/*
+ * loctomo.h -- C-ABI of the B200-native local tomography library
+ * (local approximation of regularized iterative reconstruction,
+ *  Pelt & Batenburg, arXiv 1604.02292; "P:Lnnn" = PAPER.md line).
+ *
+ * Conventions (V1-V4):
+ *  - image: N x N fp32, row-major, row i = 0 at the top; pixel centre
+ *    x_j = j - (N-1)/2, y_i = (N-1)/2 - i.
+ *  - sinogram: [N_theta][N_d] fp32, bin centre t_d = d - (N_d-1)/2.
+ *  - W: Joseph interpolation, W[(a,d),(i,j)] = hat((t_d - t_ij)/c_a)/c_a,
+ *    c_a = max(|cos|,|sin|); W^T is its exact transpose.
+ *  - alpha = 1/(N_theta N_d).
+ *  - ROI: square core of half-side `radius` around integer pixel-corner
+ *    centre (row, col); extended ROI L' = core padded by `margin` and clipped
+ *    to the grid.
+ *
+ * Memory: every pointer named d_* is a DEVICE pointer owned by the caller
+ * (the Python binding allocates with torch); h_* pointers are HOST memory,
+ * read (or written) only during the call.  The library never allocates
+ * device memory: all scratch lives in the caller-provided workspace bound
+ * with lt_plan_bind_workspace.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream); all device work is stream-ordered and asynchronous
+ * unless stated otherwise.
+ *
+ * Errors: LT_OK = 0; LT_ERR_RUNTIME = 1 (CUDA failure); LT_ERR_INVALID = 2
+ * (argument violates the contract; detected on the host before any launch,
+ * no partial output).  lt_last_error() returns a thread-local message.
+ * Results are deterministic: no atomics, fixed summation orders.
+ */
+#ifndef LOCTOMO_H
+#define LOCTOMO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LT_OK 0
+#define LT_ERR_RUNTIME 1
+#define LT_ERR_INVALID 2
+
+/* flags for lt_roi_setup */
+#define LT_DISC_ON 1   /* disc pre-correction, default on */
+
+typedef struct lt_plan lt_plan;
+
+/* Plan a batch of local reconstructions (host only; no device work).
+ *  n, n_angles, n_det: N, N_theta, N_d.  n_det must be odd
+ *      (filter centring, A3).
+ *  angles: host, n_angles radians, strictly increasing in [0, pi).
+ *  n_roi, center_row, center_col: host, the ROI core centres (integer pixel
+ *      corners); every core must lie inside the grid.
+ *  radius (>= 1), margin (>= 0): core half-side r and padding m.
+ *  n_iter (>= 1): outer iterations n; the filter bank holds u_1..u_n.
+ *  rank, world: this process's share of the ROIs (longest-processing-time
+ *      partition over valid-pixel counts); world = 1
+ *      for a single GPU.
+ *  out: receives the plan.  Returns LT_ERR_INVALID on any violation. */
+int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angles,
+                 int32_t n_roi, const int32_t* center_row, const int32_t* center_col,
+                 int32_t radius, int32_t margin, int32_t n_iter, int32_t flags,
+                 int32_t rank, int32_t world, lt_plan** out);
+
+/* Bytes of device workspace the plan needs (tables, filter bank, convolution
+ * cache, per-ROI state). */
+int64_t lt_plan_workspace_bytes(const lt_plan* plan);
+
+/* Bind a device workspace of >= lt_plan_workspace_bytes bytes (256-byte
+ * aligned) and upload the geometry tables (synchronous on `stream`). */
+int lt_plan_bind_workspace(lt_plan* plan, void* d_ws, int64_t bytes, void* stream);
+
+/* Local ROI count on this rank and their global ROI indices (host array of
+ * lt_plan_local_count entries). */
+int32_t lt_plan_local_count(const lt_plan* plan);
+int lt_plan_local_rois(const lt_plan* plan, int32_t* h_global_idx);
+
+/* Host copies of the plan's ROI tables (for tests and tooling):
+ * h_rects [local_count][6] = tile row0, col0 (global coords of the extended
+ * square's top-left pixel), valid rect vr0, vr1, vc0, vc1 (tile-local);
+ * h_d0 [local_count][N_theta] = first detector bin of each ROI's window;
+ * *h_wwin = window width W(h) = 2 ceil((2h-1)/sqrt2) + 4 (V4).
+ * Any pointer may be NULL. */
+int lt_plan_tables(const lt_plan* plan, int32_t* h_rects, int32_t* h_d0, int32_t* h_wwin);
+
+/* Alg. 1: compute every filter u_k, k = 1..n, into the
+ * workspace; also caches W D for the disc correction.  Geometry-only. */
+int lt_filter_bank(lt_plan* plan, void* stream);
+
+/* Copy a filter bank [n_iter][N_theta][N_d] fp32 (device) into / out of the
+ * plan (per-geometry reuse). */
+int lt_set_bank(lt_plan* plan, const float* d_bank, void* stream);
+int lt_get_bank(const lt_plan* plan, float* d_bank, void* stream);
+
+/* Forward projection.  roi = -1: full grid, d_img N x N -> d_sino N_theta x N_d
+ * (W x).  roi >= 0 (local index): W M_{L'} x, the ROI's extended
+ * region only; d_sino is the full sinogram (zero where W_{L'} is). */
+int lt_project(const lt_plan* plan, int32_t roi, const float* d_img, float* d_sino, void* stream);
+
+/* Backprojection.  roi = -1: W^T s on the full grid; roi >= 0: M_{L'} W^T s
+ * (P:L251), d_img is N x N and zero outside L'. */
+int lt_backproject(const lt_plan* plan, int32_t roi, const float* d_sino, float* d_img, void* stream);
+
+/* Disc pre-correction: d_pc = p - c W D, c minimizes the
+ * zero-frequency l2 norm; *d_c (device, 1 float) receives c.  Needs
+ * lt_filter_bank (or lt_set_bank + this computing W D on first use). */
+int lt_disc_correct(lt_plan* plan, const float* d_sino, float* d_pc, float* d_c, void* stream);
+
+/* Convolution cache b_k = C_{u_k} p_c for k = 1..n into the
+ * workspace; lt_get_conv copies it out ([n][N_theta][N_d]). */
+int lt_conv_cache(lt_plan* plan, const float* d_pc, void* stream);
+int lt_get_conv(const lt_plan* plan, float* d_out, void* stream);
+
+/* Local box-constrained SIRT (Alg. 2 with d of P:L538-546) on every local
+ * ROI: disc (if LT_DISC_ON) -> conv cache -> n iterations -> crop.
+ * d_sino: N_theta x N_d.  lo <= hi (use +INFINITY for "nonneg" SIRT).
+ * d_cores: [local_count][2r][2r]. */
+int lt_sirt_solve(lt_plan* plan, const float* d_sino, float lo, float hi, float* d_cores, void* stream);
+
+/* Local FISTA-TV (Alg. 3, FISTA update per DESIGN.md A12, FGP prox A13/A14).
+ * lambda >= 0, n_fgp >= 1. */
+int lt_tv_solve(lt_plan* plan, const float* d_sino, float lambda, int32_t n_fgp, float* d_cores, void* stream);
+
+/* Extended-ROI results of the last solve: [local_count][2h][2h], the valid
+ * part top-left aligned, zeros elsewhere (for stage-wise parity). */
+int lt_get_ext(const lt_plan* plan, float* d_ext, void* stream);
+
+/* Combine (A19): d_image (N x N) = mean of the cores
+ * covering each pixel, in ascending global ROI order, 0 where uncovered.
+ * d_cores_all: [n_slots][2r][2r] (e.g. the all-gather of every rank's
+ * d_cores); h_slot_roi: host, the global ROI index of each slot (-1 = empty). */
+int lt_combine_rois(const lt_plan* plan, const float* d_cores_all, int32_t n_slots,
+                    const int32_t* h_slot_roi, float* d_image, void* stream);
+
+/* End-to-end entry with HOST buffers (pinned recommended): copies h_sino in,
+ * runs lt_sirt_solve (mode 0) or lt_tv_solve (mode 1), combines this rank's
+ * cores into h_image (N x N).  Synchronous. */
+int lt_solve_host(lt_plan* plan, int32_t mode, const float* h_sino, float p0, float p1,
+                  int32_t n_fgp, float* h_image, void* stream);
+
+/* Global solvers the method approximates: box-SIRT
+ * (eq. sirtbox) and FISTA-TV on the full grid, from 0. */
+int lt_global_sirt(lt_plan* plan, const float* d_sino, int32_t n_iter, float lo, float hi,
+                   float* d_img, void* stream);
+int lt_global_tv(lt_plan* plan, const float* d_sino, int32_t n_iter, float lambda, int32_t n_fgp,
+                 float* d_img, void* stream);
+
+/* FGP TV prox (Beck & Teboulle) on `count` independent h x w
+ * images (d_in/d_out: count x h x w), same kernel the TV solve uses
+ * (h, w <= 256). */
+int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda,
+                 int32_t n_fgp, float* d_out, void* stream);
+
+/* Number of kernels this library has launched so far (process-wide). */
+int64_t lt_launch_count(void);
+
+void lt_plan_destroy(lt_plan* plan);
+const char* lt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOCTOMO_H */

@@ -1,0 +1,268 @@
+"""B200-native local approximation of regularized iterative tomography
+(Pelt & Batenburg, arXiv 1604.02292).
+
+Thin ctypes binding over the C-ABI library ``_loctomo.so`` (declared in
+``include/loctomo.h``): argument marshalling only -- every step of the path
+runs in the library's sm_100a kernels.  PyTorch provides device memory and
+streams.  There is no CPU fallback: importing this package without the built
+extension raises, and every call requires CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_loctomo.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(the CUDA extension is required; there is no fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+LT_OK, LT_ERR_RUNTIME, LT_ERR_INVALID = 0, 1, 2
+LT_DISC_ON = 1
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+_F = ctypes.c_float
+_i64 = ctypes.c_int64
+
+_SIGS = {
+    "lt_roi_setup": ([_I, _I, _I, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P], _I),
+    "lt_plan_workspace_bytes": ([_P], _i64),
+    "lt_plan_bind_workspace": ([_P, _P, _i64, _P], _I),
+    "lt_plan_local_count": ([_P], _I),
+    "lt_plan_local_rois": ([_P, _P], _I),
+    "lt_plan_tables": ([_P, _P, _P, _P], _I),
+    "lt_filter_bank": ([_P, _P], _I),
+    "lt_set_bank": ([_P, _P, _P], _I),
+    "lt_get_bank": ([_P, _P, _P], _I),
+    "lt_project": ([_P, _I, _P, _P, _P], _I),
+    "lt_backproject": ([_P, _I, _P, _P, _P], _I),
+    "lt_disc_correct": ([_P, _P, _P, _P, _P], _I),
+    "lt_conv_cache": ([_P, _P, _P], _I),
+    "lt_get_conv": ([_P, _P, _P], _I),
+    "lt_sirt_solve": ([_P, _P, _F, _F, _P, _P], _I),
+    "lt_tv_solve": ([_P, _P, _F, _I, _P, _P], _I),
+    "lt_get_ext": ([_P, _P, _P], _I),
+    "lt_combine_rois": ([_P, _P, _I, _P, _P, _P], _I),
+    "lt_solve_host": ([_P, _I, _P, _F, _F, _I, _P, _P], _I),
+    "lt_global_sirt": ([_P, _P, _I, _F, _F, _P, _P], _I),
+    "lt_global_tv": ([_P, _P, _I, _F, _I, _P, _P], _I),
+    "lt_fgp_batch": ([_I, _I, _I, _P, _F, _I, _P, _P], _I),
+    "lt_launch_count": ([], _i64),
+    "lt_plan_destroy": ([_P], None),
+    "lt_last_error": ([], ctypes.c_char_p),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+
+EXPORTS = tuple(_SIGS)
+
+
+class LtError(RuntimeError):
+    pass
+
+
+def _chk(rc: int, what: str) -> None:
+    if rc != LT_OK:
+        msg = _lib.lt_last_error().decode()
+        raise (ValueError if rc == LT_ERR_INVALID else LtError)(f"{what}: {msg} (code {rc})")
+
+
+def _stream(dev=None) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _cuda_f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32):
+        raise TypeError(f"{name} must be a CUDA float32 tensor")
+    return t.contiguous()
+
+
+def launch_count() -> int:
+    """Kernels launched by the library so far (process-wide)."""
+    return int(_lib.lt_launch_count())
+
+
+def window_width(h: int) -> int:
+    return 2 * math.ceil((2 * h - 1) / math.sqrt(2) - 1e-12) + 4
+
+
+class Plan:
+    """One geometry + ROI batch (``lt_roi_setup``), with its device workspace.
+
+    n, angles, n_det: grid size N, projection angles (rad), detector count N_d.
+    centres: (R, 2) integer core centres (row, col); radius r, margin m.
+    n_iter: outer iterations n (the filter bank holds u_1..u_n).
+    """
+
+    def __init__(self, n: int, angles, n_det: int, centres, radius: int, margin: int, n_iter: int,
+                 disc: bool = True, rank: int = 0, world: int = 1, device=None, bind: bool = True):
+        """bind=False plans on the host only (tables, partition); no device memory."""
+        if bind:
+            self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        else:
+            self.device = None
+        ang = np.ascontiguousarray(np.asarray(angles, dtype=np.float64))
+        cen = np.ascontiguousarray(np.asarray(centres, dtype=np.int32).reshape(-1, 2))
+        rows = np.ascontiguousarray(cen[:, 0]); cols = np.ascontiguousarray(cen[:, 1])
+        self.n, self.n_det, self.n_angles = int(n), int(n_det), len(ang)
+        self.radius, self.margin, self.n_iter = int(radius), int(margin), int(n_iter)
+        self.angles, self.centres = ang, cen
+        self.h = self.radius + self.margin
+        self._p = ctypes.c_void_p()
+        _chk(_lib.lt_roi_setup(self.n, len(ang), self.n_det, ang.ctypes.data, len(cen), rows.ctypes.data,
+                               cols.ctypes.data, self.radius, self.margin, self.n_iter,
+                               LT_DISC_ON if disc else 0, rank, world, ctypes.byref(self._p)), "lt_roi_setup")
+        self.workspace_bytes = nbytes = int(_lib.lt_plan_workspace_bytes(self._p))
+        if bind:
+            with torch.cuda.device(self.device):
+                self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+                _chk(_lib.lt_plan_bind_workspace(self._p, self.ws.data_ptr(), nbytes, _stream(self.device)),
+                     "lt_plan_bind_workspace")
+        self.R = int(_lib.lt_plan_local_count(self._p))
+        loc = np.zeros(max(self.R, 1), dtype=np.int32)
+        _chk(_lib.lt_plan_local_rois(self._p, loc.ctypes.data), "lt_plan_local_rois")
+        self.local_rois = loc[:self.R].copy()
+
+    def __del__(self):
+        p = getattr(self, "_p", None)
+        if p is not None and p.value:
+            _lib.lt_plan_destroy(p)
+            self._p = None
+
+    def tables(self):
+        """(rects [R, 6] = row0, col0, vr0, vr1, vc0, vc1; d0 [R, N_theta]; window width)."""
+        R = max(self.R, 1)
+        rects = np.zeros((R, 6), dtype=np.int32)
+        d0 = np.zeros((R, self.n_angles), dtype=np.int32)
+        w = ctypes.c_int32(0)
+        _chk(_lib.lt_plan_tables(self._p, rects.ctypes.data, d0.ctypes.data, ctypes.byref(w)), "lt_plan_tables")
+        return rects[:self.R], d0[:self.R], int(w.value)
+
+    # ---- geometry / bank ---------------------------------------------------
+    @property
+    def alpha(self) -> float:
+        return 1.0 / (self.n_angles * self.n_det)
+
+    def _empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, dtype=torch.float32, device=self.device)
+
+    def filter_bank(self) -> None:
+        _chk(_lib.lt_filter_bank(self._p, _stream(self.device)), "lt_filter_bank")
+
+    def set_bank(self, bank: torch.Tensor) -> None:
+        bank = _cuda_f32(bank, "bank")
+        assert bank.numel() == self.n_iter * self.n_angles * self.n_det
+        _chk(_lib.lt_set_bank(self._p, bank.data_ptr(), _stream(self.device)), "lt_set_bank")
+        self._keep = bank
+
+    def get_bank(self) -> torch.Tensor:
+        out = self._empty(self.n_iter, self.n_angles, self.n_det)
+        _chk(_lib.lt_get_bank(self._p, out.data_ptr(), _stream(self.device)), "lt_get_bank")
+        return out
+
+    # ---- operators -----------------------------------------------------------
+    def project(self, img: torch.Tensor, roi: int = -1) -> torch.Tensor:
+        img = _cuda_f32(img, "img")
+        out = self._empty(self.n_angles, self.n_det)
+        _chk(_lib.lt_project(self._p, roi, img.data_ptr(), out.data_ptr(), _stream(self.device)), "lt_project")
+        return out
+
+    def backproject(self, sino: torch.Tensor, roi: int = -1) -> torch.Tensor:
+        sino = _cuda_f32(sino, "sino")
+        out = self._empty(self.n, self.n)
+        _chk(_lib.lt_backproject(self._p, roi, sino.data_ptr(), out.data_ptr(), _stream(self.device)), "lt_backproject")
+        return out
+
+    def disc_correct(self, sino: torch.Tensor):
+        sino = _cuda_f32(sino, "sino")
+        pc = self._empty(self.n_angles, self.n_det)
+        c = self._empty(1)
+        _chk(_lib.lt_disc_correct(self._p, sino.data_ptr(), pc.data_ptr(), c.data_ptr(), _stream(self.device)),
+             "lt_disc_correct")
+        return pc, c
+
+    def conv_cache(self, pc: torch.Tensor) -> torch.Tensor:
+        pc = _cuda_f32(pc, "pc")
+        _chk(_lib.lt_conv_cache(self._p, pc.data_ptr(), _stream(self.device)), "lt_conv_cache")
+        out = self._empty(self.n_iter, self.n_angles, self.n_det)
+        _chk(_lib.lt_get_conv(self._p, out.data_ptr(), _stream(self.device)), "lt_get_conv")
+        return out
+
+    # ---- solves ----------------------------------------------------------------
+    def sirt_solve(self, sino: torch.Tensor, lo: float = 0.0, hi: float = math.inf,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        sino = _cuda_f32(sino, "sino")
+        side = 2 * self.radius
+        out = self._empty(self.R, side, side) if out is None else out
+        _chk(_lib.lt_sirt_solve(self._p, sino.data_ptr(), lo, hi, out.data_ptr(), _stream(self.device)),
+             "lt_sirt_solve")
+        return out
+
+    def tv_solve(self, sino: torch.Tensor, lam: float, n_fgp: int = 100,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        sino = _cuda_f32(sino, "sino")
+        side = 2 * self.radius
+        out = self._empty(self.R, side, side) if out is None else out
+        _chk(_lib.lt_tv_solve(self._p, sino.data_ptr(), lam, n_fgp, out.data_ptr(), _stream(self.device)),
+             "lt_tv_solve")
+        return out
+
+    def get_ext(self) -> torch.Tensor:
+        E = 2 * self.h
+        out = self._empty(self.R, E, E)
+        _chk(_lib.lt_get_ext(self._p, out.data_ptr(), _stream(self.device)), "lt_get_ext")
+        return out
+
+    def combine(self, cores_all: torch.Tensor, slot_roi: Sequence[int],
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        cores_all = _cuda_f32(cores_all, "cores_all")
+        slots = np.ascontiguousarray(np.asarray(slot_roi, dtype=np.int32))
+        out = self._empty(self.n, self.n) if out is None else out
+        _chk(_lib.lt_combine_rois(self._p, cores_all.data_ptr(), len(slots), slots.ctypes.data, out.data_ptr(),
+                                  _stream(self.device)), "lt_combine_rois")
+        return out
+
+    def solve_host(self, mode: str, sino_host: torch.Tensor, p0: float, p1: float = 0.0, n_fgp: int = 100,
+                   image_host: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """End-to-end with host buffers (pinned tensors recommended)."""
+        assert not sino_host.is_cuda and sino_host.dtype == torch.float32 and sino_host.is_contiguous()
+        if image_host is None:
+            image_host = torch.empty(self.n, self.n, dtype=torch.float32, pin_memory=True)
+        _chk(_lib.lt_solve_host(self._p, 0 if mode == "sirt" else 1, sino_host.data_ptr(), p0, p1, n_fgp,
+                                image_host.data_ptr(), _stream(self.device)), "lt_solve_host")
+        return image_host
+
+    def global_sirt(self, sino: torch.Tensor, n_iter: int, lo: float = 0.0, hi: float = math.inf) -> torch.Tensor:
+        sino = _cuda_f32(sino, "sino")
+        out = self._empty(self.n, self.n)
+        _chk(_lib.lt_global_sirt(self._p, sino.data_ptr(), n_iter, lo, hi, out.data_ptr(), _stream(self.device)),
+             "lt_global_sirt")
+        return out
+
+    def global_tv(self, sino: torch.Tensor, n_iter: int, lam: float, n_fgp: int = 100) -> torch.Tensor:
+        sino = _cuda_f32(sino, "sino")
+        out = self._empty(self.n, self.n)
+        _chk(_lib.lt_global_tv(self._p, sino.data_ptr(), n_iter, lam, n_fgp, out.data_ptr(), _stream(self.device)),
+             "lt_global_tv")
+        return out
+
+
+def fgp_batch(x: torch.Tensor, lam: float, n_fgp: int) -> torch.Tensor:
+    """FGP TV prox of each (h, w) image in x (count, h, w), the solver's kernel."""
+    x = _cuda_f32(x, "x")
+    cnt, h, w = x.shape
+    out = torch.empty_like(x)
+    _chk(_lib.lt_fgp_batch(h, w, cnt, x.data_ptr(), lam, n_fgp, out.data_ptr(), _stream(x.device)), "lt_fgp_batch")
+    return out

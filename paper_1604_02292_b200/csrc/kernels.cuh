@@ -1,0 +1,687 @@
+// kernels.cuh -- sm_100a kernels of the local tomography hot path.
+//
+// Notation follows PAPER.md (arXiv 1604.02292) and DESIGN.md:
+//   W   Joseph projector, W[(a,d),(i,j)] = hat((t_d - t_ij)/c_a)/c_a      (V2)
+//   "tile"  = a square block of pixels processed as one unit: the extended
+//             ROI L' of one local reconstruction, or the
+//             whole N x N grid for the global operators (Alg. 1, a10).
+//   "window" = the contiguous run of detector bins that a tile can reach at
+//             one angle (V4); W_{L'} is evaluated only there.
+//
+// Layouts (DESIGN.md §Data layout):
+//   padded tile image  [tile][T][TP], data at columns PADL..PADL+T-1, two-sided
+//                      zero padding so Joseph taps never need bounds checks.
+//                      Every padded image has a transposed twin (lines = columns)
+//                      so column-driven angles march contiguous memory too.
+//   plain tile image   [tile][T][T]
+//   window sinogram    [tile][N_theta][Wwin]
+//   sinogram           [N_theta][N_d]
+#pragma once
+#include <cuda_runtime.h>
+#include <cooperative_groups.h>
+#include <stdint.h>
+
+namespace lt {
+namespace cg = cooperative_groups;
+
+constexpr int PADL = 4;           // left zero padding of padded tile rows
+constexpr int PADR = 4;           // right zero padding
+constexpr float MAGICF = 12582912.0f;   // 1.5 * 2^23: x + MAGICF rounds x to an integer in the low mantissa bits
+constexpr int MAGICI = 0x4B400000;
+
+struct AngF {       // per-angle constants (fp32), 32 B
+    float cs, sn;   // cos, sin
+    float invc;     // 1/c, c = max(|cos|,|sin|)
+    float ic2;      // 1/c^2
+    float K;        // 1/c - 0.5/c^2  (hat weights in the magic-floor form)
+    float A, B;     // Joseph marching: pos(w, l) = Lc + (w - tau_c) A + (l - Lc) B
+    int col;        // 1 = column-driven (|sin| > |cos|): march columns on the transposed image
+};
+
+struct TileT {      // per tile, tile-local coordinates
+    int row0, col0;           // global coords of tile pixel (0,0) (negative if clipped)
+    int vr0, vr1, vc0, vc1;   // valid rectangle (inside the grid), half-open
+    int pad0, pad1;
+};
+
+struct Geo {
+    int n, na, nd;
+    const AngF* ang;
+    const double* cs64;
+    const double* sn64;
+    const double* A64;
+    const double* B64;
+};
+
+struct Tiles {
+    int T, TP, Wwin, ntiles;
+    const TileT* tile;
+    const int* d0;          // [tile][na] window start (global bin index)
+    const double* tauc;     // [tile][na] bin coordinate of the tile centre relative to d0
+};
+
+struct SinoView {           // element (tile r, angle a, window bin w)
+    const float* base;
+    long long tile_stride;  // elements between tiles (0 = shared sinogram)
+    int row_stride;         // elements between angles
+    int use_d0;             // 1: index = d0[r][a] + w (full sinogram); 0: index = w (window sinogram)
+    int len;                // valid index range [0, len)
+};
+
+__device__ __forceinline__ float sv_fetch(const SinoView& s, const int* d0, int na, int r, int a, int w) {
+    const int idx = (s.use_d0 ? __ldg(d0 + r * na + a) : 0) + w;
+    if (idx < 0 || idx >= s.len) return 0.f;
+    return __ldg(s.base + (long long)r * s.tile_stride + (long long)a * s.row_stride + idx);
+}
+
+// ---------------------------------------------------------------------------
+// Forward projection W_{L'} (ray driven, Joseph).  One thread = one ray
+// (tile r, angle a, window bin w).  The ray marches the lines (rows for
+// row-driven angles, columns via the transposed image otherwise) that its
+// footprint can touch inside the valid rectangle, interpolating linearly
+// between the two neighbouring pixel centres (V2).
+// Coordinates: the ray position is re-anchored in fp64 every 32 lines, so
+// the fp32 offsets stay < 34 pixels.
+// MODE 0: out[r][a][w] = (W y)   (zero for bins outside [0, N_d))
+// MODE 1: Alg. 1 step: out = v = W c; bank_k = bank_{k-1} + alpha v
+// MODE 2: residual: out = p - W x  (global SIRT, eq. sirtit)
+// ---------------------------------------------------------------------------
+struct FpArgs {
+    const float* img;       // padded images, row-driven source
+    const float* imgT;      // transposed twin
+    long long img_tstride;  // elements between tiles
+    float* out;             // [tile][na][Wwin]
+    long long out_tstride;
+    const float* aux_in;    // MODE 1: bank_{k-1} (nullable); MODE 2: p
+    float* aux_out;         // MODE 1: bank_k
+    float alpha;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_fp(Geo g, Tiles t, FpArgs f) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int a = blockIdx.y, r = blockIdx.z;
+    if (w >= t.Wwin) return;
+    const int na = g.na;
+    const int d = __ldg(t.d0 + r * na + a) + w;
+    float acc = 0.f;
+    const AngF an = g.ang[a];
+    if (d >= 0 && d < g.nd) {
+        const TileT ti = t.tile[r];
+        const int lv0 = an.col ? ti.vc0 : ti.vr0, lv1 = an.col ? ti.vc1 : ti.vr1;
+        const int pv0 = an.col ? ti.vr0 : ti.vc0, pv1 = an.col ? ti.vr1 : ti.vc1;
+        const double Lc = 0.5 * (t.T - 1);
+        const double A = g.A64[a], B = g.B64[a];
+        const double Pw = Lc + ((double)w - t.tauc[r * na + a]) * A;   // position at the centre line
+        int la, lb;
+        if (fabs(B) < 1e-12) {
+            const bool hit = (Pw > pv0 - 1.0) && (Pw < (double)pv1);
+            la = hit ? lv0 : 0;
+            lb = hit ? lv1 : 0;
+        } else {
+            double l1 = Lc + ((pv0 - 1.0) - Pw) / B, l2 = Lc + ((double)pv1 - Pw) / B;
+            if (l1 > l2) { const double tmp = l1; l1 = l2; l2 = tmp; }
+            la = max(lv0, (int)floor(l1));
+            lb = min(lv1, (int)ceil(l2) + 1);
+        }
+        const float* base = (an.col ? f.imgT : f.img) + (long long)r * f.img_tstride + PADL;
+        const float Bf = an.B;
+        for (int l = la; l < lb; l += 32) {
+            const double p0 = Pw + ((double)l - Lc) * B;
+            const double fb = floor(p0);
+            const int ib = (int)fb;
+            const float f0 = (float)(p0 - fb) - 0.5f;     // -0.5: magic rounding gives floor
+            const int cnt = min(32, lb - l);
+            const float* rowp = base + (long long)l * t.TP + ib;
+            #pragma unroll 4
+            for (int i = 0; i < cnt; ++i) {
+                const float tt = fmaf((float)i, Bf, f0);
+                const float rm = tt + MAGICF;
+                const int m = __float_as_int(rm) - MAGICI;
+                const float gg = tt - (rm - MAGICF);        // in [-0.5, 0.5]; frac = gg + 0.5
+                const float* q = rowp + (long long)i * t.TP + m;
+                const float v0 = __ldg(q), v1 = __ldg(q + 1);
+                const float sum = v0 + v1, dif = v1 - v0;
+                acc = fmaf(0.5f, sum, acc);
+                acc = fmaf(gg, dif, acc);
+            }
+        }
+        acc *= an.invc;
+    }
+    const long long o = (long long)r * f.out_tstride + (long long)a * t.Wwin + w;
+    if (MODE == 0) {
+        f.out[o] = acc;
+    } else if (MODE == 1) {
+        f.out[o] = acc;
+        const float prev = f.aux_in ? f.aux_in[(long long)a * g.nd + w] : 0.f;
+        f.aux_out[(long long)a * g.nd + w] = fmaf(f.alpha, acc, prev);
+    } else {
+        const float pv = (d >= 0 && d < g.nd) ? f.aux_in[(long long)a * g.nd + d] : 0.f;
+        f.out[o] = pv - acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Backprojection M_{L'} W^T (pixel driven, exact transpose of k_fp) with the
+// fused solver epilogues.  CTA = (tile r, 32x32 sub-tile); thread = 4 pixels
+// of one column.  Per chunk of CA angles the CTA stages, for each angle, the
+// SW-bin sub-window of each source sinogram that its sub-tile can reach
+// (interleaved float2 for the two-sinogram gather of the local iteration),
+// then every pixel gathers its 2 hat taps per angle from shared memory.
+// Anchors: tau at the sub-tile centre in fp64, fp32 offsets <= 15.5 px.
+// ---------------------------------------------------------------------------
+constexpr int BP_CA = 64;   // angles per staged chunk
+constexpr int BP_SW = 52;   // bins per angle per sub-tile (>= 32*sqrt2 + 4)
+
+enum BpMode {
+    BP_PLAIN_TILE = 0,   // out plain [tile][T][T]  (stage-wise parity, lt_backproject)
+    BP_PLAIN_GLOBAL = 1, // out N x N at the tile's global position
+    BP_BOX = 2,          // Alg. 2 with the box correction
+    BP_TV = 3,           // Alg. 3 lines 4-5: v = x_s + x_L - alpha W^T W x_L; keep x_s
+    BP_ALG1 = 4,         // Alg. 1: c <- c - alpha W^T v (padded image + twin)
+    BP_GSIRT = 5,        // global box-SIRT: x <- clamp(x + alpha W^T r)
+    BP_GTV = 6           // global FISTA-TV: v = x + alpha W^T r (plain N x N)
+};
+
+struct BpEpi {
+    float* out; long long out_tstride; int out_pitch;     // plain outputs
+    float* y; float* yT; long long y_tstride;              // padded tile images (state)
+    float* v; float* xs; long long p_tstride;              // plain [T][T] (TV)
+    const float* discc; int use_disc;                      // disc gray value (device)
+    float alpha, lo, hi; int last;
+};
+
+template <int NS, int MODE>
+__global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoView s2, BpEpi e) {
+    __shared__ float2 sw[BP_CA][BP_SW];
+    __shared__ float4 sa[BP_CA];
+    __shared__ float sanch[BP_CA];
+    __shared__ int ssub0[BP_CA];
+
+    const int r = blockIdx.y;
+    const int T = t.T, na = g.na;
+    const int nsx = (T + 31) >> 5;
+    const int sty = blockIdx.x / nsx, stx = blockIdx.x - sty * nsx;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int pj = stx * 32 + tx;
+    const int pi0 = sty * 32 + ty * 4;
+    const double Lc = 0.5 * (T - 1);
+    const double dxc = stx * 32 + 15.5 - Lc, dyc = sty * 32 + 15.5 - Lc;
+    const float dx = (float)tx - 15.5f, dy0 = (float)(ty * 4) - 15.5f;
+
+    float g1[4] = {0.f, 0.f, 0.f, 0.f}, g2[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int a0 = 0; a0 < na; a0 += BP_CA) {
+        const int ca = min(BP_CA, na - a0);
+        __syncthreads();
+        for (int q = threadIdx.x; q < ca; q += blockDim.x) {
+            const int a = a0 + q;
+            const double tc = t.tauc[r * na + a] + dxc * g.cs64[a] - dyc * g.sn64[a];
+            const int sub0 = (int)floor(tc) - BP_SW / 2;
+            sanch[q] = (float)(tc - (double)sub0) - 0.5f;
+            ssub0[q] = sub0;
+            const AngF an = g.ang[a];
+            sa[q] = make_float4(an.cs, an.sn, an.K, an.ic2);
+        }
+        __syncthreads();
+        for (int el = threadIdx.x; el < ca * BP_SW; el += blockDim.x) {
+            const int q = el / BP_SW, w = el - q * BP_SW;
+            const int a = a0 + q, wb = ssub0[q] + w;
+            const float v1 = sv_fetch(s1, t.d0, na, r, a, wb);
+            const float v2 = NS == 2 ? sv_fetch(s2, t.d0, na, r, a, wb) : 0.f;
+            sw[q][w] = make_float2(v1, v2);
+        }
+        __syncthreads();
+        #pragma unroll 2
+        for (int q = 0; q < ca; ++q) {
+            const float4 A4 = sa[q];
+            const float t0 = fmaf(dx, A4.x, fmaf(-dy0, A4.y, sanch[q]));
+            const float2* row = sw[q];
+            #pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float tt = fmaf(-(float)p, A4.y, t0);
+                const float rm = tt + MAGICF;
+                const int m = __float_as_int(rm) - MAGICI;
+                const float gg = tt - (rm - MAGICF);
+                const float w0 = fmaxf(0.f, fmaf(-gg, A4.w, A4.z));
+                const float w1 = fmaxf(0.f, fmaf(gg, A4.w, A4.z));
+                const float2 b0 = row[m], b1 = row[m + 1];
+                g1[p] = fmaf(w0, b0.x, fmaf(w1, b1.x, g1[p]));
+                if (NS == 2) g2[p] = fmaf(w0, b0.y, fmaf(w1, b1.y, g2[p]));
+            }
+        }
+    }
+
+    // ---- epilogue ------------------------------------------------------------
+    const TileT ti = t.tile[r];
+    const int n = g.n;
+    float discc = 0.f;
+    if ((MODE == BP_BOX || MODE == BP_TV) && e.use_disc) discc = *e.discc;
+    #pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int i = pi0 + p, j = pj;
+        if (i >= T || j >= T) continue;
+        const bool valid = i >= ti.vr0 && i < ti.vr1 && j >= ti.vc0 && j < ti.vc1;
+        const long long pp = (long long)r * e.y_tstride + (long long)i * t.TP + PADL + j;
+        const long long pt = (long long)r * e.y_tstride + (long long)j * t.TP + PADL + i;
+        if (MODE == BP_PLAIN_TILE) {
+            e.out[(long long)r * e.out_tstride + (long long)i * T + j] = valid ? g1[p] : 0.f;
+        } else if (MODE == BP_PLAIN_GLOBAL) {
+            if (valid) e.out[(long long)(ti.row0 + i) * e.out_pitch + (ti.col0 + j)] = g1[p];
+        } else if (MODE == BP_BOX || MODE == BP_TV) {
+            float xs = 0.f, yv = 0.f, val = 0.f;
+            if (valid) {
+                float dval = 0.f;
+                if (e.use_disc) {
+                    const int gi = ti.row0 + i, gj = ti.col0 + j;
+                    const int u = 2 * gj - n + 1, v = 2 * gi - n + 1;   // 2x, 2y of the pixel centre
+                    dval = (u * u + v * v <= n * n) ? discc : 0.f;      // D: centred disc, diameter N
+                }
+                xs = g1[p] + dval;                                       // x_s^k = FBP_L(p_c, u_k) + c D
+                yv = e.y[pp];
+                const float S = xs + yv - e.alpha * g2[p];               // S(x^{k-1}) split
+                if (MODE == BP_BOX) {
+                    const float x = fminf(fmaxf(S, e.lo), e.hi);         // eq. sirtbox
+                    val = e.last ? x : x - xs;                           // y^k = clamp(S) - x_s^k
+                } else {
+                    val = S;
+                }
+            }
+            if (MODE == BP_BOX) {
+                e.y[pp] = val;
+                e.yT[pt] = val;
+            } else {
+                const long long pl = (long long)r * e.p_tstride + (long long)i * T + j;
+                e.v[pl] = val;
+                e.xs[pl] = xs;
+            }
+        } else if (MODE == BP_ALG1) {
+            const float c = valid ? e.y[pp] - e.alpha * g1[p] : 0.f;
+            e.y[pp] = c;
+            e.yT[pt] = c;
+        } else if (MODE == BP_GSIRT) {
+            const float x = valid ? fminf(fmaxf(e.y[pp] + e.alpha * g1[p], e.lo), e.hi) : 0.f;
+            e.y[pp] = x;
+            e.yT[pt] = x;
+        } else if (MODE == BP_GTV) {
+            if (valid) e.out[(long long)i * T + j] = e.y[pp] + e.alpha * g1[p];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// FGP TV prox (Beck & Teboulle, named at P:L661-663; A13/A14),
+// anisotropic, Neumann boundary on each tile's valid rectangle, fused with
+// the FISTA update of Alg. 3 (lines 7-9, corrected per A12).
+// One thread-block CLUSTER per tile: CTA k of K owns a band of RB rows; all
+// FGP state (b, r, s, p_old, q_old, z) lives in shared memory for all n_FGP
+// iterations; the one halo row each phase needs is read from the neighbour
+// CTA's shared memory (DSMEM).  Two cluster barriers per FGP iteration.
+// ---------------------------------------------------------------------------
+struct FgpArgs {
+    const float* b; int b_pitch; long long b_tstride;   // input image(s)
+    const TileT* tiles;                                 // valid rect per tile (nullable: whole H x W)
+    int H, W;                                           // when tiles == nullptr
+    int RB, WP;                                         // rows per CTA, smem row pitch
+    float lam; int nfgp;
+    int mode;                                           // 0: out = x; 1: FISTA epilogue
+    float* out; int out_pitch; long long out_tstride;
+    // FISTA epilogue (mode 1)
+    const float* xs; float* xprev; long long p_tstride; int T;
+    float* y; float* yT; long long y_tstride; int TP;
+    float beta_o;
+};
+
+__device__ __forceinline__ float clip1(float v) { return fminf(1.f, fmaxf(-1.f, v)); }
+
+__global__ void __launch_bounds__(256) k_fgp(FgpArgs A) {
+    extern __shared__ float sm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int K = (int)cl.num_blocks();
+    const int kr = (int)cl.block_rank();
+    const int tile = blockIdx.y;
+    int vr0 = 0, vc0 = 0, Hv = A.H, Wv = A.W;
+    if (A.tiles) {
+        const TileT ti = A.tiles[tile];
+        vr0 = ti.vr0; vc0 = ti.vc0; Hv = ti.vr1 - ti.vr0; Wv = ti.vc1 - ti.vc0;
+    }
+    const int RB = A.RB, WP = A.WP;
+    const int i0 = kr * RB;
+    const int nrows = max(0, min(Hv, i0 + RB) - i0);
+    float* sb = sm;
+    float* sr = sb + RB * WP;
+    float* ss = sr + RB * WP;
+    float* spo = ss + RB * WP;
+    float* sqo = spo + RB * WP;
+    float* sz = sqo + RB * WP;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // blockDim (32, 8)
+    const float lam = A.lam;
+
+    for (int li = ty; li < RB; li += 8)
+        for (int j = tx; j < WP; j += 32) {
+            const int o = li * WP + j;
+            float bv = 0.f;
+            if (li < nrows && j < Wv)
+                bv = A.b[(long long)tile * A.b_tstride + (long long)(vr0 + i0 + li) * A.b_pitch + vc0 + j];
+            sb[o] = bv; sr[o] = 0.f; ss[o] = 0.f; spo[o] = 0.f; sqo[o] = 0.f; sz[o] = 0.f;
+        }
+    cl.sync();
+    const float* prev_r = kr > 0 ? cl.map_shared_rank(sr, kr - 1) : nullptr;
+    const float* prev_po = kr > 0 ? cl.map_shared_rank(spo, kr - 1) : nullptr;
+    const float* next_z = kr + 1 < K ? cl.map_shared_rank(sz, kr + 1) : nullptr;
+    const int next_rows = max(0, min(Hv, i0 + 2 * RB) - (i0 + RB));
+
+    const float gam = lam > 0.f ? 1.f / (8.f * lam) : 0.f;
+    const int nit = lam > 0.f ? A.nfgp : 0;
+    double tk = 1.0;
+    for (int it = 0; it < nit; ++it) {
+        // phase A: z = b - lam L(r, s)
+        for (int li = ty; li < nrows; li += 8) {
+            const int i = i0 + li;
+            for (int j = tx; j < Wv; j += 32) {
+                const int o = li * WP + j;
+                float rup = 0.f;
+                if (li > 0) rup = sr[o - WP];
+                else if (i > 0) rup = prev_r[(RB - 1) * WP + j];
+                const float sl = j > 0 ? ss[o - 1] : 0.f;
+                sz[o] = sb[o] - lam * (sr[o] + ss[o] - rup - sl);
+            }
+        }
+        cl.sync();
+        // phase B: dual step, projection, momentum
+        const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tk * tk));
+        const float beta = (float)((tk - 1.0) / tn);
+        tk = tn;
+        for (int li = ty; li < nrows; li += 8) {
+            const int i = i0 + li;
+            for (int j = tx; j < Wv; j += 32) {
+                const int o = li * WP + j;
+                const float zc = sz[o];
+                float pn = 0.f, qn = 0.f;
+                if (i < Hv - 1) {
+                    const float zd = (li + 1 < nrows) ? sz[o + WP] : next_z[j];
+                    pn = clip1(sr[o] + gam * (zc - zd));
+                }
+                if (j < Wv - 1) qn = clip1(ss[o] + gam * (zc - sz[o + 1]));
+                sr[o] = pn + beta * (pn - spo[o]);
+                ss[o] = qn + beta * (qn - sqo[o]);
+                spo[o] = pn;
+                sqo[o] = qn;
+            }
+        }
+        cl.sync();
+    }
+    (void)next_rows;
+    // x = b - lam L(p, q), then the epilogue
+    for (int li = ty; li < nrows; li += 8) {
+        const int i = i0 + li;
+        for (int j = tx; j < Wv; j += 32) {
+            const int o = li * WP + j;
+            float pup = 0.f;
+            if (li > 0) pup = spo[o - WP];
+            else if (i > 0) pup = prev_po[(RB - 1) * WP + j];
+            const float ql = j > 0 ? sqo[o - 1] : 0.f;
+            const float x = sb[o] - lam * (spo[o] + sqo[o] - pup - ql);
+            if (A.mode == 0) {
+                A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + j] = x;
+            } else {
+                const int ti_ = vr0 + i, tj = vc0 + j;                 // tile-local coords
+                const long long pl = (long long)tile * A.p_tstride + (long long)ti_ * A.T + tj;
+                const float xp = A.xprev[pl];
+                const float rr = x + A.beta_o * (x - xp);             // FISTA extrapolation (A12)
+                const float yv = rr - A.xs[pl];                         // x_L^k = r - x_s^k
+                A.xprev[pl] = x;
+                A.y[(long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + tj] = yv;
+                A.yT[(long long)tile * A.y_tstride + (long long)tj * A.TP + PADL + ti_] = yv;
+            }
+        }
+    }
+    cl.sync();   // keep shared memory alive until every neighbour has read its halo
+}
+
+// ---------------------------------------------------------------------------
+// Convolution cache b_k = C_{u_k} p_c, direct form
+//   b_k(a,d) = sum_j u_k(a,j) p_c(a, d - j + d_c)
+// CTA = (angle a, 8 consecutive k, 256 consecutive d); thread = one d, 8 k.
+// Products in fp32, each 512-tap chunk summed in fp32 and added into an fp64
+// accumulator (bounds the fp32 error of the N_d-long sums).
+// ---------------------------------------------------------------------------
+constexpr int CV_KB = 8, CV_DB = 256, CV_JB = 512;
+
+__global__ void __launch_bounds__(256) k_conv(int na, int nd, int nk, const float* __restrict__ bank,
+                                              const float* __restrict__ pc, float* __restrict__ outb) {
+    __shared__ float4 su[CV_JB][CV_KB / 4];
+    __shared__ float sp[CV_DB + CV_JB];
+    const int a = blockIdx.y;
+    const int k0 = blockIdx.z * CV_KB;
+    const int d0 = blockIdx.x * CV_DB;
+    const int dcen = (nd - 1) / 2;
+    const int d = d0 + threadIdx.x;
+    double accd[CV_KB];
+    #pragma unroll
+    for (int q = 0; q < CV_KB; ++q) accd[q] = 0.0;
+    for (int j0 = 0; j0 < nd; j0 += CV_JB) {
+        __syncthreads();
+        for (int el = threadIdx.x; el < CV_JB * CV_KB; el += blockDim.x) {
+            const int jj = el % CV_JB, q = el / CV_JB;
+            const int j = j0 + jj, k = k0 + q;
+            float v = 0.f;
+            if (j < nd && k < nk) v = bank[((long long)k * na + a) * nd + j];
+            reinterpret_cast<float*>(&su[jj][0])[q] = v;
+        }
+        // p index m = d - j + dcen, for d in [d0, d0+DB), j in [j0, j0+JB):
+        // m in (d0 - j0 - JB + dcen, d0 - j0 + DB - 1 + dcen]; store sp[x] = p[mbase + x]
+        const int mbase = d0 - j0 - CV_JB + 1 + dcen;
+        for (int x = threadIdx.x; x < CV_DB + CV_JB; x += blockDim.x) {
+            const int m = mbase + x;
+            sp[x] = (m >= 0 && m < nd) ? pc[(long long)a * nd + m] : 0.f;
+        }
+        __syncthreads();
+        float acc[CV_KB];
+        #pragma unroll
+        for (int q = 0; q < CV_KB; ++q) acc[q] = 0.f;
+        const int jn = min(CV_JB, nd - j0);
+        // m - mbase = (d - j + dcen) - mbase = threadIdx.x + (JB - 1) - jj
+        const float* pp = sp + threadIdx.x + CV_JB - 1;
+        #pragma unroll 4
+        for (int jj = 0; jj < jn; ++jj) {
+            const float pv = pp[-jj];
+            const float4 u0 = su[jj][0], u1 = su[jj][1];
+            acc[0] = fmaf(u0.x, pv, acc[0]); acc[1] = fmaf(u0.y, pv, acc[1]);
+            acc[2] = fmaf(u0.z, pv, acc[2]); acc[3] = fmaf(u0.w, pv, acc[3]);
+            acc[4] = fmaf(u1.x, pv, acc[4]); acc[5] = fmaf(u1.y, pv, acc[5]);
+            acc[6] = fmaf(u1.z, pv, acc[6]); acc[7] = fmaf(u1.w, pv, acc[7]);
+        }
+        #pragma unroll
+        for (int q = 0; q < CV_KB; ++q) accd[q] += (double)acc[q];
+    }
+    if (d < nd) {
+        #pragma unroll
+        for (int q = 0; q < CV_KB; ++q)
+            if (k0 + q < nk) outb[((long long)(k0 + q) * na + a) * nd + d] = (float)accd[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Small kernels: disc raster, zero-frequency sums, disc gray value, p_c,
+// image (un)packing, crop, extended-ROI export, stitch.
+// ---------------------------------------------------------------------------
+// padded image + twin from a plain N x N image (src nullable: disc raster D)
+__global__ void k_pack(int n, int TP, const float* __restrict__ src, int disc, float* __restrict__ img,
+                       float* __restrict__ imgT) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    float v;
+    if (disc) {
+        const int u = 2 * j - n + 1, w = 2 * i - n + 1;
+        v = (u * u + w * w <= n * n) ? 1.f : 0.f;
+    } else {
+        v = src[(long long)i * n + j];
+    }
+    img[(long long)i * TP + PADL + j] = v;
+    imgT[(long long)j * TP + PADL + i] = v;
+}
+
+// one block per angle: fixed-order fp64 reduction of a sinogram row
+__global__ void k_rowsum(int nd, const float* __restrict__ s, double* __restrict__ out) {
+    __shared__ double red[256];
+    const int a = blockIdx.x;
+    double acc = 0.0;
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) acc += (double)s[(long long)a * nd + d];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[a] = red[0];
+}
+
+// c = sum_a P_a D_a / sum_a D_a^2  (least squares on the zero-frequency components)
+__global__ void k_discc(int na, const double* __restrict__ P, const double* __restrict__ D,
+                        double* __restrict__ c64, float* __restrict__ c32, float* __restrict__ cuser, int* err) {
+    __shared__ double rn[256], rd[256];
+    double num = 0.0, den = 0.0;
+    for (int a = threadIdx.x; a < na; a += blockDim.x) { num += P[a] * D[a]; den += D[a] * D[a]; }
+    rn[threadIdx.x] = num; rd[threadIdx.x] = den;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+        if (threadIdx.x < st) { rn[threadIdx.x] += rn[threadIdx.x + st]; rd[threadIdx.x] += rd[threadIdx.x + st]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double c = rd[0] > 0.0 ? rn[0] / rd[0] : 0.0;
+        *c64 = c; *c32 = (float)c;
+        if (cuser) *cuser = (float)c;
+        if (!(rd[0] > 0.0)) *err = 1;
+    }
+}
+
+__global__ void k_pc(long long ne, const float* __restrict__ p, const float* __restrict__ wd,
+                     const double* __restrict__ c64, float* __restrict__ pc) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < ne) pc[e] = (float)((double)p[e] - *c64 * (double)wd[e]);
+}
+
+// core crop: cores[r][i][j] = src[r][(m+i)][(m+j)] (src padded or plain)
+__global__ void k_crop(int side, int m, const float* __restrict__ src, long long s_tstride, int s_pitch,
+                       int s_off, float* __restrict__ cores) {
+    const int r = blockIdx.z;
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= side || j >= side) return;
+    cores[((long long)r * side + i) * side + j] =
+        src[(long long)r * s_tstride + (long long)(m + i) * s_pitch + s_off + m + j];
+}
+
+// extended export: ext[r][i][j] = src[r][vr0+i][vc0+j] for the valid rect, 0 elsewhere
+__global__ void k_ext(int E, const TileT* tiles, const float* __restrict__ src, long long s_tstride,
+                      int s_pitch, int s_off, float* __restrict__ ext) {
+    const int r = blockIdx.z;
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= E || j >= E) return;
+    const TileT ti = tiles[r];
+    float v = 0.f;
+    if (i < ti.vr1 - ti.vr0 && j < ti.vc1 - ti.vc0)
+        v = src[(long long)r * s_tstride + (long long)(ti.vr0 + i) * s_pitch + s_off + ti.vc0 + j];
+    ext[((long long)r * E + i) * E + j] = v;
+}
+
+// ROI extraction for lt_project(roi): padded tile + twin of M_{L'} x
+__global__ void k_extract(int n, int T, int TP, TileT ti, const float* __restrict__ img,
+                          float* __restrict__ t, float* __restrict__ tT) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= T || j >= T) return;
+    const bool valid = i >= ti.vr0 && i < ti.vr1 && j >= ti.vc0 && j < ti.vc1;
+    const float v = valid ? img[(long long)(ti.row0 + i) * n + ti.col0 + j] : 0.f;
+    t[(long long)i * TP + PADL + j] = v;
+    tT[(long long)j * TP + PADL + i] = v;
+}
+
+// window -> full sinogram (zero outside the window)
+__global__ void k_scatter_win(int na, int nd, int Wwin, const int* __restrict__ d0,
+                              const float* __restrict__ win, float* __restrict__ sino) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x, a = blockIdx.y;
+    if (d >= nd) return;
+    const int w = d - d0[a];
+    sino[(long long)a * nd + d] = (w >= 0 && w < Wwin) ? win[(long long)a * Wwin + w] : 0.f;
+}
+
+// combine: CTA per 32x32 image block, fixed ascending-ROI order (A19)
+__global__ void k_stitch(int n, int side, int nbx, const int* __restrict__ lst_off, const int* __restrict__ lst,
+                         const int* __restrict__ slot_r0, const int* __restrict__ slot_c0,
+                         const float* __restrict__ cores, float* __restrict__ img) {
+    const int bx = blockIdx.x % nbx, by = blockIdx.x / nbx;
+    const int j = bx * 32 + threadIdx.x;
+    const int beg = lst_off[blockIdx.x], end = lst_off[blockIdx.x + 1];
+    for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
+        const int i = by * 32 + ii;
+        if (i >= n || j >= n) continue;
+        float sum = 0.f; int cnt = 0;
+        for (int q = beg; q < end; ++q) {
+            const int s = lst[q];
+            const int li = i - slot_r0[s], lj = j - slot_c0[s];
+            if (li >= 0 && li < side && lj >= 0 && lj < side) {
+                sum += cores[((long long)s * side + li) * side + lj];
+                ++cnt;
+            }
+        }
+        img[(long long)i * n + j] = cnt ? sum / (float)cnt : 0.f;
+    }
+}
+
+// global FGP (a10 FISTA-TV on the full grid): one launch per phase, state in HBM
+__global__ void k_gfgp_z(int n, float lam, const float* __restrict__ b, const float* __restrict__ r,
+                         const float* __restrict__ s, float* __restrict__ z) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const long long o = (long long)i * n + j;
+    const float rup = i > 0 ? r[o - n] : 0.f, sl = j > 0 ? s[o - 1] : 0.f;
+    z[o] = b[o] - lam * (r[o] + s[o] - rup - sl);
+}
+__global__ void k_gfgp_dual(int n, float gam, float beta, const float* __restrict__ z, float* __restrict__ r,
+                            float* __restrict__ s, float* __restrict__ po, float* __restrict__ qo) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const long long o = (long long)i * n + j;
+    const float zc = z[o];
+    const float pn = i < n - 1 ? clip1(r[o] + gam * (zc - z[o + n])) : 0.f;
+    const float qn = j < n - 1 ? clip1(s[o] + gam * (zc - z[o + 1])) : 0.f;
+    r[o] = pn + beta * (pn - po[o]); s[o] = qn + beta * (qn - qo[o]);
+    po[o] = pn; qo[o] = qn;
+}
+__global__ void k_gfgp_out(int n, float lam, float beta_o, const float* __restrict__ b,
+                           const float* __restrict__ po, const float* __restrict__ qo,
+                           float* __restrict__ xprev, float* __restrict__ rm, float* __restrict__ rmT, int TP) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const long long o = (long long)i * n + j;
+    const float pup = i > 0 ? po[o - n] : 0.f, ql = j > 0 ? qo[o - 1] : 0.f;
+    const float x = b[o] - lam * (po[o] + qo[o] - pup - ql);
+    const float r = x + beta_o * (x - xprev[o]);
+    xprev[o] = x;
+    rm[(long long)i * TP + PADL + j] = r;
+    rmT[(long long)j * TP + PADL + i] = r;
+}
+
+__global__ void k_unpack(int n, int TP, const float* __restrict__ img, float* __restrict__ out) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    out[(long long)i * n + j] = img[(long long)i * TP + PADL + j];
+}
+
+__global__ void k_impulse(int n, int TP, float* img, float* imgT) {
+    // e_c (A5): 2x2 average of the central pixels for even N, centre pixel for odd N
+    if (threadIdx.x != 0) return;
+    if (n % 2) {
+        const int m = n / 2;
+        img[(long long)m * TP + PADL + m] = 1.f; imgT[(long long)m * TP + PADL + m] = 1.f;
+    } else {
+        const int m = n / 2;
+        for (int di = -1; di <= 0; ++di)
+            for (int dj = -1; dj <= 0; ++dj) {
+                img[(long long)(m + di) * TP + PADL + m + dj] = 0.25f;
+                imgT[(long long)(m + dj) * TP + PADL + m + di] = 0.25f;
+            }
+    }
+}
+
+}  // namespace lt

@@ -1,0 +1,800 @@
+// loctomo.cu -- C-ABI (include/loctomo.h), host planner and launch logic of
+// the B200-native local tomography library (arXiv 1604.02292).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared.
+#include "loctomo.h"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace lt;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define LT_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) return fail(LT_ERR_RUNTIME, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LT_LAUNCHED()                                                                     \
+    do {                                                                                  \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                               \
+        cudaError_t e_ = cudaGetLastError();                                              \
+        if (e_ != cudaSuccess) return fail(LT_ERR_RUNTIME, "launch: %s", cudaGetErrorString(e_)); \
+    } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct lt_plan {
+    int n = 0, na = 0, nd = 0, nroi_all = 0, radius = 0, margin = 0, h = 0;
+    int T = 0, TP = 0, Wwin = 0, n_iter = 0, flags = 0, rank = 0, world = 1;
+    int GT = 0, GTP = 0;          // global tile (whole image)
+    double alpha = 0.0;
+    std::vector<double> ang;
+    std::vector<int> cen;         // [nroi_all][2]
+    std::vector<int> local;       // global ROI indices on this rank (ascending)
+    int R = 0;
+    // host tables
+    std::vector<AngF> angf;
+    std::vector<double> cs64, sn64, A64, B64;
+    std::vector<TileT> tiles, gtile;
+    std::vector<int> d0, gd0;
+    std::vector<double> tauc, gtauc;
+    // workspace
+    char* ws = nullptr;
+    int64_t ws_bytes = 0;
+    bool bound = false, bank_ready = false, wd_ready = false;
+    int last_mode = -1;
+    int stitch_cap = 0;           // max list entries
+    struct {
+        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc;
+        size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
+        size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
+        size_t y, yT, s, v, xs, xprev;
+        size_t tt, ttT, tw;
+        size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
+        size_t total;
+    } off{};
+
+    template <class X> X* P(size_t o) const { return reinterpret_cast<X*>(ws + o); }
+    Geo geo() const {
+        return Geo{n, na, nd, P<AngF>(off.angf), P<double>(off.cs64), P<double>(off.sn64),
+                   P<double>(off.A64), P<double>(off.B64)};
+    }
+    Tiles roi_tiles() const { return Tiles{T, TP, Wwin, R, P<TileT>(off.tiles), P<int>(off.d0), P<double>(off.tauc)}; }
+    Tiles glob_tiles() const { return Tiles{GT, GTP, nd, 1, P<TileT>(off.gtile), P<int>(off.gd0), P<double>(off.gtauc)}; }
+    long long ytile() const { return (long long)T * TP; }
+    long long ptile() const { return (long long)T * T; }
+};
+
+namespace {
+
+int window_width(int h) {
+    // W(h) = 2 ceil((2h-1)/sqrt2) + 4 (V4): covers the support of every
+    // pixel of a 2h x 2h tile at every angle.
+    return 2 * (int)std::ceil((2.0 * h - 1.0) / std::sqrt(2.0) - 1e-12) + 4;
+}
+
+void tile_window(const lt_plan& p, double cx, double cy, int Wwin, int* d0_out, double* tauc_out) {
+    // cx, cy: coordinates of the tile centre point; tau = x cos + y sin + (N_d-1)/2
+    for (int a = 0; a < p.na; ++a) {
+        const double tau = cx * p.cs64[a] + cy * p.sn64[a] + 0.5 * (p.nd - 1);
+        const int d0 = (int)std::floor(tau) - Wwin / 2;
+        d0_out[a] = d0;
+        tauc_out[a] = tau - d0;
+    }
+}
+
+int check_plan(const lt_plan* p) {
+    if (!p) return fail(LT_ERR_INVALID, "null plan");
+    if (!p->bound) return fail(LT_ERR_INVALID, "workspace not bound");
+    return LT_OK;
+}
+
+// ---- launch helpers -------------------------------------------------------
+int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, const float* imgT, long long img_ts,
+              float* out, long long out_ts, const float* aux_in, float* aux_out, cudaStream_t st) {
+    FpArgs f{img, imgT, img_ts, out, out_ts, aux_in, aux_out, (float)p.alpha};
+    dim3 grid((t.Wwin + 127) / 128, p.na, t.ntiles);
+    if (mode == 0) k_fp<0><<<grid, 128, 0, st>>>(p.geo(), t, f);
+    else if (mode == 1) k_fp<1><<<grid, 128, 0, st>>>(p.geo(), t, f);
+    else k_fp<2><<<grid, 128, 0, st>>>(p.geo(), t, f);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+template <int NS, int MODE>
+int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const SinoView& s2, const BpEpi& e,
+                cudaStream_t st) {
+    const int nsx = (t.T + 31) / 32;
+    dim3 grid(nsx * nsx, t.ntiles);
+    k_bp<NS, MODE><<<grid, 256, 0, st>>>(p.geo(), t, s1, s2, e);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+BpEpi epi0() {
+    BpEpi e;
+    memset(&e, 0, sizeof e);
+    e.hi = INFINITY;
+    e.lo = -INFINITY;
+    return e;
+}
+
+SinoView view_full(const float* base, int nd, long long tile_stride = 0) {
+    return SinoView{base, tile_stride, nd, 1, nd};
+}
+SinoView view_win(const float* base, int Wwin, int na) {
+    return SinoView{base, (long long)na * Wwin, Wwin, 0, Wwin};
+}
+
+// FGP cluster configuration: K CTAs, RB rows each, pitch WP, 6 arrays in smem
+int fgp_config(int rows, int cols, int* K, int* RB, int* WP, size_t* smem) {
+    const int wp = cols;
+    for (int k = 1; k <= 16; k *= 2) {
+        const int rb = (rows + k - 1) / k;
+        const size_t bytes = (size_t)6 * rb * wp * sizeof(float);
+        if (bytes <= 200 * 1024) {
+            *K = k; *RB = rb; *WP = wp; *smem = bytes;
+            return LT_OK;
+        }
+    }
+    return fail(LT_ERR_INVALID, "FGP tile %dx%d too large for a 16-CTA cluster", rows, cols);
+}
+
+int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
+    int K, RB, WP;
+    size_t smem;
+    if (int rc = fgp_config(rows, cols, &K, &RB, &WP, &smem)) return rc;
+    A.RB = RB;
+    A.WP = WP;
+    LT_CUDA(cudaFuncSetAttribute(k_fgp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (K > 8) LT_CUDA(cudaFuncSetAttribute(k_fgp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(K, ntiles, 1);
+    cfg.blockDim = dim3(32, 8, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LT_CUDA(cudaLaunchKernelEx(&cfg, k_fgp, A));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+dim3 grid2d(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }
+
+// W D and its zero-frequency sums (geometry only, cached)
+int ensure_wd(lt_plan& p, cudaStream_t st) {
+    if (p.wd_ready) return LT_OK;
+    float* gi = p.P<float>(p.off.gimg);
+    float* giT = p.P<float>(p.off.gimgT);
+    const size_t gbytes = (size_t)p.GT * p.GTP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(gi, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(giT, 0, gbytes, st));
+    k_pack<<<grid2d(p.n, p.n), dim3(32, 8), 0, st>>>(p.n, p.GTP, nullptr, 1, gi, giT);
+    LT_LAUNCHED();
+    if (int rc = launch_fp(p, 0, p.glob_tiles(), gi, giT, 0, p.P<float>(p.off.wd), 0, nullptr, nullptr, st)) return rc;
+    k_rowsum<<<p.na, 256, 0, st>>>(p.nd, p.P<float>(p.off.wd), p.P<double>(p.off.wdsum));
+    LT_LAUNCHED();
+    p.wd_ready = true;
+    return LT_OK;
+}
+
+int disc_correct(lt_plan& p, const float* d_sino, float* d_pc, float* d_cuser, cudaStream_t st) {
+    if (int rc = ensure_wd(p, st)) return rc;
+    k_rowsum<<<p.na, 256, 0, st>>>(p.nd, d_sino, p.P<double>(p.off.psum));
+    LT_LAUNCHED();
+    k_discc<<<1, 256, 0, st>>>(p.na, p.P<double>(p.off.psum), p.P<double>(p.off.wdsum), p.P<double>(p.off.discc64),
+                               p.P<float>(p.off.discc32), d_cuser, p.P<int>(p.off.err));
+    LT_LAUNCHED();
+    const long long ne = (long long)p.na * p.nd;
+    k_pc<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(ne, d_sino, p.P<float>(p.off.wd), p.P<double>(p.off.discc64), d_pc);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
+    if (!p.bank_ready) return fail(LT_ERR_INVALID, "filter bank not computed (lt_filter_bank / lt_set_bank)");
+    dim3 grid((p.nd + CV_DB - 1) / CV_DB, p.na, (p.n_iter + CV_KB - 1) / CV_KB);
+    k_conv<<<grid, 256, 0, st>>>(p.na, p.nd, p.n_iter, p.P<float>(p.off.bank), d_pc, p.P<float>(p.off.conv));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+// the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
+int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st) {
+    const Tiles t = p.roi_tiles();
+    const long long yts = p.ytile();
+    float* y = p.P<float>(p.off.y);
+    float* yT = p.P<float>(p.off.yT);
+    float* s = p.P<float>(p.off.s);
+    LT_CUDA(cudaMemsetAsync(y, 0, (size_t)p.R * yts * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(yT, 0, (size_t)p.R * yts * sizeof(float), st));
+    if (mode == 1) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
+    const long long ns = (long long)p.na * p.nd;
+    const bool disc = (p.flags & LT_DISC_ON) != 0;
+    double tk = 1.0;
+    for (int k = 0; k < p.n_iter; ++k) {
+        const float* bk = p.P<float>(p.off.conv) + (long long)k * ns;
+        BpEpi e = epi0();
+        e.y = y; e.yT = yT; e.y_tstride = yts;
+        e.v = p.P<float>(p.off.v); e.xs = p.P<float>(p.off.xs); e.p_tstride = p.ptile();
+        e.discc = p.P<float>(p.off.discc32); e.use_disc = disc;
+        e.alpha = (float)p.alpha; e.lo = lo; e.hi = hi; e.last = (k == p.n_iter - 1);
+        const SinoView vb = view_full(bk, p.nd);
+        if (k == 0) {
+            // y^0 = 0: W_{L'} y^0 = 0, single-sinogram gather
+            if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vb, vb, e, st)) return rc; }
+            else { if (int rc = launch_bp_t<1, BP_TV>(p, t, vb, vb, e, st)) return rc; }
+        } else {
+            if (int rc = launch_fp(p, 0, t, y, yT, yts, s, (long long)p.na * p.Wwin, nullptr, nullptr, st)) return rc;
+            const SinoView vs = view_win(s, p.Wwin, p.na);
+            if (mode == 0) { if (int rc = launch_bp_t<2, BP_BOX>(p, t, vb, vs, e, st)) return rc; }
+            else { if (int rc = launch_bp_t<2, BP_TV>(p, t, vb, vs, e, st)) return rc; }
+        }
+        if (mode == 1) {
+            const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
+            const double beta = (tk - 1.0) / tn;
+            tk = tn;
+            FgpArgs A;
+            memset(&A, 0, sizeof A);
+            A.b = p.P<float>(p.off.v); A.b_pitch = p.T; A.b_tstride = p.ptile();
+            A.tiles = p.P<TileT>(p.off.tiles);
+            A.lam = lam; A.nfgp = nfgp; A.mode = 1;
+            A.xs = p.P<float>(p.off.xs); A.xprev = p.P<float>(p.off.xprev); A.p_tstride = p.ptile(); A.T = p.T;
+            A.y = y; A.yT = yT; A.y_tstride = yts; A.TP = p.TP;
+            A.beta_o = (float)beta;
+            if (int rc = launch_fgp(A, p.T, p.T, p.R, st)) return rc;
+        }
+    }
+    p.last_mode = mode;
+    return LT_OK;
+}
+
+int crop_cores(lt_plan& p, float* d_cores, cudaStream_t st) {
+    const int side = 2 * p.radius;
+    dim3 grid((side + 31) / 32, (side + 7) / 8, p.R);
+    if (p.last_mode == 0)
+        k_crop<<<grid, dim3(32, 8), 0, st>>>(side, p.margin, p.P<float>(p.off.y), p.ytile(), p.TP, PADL, d_cores);
+    else
+        k_crop<<<grid, dim3(32, 8), 0, st>>>(side, p.margin, p.P<float>(p.off.xprev), p.ptile(), p.T, 0, d_cores);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfgp, float* d_cores, cudaStream_t st) {
+    float* pc = p.P<float>(p.off.pc);
+    if (p.flags & LT_DISC_ON) {
+        if (int rc = disc_correct(p, d_sino, pc, nullptr, st)) return rc;
+    } else {
+        LT_CUDA(cudaMemcpyAsync(pc, d_sino, (size_t)p.na * p.nd * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.discc32), 0, sizeof(float), st));
+    }
+    if (int rc = conv_cache(p, pc, st)) return rc;
+    if (int rc = local_iterations(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode == 1 ? a0 : 0.f, nfgp, st))
+        return rc;
+    return crop_cores(p, d_cores, st);
+}
+
+int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot_roi, float* d_image, cudaStream_t st) {
+    const int side = 2 * p.radius;
+    const int nb = (p.n + 31) / 32;
+    std::vector<std::vector<std::pair<int, int>>> buckets((size_t)nb * nb);
+    std::vector<int> r0(std::max(n_slots, 1)), c0(std::max(n_slots, 1));
+    for (int s = 0; s < n_slots; ++s) {
+        const int g = slot_roi[s];
+        if (g < -1 || g >= p.nroi_all) return fail(LT_ERR_INVALID, "slot %d: bad ROI index %d", s, g);
+        if (g < 0) { r0[s] = c0[s] = -1000000; continue; }
+        r0[s] = p.cen[2 * g] - p.radius;
+        c0[s] = p.cen[2 * g + 1] - p.radius;
+        for (int by = r0[s] / 32; by <= (r0[s] + side - 1) / 32; ++by)
+            for (int bx = c0[s] / 32; bx <= (c0[s] + side - 1) / 32; ++bx) buckets[(size_t)by * nb + bx].push_back({g, s});
+    }
+    std::vector<int> offs(1, 0), lst;
+    for (auto& b : buckets) {
+        std::sort(b.begin(), b.end());
+        for (auto& e : b) lst.push_back(e.second);
+        offs.push_back((int)lst.size());
+    }
+    if ((int)lst.size() > p.stitch_cap || n_slots > p.nroi_all * std::max(1, p.world))
+        return fail(LT_ERR_INVALID, "combine: %zu list entries / %d slots exceed the plan's capacity", lst.size(), n_slots);
+    // tables live in the workspace (stream-ordered upload from pageable host memory)
+    int* d_off = p.P<int>(p.off.st_off);
+    int* d_lst = p.P<int>(p.off.st_lst);
+    int* d_r0 = p.P<int>(p.off.st_r0);
+    int* d_c0 = p.P<int>(p.off.st_c0);
+    LT_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!lst.empty()) LT_CUDA(cudaMemcpyAsync(d_lst, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(d_r0, r0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(d_c0, c0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
+    k_stitch<<<nb * nb, dim3(32, 8), 0, st>>>(p.n, side, nb, d_off, d_lst, d_r0, d_c0, d_cores, d_image);
+    LT_LAUNCHED();
+    // pageable copies above are staged synchronously by the driver before returning
+    return LT_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+extern "C" {
+
+const char* lt_last_error(void) { return g_err.c_str(); }
+int64_t lt_launch_count(void) { return g_launches.load(); }
+
+int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angles, int32_t n_roi,
+                 const int32_t* center_row, const int32_t* center_col, int32_t radius, int32_t margin,
+                 int32_t n_iter, int32_t flags, int32_t rank, int32_t world, lt_plan** out) {
+    if (!out) return fail(LT_ERR_INVALID, "out is null");
+    *out = nullptr;
+    if (n < 1 || n_angles < 1 || n_det < 1) return fail(LT_ERR_INVALID, "N, N_theta, N_d must be >= 1");
+    if (n_det % 2 == 0) return fail(LT_ERR_INVALID, "N_d must be odd (filter centring)");
+    if (!angles) return fail(LT_ERR_INVALID, "angles is null");
+    for (int a = 0; a < n_angles; ++a) {
+        if (!(angles[a] >= 0.0 && angles[a] < M_PI)) return fail(LT_ERR_INVALID, "angle %d outside [0, pi)", a);
+        if (a && !(angles[a] > angles[a - 1])) return fail(LT_ERR_INVALID, "angles not strictly increasing at %d", a);
+    }
+    if (n_roi < 0 || (n_roi > 0 && (!center_row || !center_col))) return fail(LT_ERR_INVALID, "bad ROI list");
+    if (radius < 1 || margin < 0 || n_iter < 1) return fail(LT_ERR_INVALID, "radius >= 1, margin >= 0, n_iter >= 1");
+    if (world < 1 || rank < 0 || rank >= world) return fail(LT_ERR_INVALID, "bad rank/world");
+    for (int r = 0; r < n_roi; ++r)
+        if (center_row[r] - radius < 0 || center_col[r] - radius < 0 || center_row[r] + radius > n ||
+            center_col[r] + radius > n)
+            return fail(LT_ERR_INVALID, "ROI %d core outside the grid", r);
+    lt_plan* p = new lt_plan();
+    p->n = n; p->na = n_angles; p->nd = n_det; p->nroi_all = n_roi; p->radius = radius; p->margin = margin;
+    p->h = radius + margin; p->T = 2 * p->h; p->TP = p->T + PADL + PADR;
+    p->Wwin = window_width(p->h);
+    p->n_iter = n_iter; p->flags = flags; p->rank = rank; p->world = world;
+    p->GT = n; p->GTP = n + PADL + PADR;
+    p->alpha = 1.0 / ((double)n_angles * n_det);
+    p->ang.assign(angles, angles + n_angles);
+    p->cen.resize(2 * (size_t)n_roi);
+    for (int r = 0; r < n_roi; ++r) { p->cen[2 * r] = center_row[r]; p->cen[2 * r + 1] = center_col[r]; }
+    // per-angle tables
+    p->angf.resize(n_angles); p->cs64.resize(n_angles); p->sn64.resize(n_angles);
+    p->A64.resize(n_angles); p->B64.resize(n_angles);
+    for (int a = 0; a < n_angles; ++a) {
+        const double cs = std::cos(angles[a]), sn = std::sin(angles[a]);
+        const double c = std::max(std::fabs(cs), std::fabs(sn));
+        const bool col = std::fabs(sn) > std::fabs(cs);
+        const double A = col ? -1.0 / sn : 1.0 / cs;
+        const double B = col ? cs / sn : sn / cs;
+        p->cs64[a] = cs; p->sn64[a] = sn; p->A64[a] = A; p->B64[a] = B;
+        AngF f;
+        f.cs = (float)cs; f.sn = (float)sn; f.invc = (float)(1.0 / c); f.ic2 = (float)(1.0 / (c * c));
+        f.K = (float)(1.0 / c - 0.5 / (c * c)); f.A = (float)A; f.B = (float)B; f.col = col ? 1 : 0;
+        p->angf[a] = f;
+    }
+    // partition: longest-processing-time over valid extended pixel counts, ties by index
+    std::vector<long long> cost(n_roi);
+    for (int r = 0; r < n_roi; ++r) {
+        const int cr = p->cen[2 * r], cc = p->cen[2 * r + 1], h = p->h;
+        const long long hv = std::min(n, cr + h) - std::max(0, cr - h);
+        const long long wv = std::min(n, cc + h) - std::max(0, cc - h);
+        cost[r] = hv * wv;
+    }
+    std::vector<int> order(n_roi);
+    for (int r = 0; r < n_roi; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    std::vector<long long> load(world, 0);
+    std::vector<int> owner(n_roi, 0);
+    for (int r : order) {
+        int best = 0;
+        for (int g = 1; g < world; ++g)
+            if (load[g] < load[best]) best = g;
+        owner[r] = best;
+        load[best] += cost[r];
+    }
+    for (int r = 0; r < n_roi; ++r)
+        if (owner[r] == rank) p->local.push_back(r);
+    p->R = (int)p->local.size();
+    // ROI tiles and windows
+    p->tiles.resize(std::max(p->R, 1));
+    p->d0.resize((size_t)std::max(p->R, 1) * n_angles);
+    p->tauc.resize((size_t)std::max(p->R, 1) * n_angles);
+    for (int q = 0; q < p->R; ++q) {
+        const int g = p->local[q];
+        const int cr = p->cen[2 * g], cc = p->cen[2 * g + 1], h = p->h;
+        TileT t;
+        t.row0 = cr - h; t.col0 = cc - h;
+        t.vr0 = std::max(0, -t.row0); t.vr1 = std::min(p->T, n - t.row0);
+        t.vc0 = std::max(0, -t.col0); t.vc1 = std::min(p->T, n - t.col0);
+        t.pad0 = t.pad1 = 0;
+        p->tiles[q] = t;
+        // tile centre point (x, y) = (cc - N/2, N/2 - cr)
+        tile_window(*p, cc - 0.5 * n, 0.5 * n - cr, p->Wwin, &p->d0[(size_t)q * n_angles], &p->tauc[(size_t)q * n_angles]);
+    }
+    // global tile: the whole grid, window = the full detector
+    {
+        TileT t;
+        t.row0 = 0; t.col0 = 0; t.vr0 = 0; t.vr1 = n; t.vc0 = 0; t.vc1 = n; t.pad0 = t.pad1 = 0;
+        p->gtile.assign(1, t);
+        p->gd0.assign(n_angles, 0);
+        p->gtauc.assign(n_angles, 0.5 * (n_det - 1));
+    }
+    // workspace layout
+    const size_t fs = sizeof(float);
+    const size_t ns = (size_t)n_angles * n_det, R = std::max(p->R, 1);
+    const size_t gimg = (size_t)p->GT * p->GTP, ytile = (size_t)p->T * p->TP, ptile = (size_t)p->T * p->T;
+    const int side = 2 * radius;
+    const int nb = (n + 31) / 32;
+    p->stitch_cap = n_roi * std::max(1, world) * ((side + 31) / 32 + 1) * ((side + 31) / 32 + 1);
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t r = o; o = align256(o + bytes); return r; };
+    auto& f = p->off;
+    f.angf = take(n_angles * sizeof(AngF));
+    f.cs64 = take(n_angles * 8); f.sn64 = take(n_angles * 8); f.A64 = take(n_angles * 8); f.B64 = take(n_angles * 8);
+    f.tiles = take(R * sizeof(TileT)); f.d0 = take(R * n_angles * 4); f.tauc = take(R * n_angles * 8);
+    f.gtile = take(sizeof(TileT)); f.gd0 = take(n_angles * 4); f.gtauc = take(n_angles * 8);
+    f.bank = take((size_t)n_iter * ns * fs); f.conv = take((size_t)n_iter * ns * fs);
+    f.pc = take(ns * fs); f.wd = take(ns * fs); f.wdsum = take(n_angles * 8); f.psum = take(n_angles * 8);
+    f.discc64 = take(8); f.discc32 = take(4); f.err = take(4);
+    f.gimg = take(gimg * fs); f.gimgT = take(gimg * fs); f.gsino = take(ns * fs); f.gsino2 = take(ns * fs);
+    const size_t nn = (size_t)n * n;
+    f.gplain = take(nn * fs); f.gr = take(nn * fs); f.gs = take(nn * fs); f.gpo = take(nn * fs);
+    f.gqo = take(nn * fs); f.gz = take(nn * fs); f.gxprev = take(nn * fs);
+    f.y = take(R * ytile * fs); f.yT = take(R * ytile * fs); f.s = take(R * n_angles * p->Wwin * fs);
+    f.v = take(R * ptile * fs); f.xs = take(R * ptile * fs); f.xprev = take(R * ptile * fs);
+    f.tt = take(ytile * fs); f.ttT = take(ytile * fs); f.tw = take((size_t)n_angles * p->Wwin * fs);
+    f.st_off = take(((size_t)nb * nb + 1) * 4); f.st_lst = take((size_t)p->stitch_cap * 4);
+    f.st_r0 = take((size_t)n_roi * std::max(1, world) * 4 + 4); f.st_c0 = take((size_t)n_roi * std::max(1, world) * 4 + 4);
+    f.cores = take(R * side * side * fs); f.hsino = take(ns * fs); f.himg = take(nn * fs);
+    f.total = o;
+    p->ws_bytes = (int64_t)o;
+    *out = p;
+    return LT_OK;
+}
+
+int64_t lt_plan_workspace_bytes(const lt_plan* p) { return p ? (int64_t)p->off.total : -1; }
+
+int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) {
+    if (!p || !d_ws) return fail(LT_ERR_INVALID, "null plan/workspace");
+    if (bytes < (int64_t)p->off.total) return fail(LT_ERR_INVALID, "workspace too small: %lld < %lld", (long long)bytes, (long long)p->off.total);
+    if (((uintptr_t)d_ws) & 255) return fail(LT_ERR_INVALID, "workspace must be 256-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    p->ws = (char*)d_ws;
+    auto up = [&](size_t o, const void* src, size_t bytes_) {
+        return cudaMemcpyAsync(p->ws + o, src, bytes_, cudaMemcpyHostToDevice, st);
+    };
+    const size_t na = p->na;
+    LT_CUDA(up(p->off.angf, p->angf.data(), na * sizeof(AngF)));
+    LT_CUDA(up(p->off.cs64, p->cs64.data(), na * 8));
+    LT_CUDA(up(p->off.sn64, p->sn64.data(), na * 8));
+    LT_CUDA(up(p->off.A64, p->A64.data(), na * 8));
+    LT_CUDA(up(p->off.B64, p->B64.data(), na * 8));
+    LT_CUDA(up(p->off.tiles, p->tiles.data(), p->tiles.size() * sizeof(TileT)));
+    LT_CUDA(up(p->off.d0, p->d0.data(), p->d0.size() * 4));
+    LT_CUDA(up(p->off.tauc, p->tauc.data(), p->tauc.size() * 8));
+    LT_CUDA(up(p->off.gtile, p->gtile.data(), sizeof(TileT)));
+    LT_CUDA(up(p->off.gd0, p->gd0.data(), na * 4));
+    LT_CUDA(up(p->off.gtauc, p->gtauc.data(), na * 8));
+    LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));
+    LT_CUDA(cudaMemsetAsync(p->ws + p->off.discc32, 0, 4, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    p->bound = true;
+    p->bank_ready = p->wd_ready = false;
+    return LT_OK;
+}
+
+int32_t lt_plan_local_count(const lt_plan* p) { return p ? p->R : -1; }
+
+int lt_plan_local_rois(const lt_plan* p, int32_t* out) {
+    if (!p || !out) return fail(LT_ERR_INVALID, "null argument");
+    for (int q = 0; q < p->R; ++q) out[q] = p->local[q];
+    return LT_OK;
+}
+
+int lt_plan_tables(const lt_plan* p, int32_t* rects, int32_t* d0, int32_t* wwin) {
+    if (!p) return fail(LT_ERR_INVALID, "null plan");
+    for (int q = 0; q < p->R; ++q) {
+        const TileT& t = p->tiles[q];
+        if (rects) {
+            int32_t* o = rects + 6 * q;
+            o[0] = t.row0; o[1] = t.col0; o[2] = t.vr0; o[3] = t.vr1; o[4] = t.vc0; o[5] = t.vc1;
+        }
+        if (d0)
+            for (int a = 0; a < p->na; ++a) d0[(size_t)q * p->na + a] = p->d0[(size_t)q * p->na + a];
+    }
+    if (wwin) *wwin = p->Wwin;
+    return LT_OK;
+}
+
+int lt_filter_bank(lt_plan* p, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = ensure_wd(*p, st)) return rc;
+    // Alg. 1: c = e_c; for k: v = W c; u_k = u_{k-1} + alpha v; c <- c - alpha W^T v
+    float* c = p->P<float>(p->off.gimg);
+    float* cT = p->P<float>(p->off.gimgT);
+    float* v = p->P<float>(p->off.gsino);
+    const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(c, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(cT, 0, gbytes, st));
+    k_impulse<<<1, 32, 0, st>>>(p->n, p->GTP, c, cT);
+    LT_LAUNCHED();
+    const long long ns = (long long)p->na * p->nd;
+    const Tiles gt = p->glob_tiles();
+    for (int k = 0; k < p->n_iter; ++k) {
+        float* bk = p->P<float>(p->off.bank) + k * ns;
+        const float* bprev = k ? bk - ns : nullptr;
+        if (int rc = launch_fp(*p, 1, gt, c, cT, 0, v, 0, bprev, bk, st)) return rc;
+        if (k + 1 < p->n_iter) {
+            BpEpi e = epi0();
+            e.y = c; e.yT = cT; e.y_tstride = 0; e.alpha = (float)p->alpha;
+            const SinoView sv = view_full(v, p->nd);
+            if (int rc = launch_bp_t<1, BP_ALG1>(*p, gt, sv, sv, e, st)) return rc;
+        }
+    }
+    p->bank_ready = true;
+    return LT_OK;
+}
+
+int lt_set_bank(lt_plan* p, const float* d_bank, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_bank) return fail(LT_ERR_INVALID, "null bank");
+    LT_CUDA(cudaMemcpyAsync(p->ws + p->off.bank, d_bank, (size_t)p->n_iter * p->na * p->nd * sizeof(float),
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    p->bank_ready = true;
+    return LT_OK;
+}
+
+int lt_get_bank(const lt_plan* p, float* d_bank, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!p->bank_ready) return fail(LT_ERR_INVALID, "bank not computed");
+    LT_CUDA(cudaMemcpyAsync(d_bank, p->ws + p->off.bank, (size_t)p->n_iter * p->na * p->nd * sizeof(float),
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return LT_OK;
+}
+
+int lt_project(const lt_plan* cp, int32_t roi, const float* d_img, float* d_sino, void* stream) {
+    if (int rc = check_plan(cp)) return rc;
+    lt_plan* p = const_cast<lt_plan*>(cp);
+    if (!d_img || !d_sino) return fail(LT_ERR_INVALID, "null pointer");
+    if (roi < -1 || roi >= p->R) return fail(LT_ERR_INVALID, "roi %d out of range", roi);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (roi < 0) {
+        float* gi = p->P<float>(p->off.gimg);
+        float* giT = p->P<float>(p->off.gimgT);
+        const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float);
+        LT_CUDA(cudaMemsetAsync(gi, 0, gbytes, st));
+        LT_CUDA(cudaMemsetAsync(giT, 0, gbytes, st));
+        k_pack<<<grid2d(p->n, p->n), dim3(32, 8), 0, st>>>(p->n, p->GTP, d_img, 0, gi, giT);
+        LT_LAUNCHED();
+        return launch_fp(*p, 0, p->glob_tiles(), gi, giT, 0, d_sino, 0, nullptr, nullptr, st);
+    }
+    float* tt = p->P<float>(p->off.tt);
+    float* ttT = p->P<float>(p->off.ttT);
+    float* tw = p->P<float>(p->off.tw);
+    const size_t tb = (size_t)p->T * p->TP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(tt, 0, tb, st));
+    LT_CUDA(cudaMemsetAsync(ttT, 0, tb, st));
+    k_extract<<<grid2d(p->T, p->T), dim3(32, 8), 0, st>>>(p->n, p->T, p->TP, p->tiles[roi], d_img, tt, ttT);
+    LT_LAUNCHED();
+    // single-tile view of this ROI's tables
+    Tiles t = p->roi_tiles();
+    t.tile += roi; t.d0 += (size_t)roi * p->na; t.tauc += (size_t)roi * p->na; t.ntiles = 1;
+    if (int rc = launch_fp(*p, 0, t, tt, ttT, 0, tw, 0, nullptr, nullptr, st)) return rc;
+    k_scatter_win<<<dim3((p->nd + 255) / 256, p->na), 256, 0, st>>>(p->na, p->nd, p->Wwin, t.d0, tw, d_sino);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int lt_backproject(const lt_plan* cp, int32_t roi, const float* d_sino, float* d_img, void* stream) {
+    if (int rc = check_plan(cp)) return rc;
+    lt_plan* p = const_cast<lt_plan*>(cp);
+    if (!d_img || !d_sino) return fail(LT_ERR_INVALID, "null pointer");
+    if (roi < -1 || roi >= p->R) return fail(LT_ERR_INVALID, "roi %d out of range", roi);
+    cudaStream_t st = (cudaStream_t)stream;
+    BpEpi e = epi0();
+    e.out = d_img; e.out_pitch = p->n;
+    const SinoView sv = view_full(d_sino, p->nd);
+    if (roi < 0) return launch_bp_t<1, BP_PLAIN_GLOBAL>(*p, p->glob_tiles(), sv, sv, e, st);
+    LT_CUDA(cudaMemsetAsync(d_img, 0, (size_t)p->n * p->n * sizeof(float), st));
+    Tiles t = p->roi_tiles();
+    t.tile += roi; t.d0 += (size_t)roi * p->na; t.tauc += (size_t)roi * p->na; t.ntiles = 1;
+    return launch_bp_t<1, BP_PLAIN_GLOBAL>(*p, t, sv, sv, e, st);
+}
+
+int lt_disc_correct(lt_plan* p, const float* d_sino, float* d_pc, float* d_c, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || !d_pc) return fail(LT_ERR_INVALID, "null pointer");
+    return disc_correct(*p, d_sino, d_pc, d_c, (cudaStream_t)stream);
+}
+
+int lt_conv_cache(lt_plan* p, const float* d_pc, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_pc) return fail(LT_ERR_INVALID, "null pointer");
+    return conv_cache(*p, d_pc, (cudaStream_t)stream);
+}
+
+int lt_get_conv(const lt_plan* p, float* d_out, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    LT_CUDA(cudaMemcpyAsync(d_out, p->ws + p->off.conv, (size_t)p->n_iter * p->na * p->nd * sizeof(float),
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return LT_OK;
+}
+
+int lt_sirt_solve(lt_plan* p, const float* d_sino, float lo, float hi, float* d_cores, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
+    if (!(lo <= hi)) return fail(LT_ERR_INVALID, "lo > hi");
+    if (p->R == 0) return LT_OK;
+    return solve(*p, 0, d_sino, lo, hi, 0, d_cores, (cudaStream_t)stream);
+}
+
+int lt_tv_solve(lt_plan* p, const float* d_sino, float lambda, int32_t n_fgp, float* d_cores, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
+    if (!(lambda >= 0.f) || n_fgp < 1) return fail(LT_ERR_INVALID, "lambda >= 0 and n_fgp >= 1 required");
+    int K, RB, WP; size_t sm;
+    if (int rc = fgp_config(p->T, p->T, &K, &RB, &WP, &sm)) return rc;
+    if (p->R == 0) return LT_OK;
+    return solve(*p, 1, d_sino, lambda, 0.f, n_fgp, d_cores, (cudaStream_t)stream);
+}
+
+int lt_get_ext(const lt_plan* p, float* d_ext, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (p->last_mode < 0) return fail(LT_ERR_INVALID, "no solve has run");
+    const int E = p->T;
+    dim3 grid((E + 31) / 32, (E + 7) / 8, p->R);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->last_mode == 0)
+        k_ext<<<grid, dim3(32, 8), 0, st>>>(E, p->P<TileT>(p->off.tiles), p->P<float>(p->off.y), p->ytile(), p->TP, PADL, d_ext);
+    else
+        k_ext<<<grid, dim3(32, 8), 0, st>>>(E, p->P<TileT>(p->off.tiles), p->P<float>(p->off.xprev), p->ptile(), p->T, 0, d_ext);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int lt_combine_rois(const lt_plan* p, const float* d_cores_all, int32_t n_slots, const int32_t* h_slot_roi,
+                    float* d_image, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_image || n_slots < 0 || (n_slots > 0 && (!d_cores_all || !h_slot_roi))) return fail(LT_ERR_INVALID, "bad arguments");
+    return combine(*p, d_cores_all, n_slots, h_slot_roi, d_image, (cudaStream_t)stream);
+}
+
+int lt_solve_host(lt_plan* p, int32_t mode, const float* h_sino, float p0, float p1, int32_t n_fgp, float* h_image,
+                  void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!h_sino || !h_image) return fail(LT_ERR_INVALID, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    float* ds = p->P<float>(p->off.hsino);
+    float* di = p->P<float>(p->off.himg);
+    float* dc = p->P<float>(p->off.cores);
+    LT_CUDA(cudaMemcpyAsync(ds, h_sino, (size_t)p->na * p->nd * sizeof(float), cudaMemcpyHostToDevice, st));
+    int rc = mode == 0 ? lt_sirt_solve(p, ds, p0, p1, dc, st) : lt_tv_solve(p, ds, p0, n_fgp, dc, st);
+    if (rc) return rc;
+    std::vector<int> slots(p->local.begin(), p->local.end());
+    if (int rc2 = combine(*p, dc, p->R, slots.data(), di, st)) return rc2;
+    LT_CUDA(cudaMemcpyAsync(h_image, di, (size_t)p->n * p->n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    return LT_OK;
+}
+
+int lt_global_sirt(lt_plan* p, const float* d_sino, int32_t n_iter, float lo, float hi, float* d_img, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || !d_img || n_iter < 1 || !(lo <= hi)) return fail(LT_ERR_INVALID, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    float* x = p->P<float>(p->off.gimg);
+    float* xT = p->P<float>(p->off.gimgT);
+    float* r = p->P<float>(p->off.gsino);
+    const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(x, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(xT, 0, gbytes, st));
+    const Tiles gt = p->glob_tiles();
+    for (int k = 0; k < n_iter; ++k) {
+        if (int rc = launch_fp(*p, 2, gt, x, xT, 0, r, 0, d_sino, nullptr, st)) return rc;   // r = p - W x
+        BpEpi e = epi0();
+        e.y = x; e.yT = xT; e.alpha = (float)p->alpha; e.lo = lo; e.hi = hi;
+        const SinoView sv = view_full(r, p->nd);
+        if (int rc = launch_bp_t<1, BP_GSIRT>(*p, gt, sv, sv, e, st)) return rc;
+    }
+    k_unpack<<<grid2d(p->n, p->n), dim3(32, 8), 0, st>>>(p->n, p->GTP, x, d_img);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int lt_global_tv(lt_plan* p, const float* d_sino, int32_t n_iter, float lambda, int32_t n_fgp, float* d_img,
+                 void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || !d_img || n_iter < 1 || !(lambda >= 0.f) || n_fgp < 1) return fail(LT_ERR_INVALID, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = p->n;
+    float* xm = p->P<float>(p->off.gimg);     // momentum point r^k (padded + twin)
+    float* xmT = p->P<float>(p->off.gimgT);
+    float* r = p->P<float>(p->off.gsino);
+    float* v = p->P<float>(p->off.gplain);
+    float* gr = p->P<float>(p->off.gr);
+    float* gs = p->P<float>(p->off.gs);
+    float* gpo = p->P<float>(p->off.gpo);
+    float* gqo = p->P<float>(p->off.gqo);
+    float* gz = p->P<float>(p->off.gz);
+    float* xprev = p->P<float>(p->off.gxprev);
+    const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float), nb = (size_t)n * n * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(xm, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(xmT, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(xprev, 0, nb, st));
+    const Tiles gt = p->glob_tiles();
+    const dim3 g2 = grid2d(n, n), b2(32, 8);
+    double tk = 1.0;
+    for (int k = 0; k < n_iter; ++k) {
+        if (int rc = launch_fp(*p, 2, gt, xm, xmT, 0, r, 0, d_sino, nullptr, st)) return rc;
+        BpEpi e = epi0();
+        e.y = xm; e.out = v; e.alpha = (float)p->alpha;
+        const SinoView sv = view_full(r, p->nd);
+        if (int rc = launch_bp_t<1, BP_GTV>(*p, gt, sv, sv, e, st)) return rc;    // v = S(r^{k-1})
+        LT_CUDA(cudaMemsetAsync(gr, 0, nb, st));
+        LT_CUDA(cudaMemsetAsync(gs, 0, nb, st));
+        LT_CUDA(cudaMemsetAsync(gpo, 0, nb, st));
+        LT_CUDA(cudaMemsetAsync(gqo, 0, nb, st));
+        if (lambda > 0.f) {
+            double ti = 1.0;
+            for (int it = 0; it < n_fgp; ++it) {
+                k_gfgp_z<<<g2, b2, 0, st>>>(n, lambda, v, gr, gs, gz);
+                LT_LAUNCHED();
+                const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * ti * ti));
+                const float beta = (float)((ti - 1.0) / tn);
+                ti = tn;
+                k_gfgp_dual<<<g2, b2, 0, st>>>(n, 1.f / (8.f * lambda), beta, gz, gr, gs, gpo, gqo);
+                LT_LAUNCHED();
+            }
+        }
+        const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
+        const float beta_o = (float)((tk - 1.0) / tn);
+        tk = tn;
+        k_gfgp_out<<<g2, b2, 0, st>>>(n, lambda, beta_o, v, gpo, gqo, xprev, xm, xmT, p->GTP);
+        LT_LAUNCHED();
+    }
+    LT_CUDA(cudaMemcpyAsync(d_img, xprev, nb, cudaMemcpyDeviceToDevice, st));
+    return LT_OK;
+}
+
+int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda, int32_t n_fgp, float* d_out,
+                 void* stream) {
+    if (h < 1 || w < 1 || count < 0 || !(lambda >= 0.f) || n_fgp < 1 || h > 256 || w > 256)
+        return fail(LT_ERR_INVALID, "bad FGP arguments");
+    if (count == 0) return LT_OK;
+    if (!d_in || !d_out) return fail(LT_ERR_INVALID, "null pointer");
+    FgpArgs A;
+    memset(&A, 0, sizeof A);
+    A.b = d_in; A.b_pitch = w; A.b_tstride = (long long)h * w;
+    A.tiles = nullptr; A.H = h; A.W = w;
+    A.lam = lambda; A.nfgp = n_fgp; A.mode = 0;
+    A.out = d_out; A.out_pitch = w; A.out_tstride = (long long)h * w;
+    return launch_fgp(A, h, w, count, (cudaStream_t)stream);
+}
+
+void lt_plan_destroy(lt_plan* p) { delete p; }
+
+}  // extern "C"

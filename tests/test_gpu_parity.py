@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C-ABI binding) against the fp64
+oracle on the same seeded inputs (-m gpu).
+
+Tolerances (north star / DESIGN.md §Parity): one A or A^T application and the
+convolution cache <= 1e-5 relative L2 (fp32); filter bank <= 1e-4; full solves
+<= 1e-3 per ROI core and on the stitched image; ROI indexing exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def relerr(a, b):
+    a = np.asarray(a, dtype=np.float64); b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def lt():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1604_02292_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def nd_for(n):
+    return int(math.ceil(math.sqrt(2) * n)) | 1
+
+
+def gpu(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def cpu(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().double().numpy()
+
+
+# ------------------------------------------------------------------ operators
+
+@pytest.mark.parametrize("n,na,span", [(64, 32, math.pi), (300, 45, math.pi), (200, 32, 2 * math.pi / 3), (37, 17, math.pi)])
+def test_global_project_backproject(lt, orc, n, na, span):
+    nd = nd_for(n)
+    ang = synth.angles_for(na, span)
+    plan = lt.Plan(n, ang, nd, [[n // 2, n // 2]], 4, 2, 1)
+    rng = np.random.default_rng(n)
+    x = rng.random((n, n)); s = rng.standard_normal((na, nd))
+    assert relerr(cpu(plan.project(gpu(x))), orc.forward(x, ang, nd)) <= 1e-5
+    assert relerr(cpu(plan.backproject(gpu(s))), orc.back(s, ang, n)) <= 1e-5
+    # fp32 adjoint identity on the GPU pair
+    wx = cpu(plan.project(gpu(x))); wts = cpu(plan.backproject(gpu(s)))
+    assert abs(np.vdot(wx, s) - np.vdot(x, wts)) <= 1e-5 * np.linalg.norm(wx) * np.linalg.norm(s)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_roi_project_backproject_all_bins(lt, orc, cfg):
+    """W_{L'} x = W(M_{L'} x) on ALL bins (window correctness) and M_{L'} W^T s,
+    for every ROI including clipped ones."""
+    c = synth.config(cfg)
+    ang = synth.angles_for(c.n_angles, c.span)
+    cen = synth.roi_centres(c)[:6]
+    cen = np.concatenate([cen, [[c.radius, c.radius], [c.n - c.radius, c.radius]]]).astype(np.int32)
+    plan = lt.Plan(c.n, ang, c.n_det, cen, c.radius, c.margin, 1)
+    rects = orc.roi_rects(c.n, cen, c.radius, c.margin)
+    rng = np.random.default_rng(3)
+    x = rng.random((c.n, c.n)); s = rng.standard_normal((c.n_angles, c.n_det))
+    xg, sg = gpu(x), gpu(s)
+    for q in range(plan.R):
+        g = plan.local_rois[q]
+        rect = tuple(int(v) for v in rects[g][4:8])
+        ref = orc.forward(x, ang, c.n_det, rect)
+        got = cpu(plan.project(xg, roi=q))
+        assert relerr(got, ref) <= 1e-5, (cfg, q)
+        assert np.all(got[ref == 0] == 0)
+        refb = orc.back(s, ang, c.n, rect)
+        gotb = cpu(plan.backproject(sg, roi=q))
+        assert relerr(gotb, refb) <= 1e-5, (cfg, q)
+        assert np.all(gotb[refb == 0] == 0)
+
+
+def test_filter_bank(lt, orc):
+    n, na, nd, nk = 64, 32, 91, 100
+    ang = synth.angles_for(na)
+    plan = lt.Plan(n, ang, nd, [[32, 32]], 12, 8, nk)
+    plan.filter_bank()
+    got = cpu(plan.get_bank())
+    ref = orc.filter_bank(n, ang, nd, nk)
+    for k in (0, 9, 49, 99):
+        assert relerr(got[k], ref[k]) <= 1e-4, k
+
+
+def test_filter_bank_odd_limited(lt, orc):
+    n, na, nk = 45, 20, 12
+    nd = nd_for(n)
+    ang = synth.angles_for(na, 2 * math.pi / 3)
+    plan = lt.Plan(n, ang, nd, [[22, 22]], 5, 3, nk)
+    plan.filter_bank()
+    got = cpu(plan.get_bank())
+    ref = orc.filter_bank(n, ang, nd, nk)
+    assert relerr(got, ref) <= 1e-4
+
+
+def test_disc_and_conv_cache(lt, orc):
+    inp = synth.make_inputs("C1")
+    n, nd, nk = 64, 91, 30
+    plan = lt.Plan(n, inp.angles, nd, inp.centres, 12, 8, nk)
+    plan.filter_bank()
+    pc_g, c_g = plan.disc_correct(gpu(inp.sino))
+    pc_o, c_o, _, _ = orc.disc(inp.sino.astype(np.float64), inp.angles, n)
+    assert abs(cpu(c_g)[0] - c_o) <= 1e-5 * abs(c_o)
+    assert relerr(cpu(pc_g), pc_o) <= 1e-5
+    # stage-wise: oracle bank + oracle p_c in, b_k out
+    bank_o = orc.filter_bank(n, inp.angles, nd, nk)
+    plan.set_bank(gpu(bank_o))
+    b_g = cpu(plan.conv_cache(gpu(pc_o)))
+    b_o = orc.conv_cache(bank_o, pc_o)
+    for k in (0, 5, 29):
+        assert relerr(b_g[k], b_o[k]) <= 1e-5, k
+
+
+def test_conv_cache_wide_detector(lt, orc):
+    """Several 512-tap chunks and a ragged tail (N_d = 1449)."""
+    rng = np.random.default_rng(4)
+    n, na, nd, nk = 1024, 3, 1449, 9
+    ang = synth.angles_for(na)
+    plan = lt.Plan(n, ang, nd, [[512, 512]], 8, 0, nk, disc=False)
+    bank = rng.standard_normal((nk, na, nd)) * np.exp(-np.abs(np.arange(nd) - 724) / 50.0)
+    p = rng.random((na, nd))
+    plan.set_bank(gpu(bank))
+    got = cpu(plan.conv_cache(gpu(p)))
+    ref = orc.conv_cache(bank.astype(np.float32).astype(np.float64), p.astype(np.float32).astype(np.float64))
+    assert relerr(got, ref) <= 1e-5
+
+
+# ------------------------------------------------------------------ FGP
+
+@pytest.mark.parametrize("h,w", [(6, 6), (40, 40), (100, 77), (128, 128), (192, 192), (256, 256), (1, 9)])
+def test_fgp_batch(lt, orc, h, w):
+    rng = np.random.default_rng(h * 1000 + w)
+    cnt = 3
+    b = rng.random((cnt, h, w))
+    lam, nf = 0.05, 100
+    got = cpu(lt.fgp_batch(gpu(b), lam, nf))
+    for q in range(cnt):
+        ref = orc.fgp(b[q].astype(np.float32).astype(np.float64), lam, nf)
+        assert relerr(got[q], ref) <= 1e-5, (h, w, q)
+
+
+def test_fgp_lambda_zero_identity(lt):
+    x = torch.rand(2, 30, 30, device="cuda")
+    assert torch.equal(lt.fgp_batch(x, 0.0, 10), x)
+
+
+# ------------------------------------------------------------------ full solves
+
+def _oracle_solve(orc, inp, cfg, n_iter, mode, lam=0.0, nfgp=100, roi_idx=None, bank=None):
+    cen = inp.centres if roi_idx is None else inp.centres[roi_idx]
+    return orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, n_iter,
+                        mode=mode, lam=lam, n_fgp=nfgp, bank=bank, want_ext=True)
+
+
+def test_sirt_solve_C1(lt, orc):
+    cfg = synth.config("C1")
+    inp = synth.make_inputs("C1")
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.sirt_solve(gpu(inp.sino), 0.0, math.inf))
+    ext = cpu(plan.get_ext())
+    ref, ref_ext = _oracle_solve(orc, inp, cfg, cfg.n_iter, "box")
+    assert relerr(cores, ref) <= 1e-3
+    assert relerr(ext, ref_ext) <= 1e-3
+    assert cores.min() >= 0.0
+
+
+def test_tv_solve_small(lt, orc):
+    cfg = synth.Config(20, "tvsmall", 128, 24, math.pi, 181, "poisson", 1e4, 5, 16, 16, "seeded", 12, "tv",
+                       0.05, 50, 6, 0)
+    inp = synth.make_inputs(cfg)
+    cen = np.array([[64, 64], [16, 16], [112, 40], [40, 112], [20, 100]], dtype=np.int32)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.tv_solve(gpu(inp.sino), cfg.lam, cfg.n_fgp))
+    ext = cpu(plan.get_ext())
+    ref, ref_ext = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin,
+                                cfg.n_iter, mode="tv", lam=cfg.lam, n_fgp=cfg.n_fgp, want_ext=True)
+    for q in range(5):
+        assert relerr(cores[q], ref[q]) <= 1e-3, q
+    assert relerr(ext, ref_ext) <= 1e-3
+
+
+def test_sirt_solve_C3_subset(lt, orc):
+    """C3 geometry (limited angle [0, 2pi/3)), seeded ROIs, 30 iterations."""
+    cfg = synth.config("C3")
+    inp = synth.make_inputs("C3")
+    n_iter = 30
+    cen = inp.centres[:6]
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.sirt_solve(gpu(inp.sino), 0.0, math.inf))
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, n_iter,
+                       mode="box")
+    for q in range(len(cen)):
+        assert relerr(cores[q], ref[q]) <= 1e-3, q
+
+
+def test_combine_matches_oracle_stitch(lt, orc):
+    n, r = 96, 8
+    cen = np.array([[8, 8], [8, 24], [20, 30], [88, 88], [50, 50], [52, 54]], dtype=np.int32)
+    plan = lt.Plan(n, synth.angles_for(4), nd_for(n), cen, r, 2, 1)
+    cores = np.random.default_rng(5).random((6, 16, 16))
+    got = cpu(plan.combine(gpu(cores), list(range(6))))
+    ref = orc.stitch(n, cen, r, cores.astype(np.float32).astype(np.float64))
+    assert relerr(got, ref) <= 1e-6
+    # slot order does not change the result (sum in ascending ROI order)
+    perm = [3, 1, 5, 0, 2, 4]
+    got2 = cpu(plan.combine(gpu(cores[perm]), perm))
+    assert np.array_equal(got, got2)
+
+
+def test_global_solvers(lt, orc):
+    n, na = 48, 24
+    nd = nd_for(n)
+    ang = synth.angles_for(na)
+    shapes = synth.random_shapes(n, 4, 1, np.random.default_rng(2))
+    p = synth.analytic_sinogram(shapes, ang, nd).astype(np.float32)
+    plan = lt.Plan(n, ang, nd, [[24, 24]], 4, 2, 1)
+    got = cpu(plan.global_sirt(gpu(p), 50, 0.0, math.inf))
+    ref = orc.global_box(p.astype(np.float64), ang, n, 50, lo=0.0, hi=np.inf)
+    assert relerr(got, ref) <= 1e-3
+    got = cpu(plan.global_tv(gpu(p), 10, 0.05, 40))
+    ref = orc.global_tv(p.astype(np.float64), ang, n, 10, 0.05, 40)
+    assert relerr(got, ref) <= 1e-3
+
+
+def test_full_size_C4_launch_config_sampled(lt, orc):
+    """C4 geometry and the full 256-ROI batch bench.py times, n = 3 iterations;
+    8 sampled ROIs (corners, edges, interior) against the oracle."""
+    cfg = synth.config("C4")
+    inp = synth.make_inputs("C4")
+    n_iter = 3
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.tv_solve(gpu(inp.sino), cfg.lam, 20))
+    sample = np.array([0, 15, 240, 255, 7, 100, 136, 200])
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, inp.centres[sample], cfg.radius,
+                       cfg.margin, n_iter, mode="tv", lam=cfg.lam, n_fgp=20)
+    for k, g in enumerate(sample):
+        q = int(np.nonzero(plan.local_rois == g)[0][0])
+        assert relerr(cores[q], ref[k]) <= 1e-3, g
+
+
+def test_determinism_and_empty(lt):
+    inp = synth.make_inputs("C1")
+    plan = lt.Plan(64, inp.angles, 91, inp.centres, 12, 8, 10)
+    plan.filter_bank()
+    a = cpu(plan.sirt_solve(gpu(inp.sino)))
+    b = cpu(plan.sirt_solve(gpu(inp.sino)))
+    assert np.array_equal(a, b)
+    empty = lt.Plan(64, inp.angles, 91, np.zeros((0, 2), np.int32), 12, 8, 10)
+    assert empty.R == 0
+    empty.filter_bank()
+    assert empty.sirt_solve(gpu(inp.sino)).shape == (0, 24, 24)

@@ -1,0 +1,144 @@
+"""Host-side checks of the C-ABI library (-m "not gpu"): it loads, exports every
+symbol include/loctomo.h declares, validates arguments (error code 2), and
+its ROI plan (rectangles, windows, partition) is exact against the oracle and
+brute force.  No device compute is called here."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lt():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1604_02292_b200 as m
+    return m
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "loctomo.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lt_\w+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(lt):
+    lib = ctypes.CDLL(lt.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(lt.EXPORTS)
+
+
+def _setup(lt, n=64, angles=None, nd=91, cen=((32, 32),), r=12, m=8, nit=10, rank=0, world=1):
+    angles = synth.angles_for(32) if angles is None else np.asarray(angles, dtype=np.float64)
+    cen = np.asarray(cen, dtype=np.int32).reshape(-1, 2)
+    rows = np.ascontiguousarray(cen[:, 0]); cols = np.ascontiguousarray(cen[:, 1])
+    p = ctypes.c_void_p()
+    rc = lt._lib.lt_roi_setup(n, len(angles), nd, angles.ctypes.data, len(cen), rows.ctypes.data, cols.ctypes.data,
+                              r, m, nit, 1, rank, world, ctypes.byref(p))
+    if rc == 0:
+        lt._lib.lt_plan_destroy(p)
+    return rc
+
+
+def test_argument_validation(lt):
+    assert _setup(lt) == 0
+    assert _setup(lt, nd=90) == 2                                   # even N_d
+    assert _setup(lt, angles=[0.0, 0.5, 0.4]) == 2                  # not increasing
+    assert _setup(lt, angles=[0.0, 3.2]) == 2                       # outside [0, pi)
+    assert _setup(lt, cen=((5, 32),)) == 2                          # core outside the grid
+    assert _setup(lt, r=0) == 2
+    assert _setup(lt, m=-1) == 2
+    assert _setup(lt, nit=0) == 2
+    assert _setup(lt, rank=2, world=2) == 2
+    assert _setup(lt, n=0) == 2
+    assert _setup(lt, cen=np.zeros((0, 2))) == 0                    # empty ROI list is valid
+
+
+def test_unbound_plan_errors(lt):
+    plan = lt.Plan(64, synth.angles_for(8), 91, [[32, 32]], 12, 8, 5, bind=False)
+    rc = lt._lib.lt_filter_bank(plan._p, None)
+    assert rc == 2 and b"workspace" in lt._lib.lt_last_error()
+
+
+def test_rects_match_oracle(lt, orc):
+    for cfg in ("C1", "C2", "C3", "C4"):
+        c = synth.config(cfg)
+        cen = synth.roi_centres(c)
+        plan = lt.Plan(c.n, synth.angles_for(c.n_angles, c.span), c.n_det, cen, c.radius, c.margin, 1, bind=False)
+        rects, _, _ = plan.tables()
+        ref = orc.roi_rects(c.n, cen, c.radius, c.margin)
+        h = c.radius + c.margin
+        for q, g in enumerate(plan.local_rois):
+            row0, col0, vr0, vr1, vc0, vc1 = rects[q]
+            assert (row0 + vr0, row0 + vr1, col0 + vc0, col0 + vc1) == tuple(ref[g][4:8])
+            assert (row0 + h - c.radius, col0 + h - c.radius) == (ref[g][0], ref[g][2])
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_windows_contain_exact_support(lt, orc, cfg):
+    """P12: each ROI's window [d0, d0 + W) contains every bin where W_{L'} is
+    nonzero (brute force with the oracle's W on the indicator of L')."""
+    c = synth.config(cfg)
+    ang = synth.angles_for(c.n_angles, c.span)
+    cen = np.concatenate([synth.roi_centres(c)[:4], [[c.radius, c.radius], [c.n - c.radius, c.n - c.radius]]])
+    plan = lt.Plan(c.n, ang, c.n_det, cen, c.radius, c.margin, 1, bind=False)
+    rects, d0, W = plan.tables()
+    assert W == lt.window_width(c.radius + c.margin)
+    ref = orc.roi_rects(c.n, cen, c.radius, c.margin)
+    ones = np.ones((c.n, c.n))
+    for q, g in enumerate(plan.local_rois):
+        s = orc.forward(ones, ang, c.n_det, tuple(int(v) for v in ref[g][4:8]))
+        for a in range(c.n_angles):
+            nz = np.nonzero(s[a])[0]
+            assert nz.min() >= d0[q, a] and nz.max() < d0[q, a] + W, (cfg, g, a)
+
+
+def test_window_width_bruteforce():
+    """W(h) = 2 ceil((2h-1)/sqrt2) + 4 >= the support width of a 2h x 2h square
+    at any angle and any sub-bin offset of its centre (V4)."""
+    import paper_1604_02292_b200 as m
+    rng = np.random.default_rng(0)
+    for h in (1, 2, 5, 20, 64, 96, 128):
+        W = m.window_width(h)
+        for _ in range(400):
+            th = rng.uniform(0, math.pi)
+            c = max(abs(math.cos(th)), abs(math.sin(th)))
+            tau = rng.uniform(-50, 50)
+            half = (h - 0.5) * (abs(math.cos(th)) + abs(math.sin(th)))
+            lo = math.floor(tau - half - c) + 1          # smallest bin strictly inside the support
+            hi = math.ceil(tau + half + c) - 1
+            d0 = math.floor(tau) - W // 2
+            assert lo >= d0 and hi < d0 + W, (h, th, tau)
+
+
+def test_partition_covers_every_roi_once(lt):
+    c = synth.config("C4")
+    cen = synth.roi_centres(c)
+    ang = synth.angles_for(8)
+    for world in (1, 2, 3, 4, 8):
+        seen = []
+        counts = []
+        for rank in range(world):
+            plan = lt.Plan(c.n, ang, c.n_det, cen, c.radius, c.margin, 1, rank=rank, world=world, bind=False)
+            assert np.all(np.diff(plan.local_rois) > 0)
+            seen.extend(plan.local_rois.tolist()); counts.append(plan.R)
+        assert sorted(seen) == list(range(len(cen)))
+        assert max(counts) - min(counts) <= 2
+
+
+def test_workspace_size_reasonable(lt):
+    c = synth.config("C5")
+    plan = lt.Plan(c.n, synth.angles_for(c.n_angles), c.n_det, synth.roi_centres(c), c.radius, c.margin,
+                   c.n_iter, bind=False)
+    gb = plan.workspace_bytes / 2**30
+    assert 5.0 < gb < 40.0, gb          # bank + conv cache (2 x 2.97 GB) + ROI state fit 180 GB
