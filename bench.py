@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the local-tomography hot path (BASELINE.json metric).
+
+Step = one pass of the whole hot path over one synthetic C4 batch:
+disc pre-correction (a2) + convolution cache (a4) + n = 200 local FISTA-TV
+iterations on every ROI (a5-a8: Joseph FP, fused two-sinogram BP + update,
+cluster FGP + momentum) + crop (a9) + combine into one N x N image (a9/e:
+NCCL all-gather of the cores when N > 1, stitch kernel).  The filter bank
+(a3, Alg. 1) depends only on the geometry and is computed once before the
+timed region ("subsequent applications"); its time is
+reported as bank_ms.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+Multi-GPU: launched by torchrun, one rank per GPU; ROIs are partitioned
+across ranks (strong scaling of one image), timing = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "ROI solves/sec and A+A^T Gray/s (ray-pixel updates/s) vs HBM roofline, 1–8 GPU"
+UNIT = "ROI solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        time.sleep(0.1)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- work counts
+def algorithmic_counts(cfg, plan_rects, n_iter):
+    """Pixel-angle updates of one step (A+A^T Gray), FGP pixel-iterations."""
+    P = [(r[3] - r[2]) * (r[5] - r[4]) for r in plan_rects]
+    Ptot = float(sum(P))
+    # iteration 1: y = 0 -> one A^T (of b_1); iterations 2..n: A y, A^T b_k, A^T s
+    updates = cfg.n_angles * Ptot * (1 + 3 * (n_iter - 1))
+    fgp_px_it = Ptot * n_iter * cfg.n_fgp if "tv" in cfg.solver else 0.0
+    return updates, fgp_px_it, Ptot
+
+
+# FP32 operations per unit, DESIGN.md §Roofline (counted from the formulas, not the SASS)
+FGP_FLOPS_PER_PX_IT = 21.0      # z (5) + two dual steps with clip (10) + momentum (6)
+JOSEPH_FLOPS_PER_UPDATE = 8.0   # hat weight (2 FMA-equivalents) + 2 taps x FMA, per pixel-angle
+
+
+def run_ours(args, cfg):
+    import torch
+    import paper_1604_02292_b200 as lt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    inp = synth.make_inputs(cfg)
+    n_iter = cfg.n_iter
+    mode = "tv" if "tv" in cfg.solver else "sirt"
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter, rank=rank, world=world)
+    rects, _, _ = plan.tables()
+    # per-geometry precompute (outside the timed region)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan.filter_bank()
+    torch.cuda.synchronize()
+    bank_ms = (time.perf_counter() - t0) * 1e3
+
+    sino_host = torch.from_numpy(inp.sino).pin_memory()
+    sino = sino_host.cuda()
+    side = 2 * cfg.radius
+    max_local = -(-cfg.n_roi // world)
+    cores = torch.zeros(max_local, side, side, device="cuda")
+    image = torch.empty(cfg.n, cfg.n, device="cuda")
+    gathered = torch.empty(world * max_local, side, side, device="cuda") if world > 1 else None
+    # slot -> global ROI table for the gathered layout
+    slot_roi = np.full(world * max_local, -1, dtype=np.int32)
+    if world > 1:
+        all_local = [None] * world
+        dist.all_gather_object(all_local, plan.local_rois.tolist())
+        for g, lst in enumerate(all_local):
+            slot_roi[g * max_local:g * max_local + len(lst)] = lst
+    else:
+        slot_roi[:plan.R] = plan.local_rois
+
+    def step():
+        out = cores[:plan.R]
+        if mode == "tv":
+            plan.tv_solve(sino, cfg.lam, cfg.n_fgp, out=out)
+        else:
+            plan.sirt_solve(sino, 0.0, math.inf, out=out)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, cores)
+            plan.combine(gathered, slot_roi, out=image)
+        else:
+            plan.combine(cores[:plan.R], slot_roi[:plan.R], out=image)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    lt.timing_enable(True)
+    lt.timing_read()
+    n_launch0 = lt.launch_count()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    n_launch = lt.launch_count() - n_launch0
+    ktimes = lt.timing_read()
+    lt.timing_enable(False)
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    # e2e: same step through the host-buffer C-ABI entry (pinned H2D + solve + combine + D2H)
+    image_host = torch.empty(cfg.n, cfg.n, dtype=torch.float32).pin_memory()
+    if world == 1:
+        def e2e_step():
+            plan.solve_host(mode, sino_host, cfg.lam if mode == "tv" else 0.0,
+                            0.0 if mode == "tv" else math.inf, cfg.n_fgp, image_host)
+    else:
+        def e2e_step():
+            sino.copy_(sino_host, non_blocking=True)
+            step()
+            image_host.copy_(image, non_blocking=True)
+            torch.cuda.synchronize()
+    e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e_steps = max(1, min(args.steps, 3))
+    for _ in range(e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # global counts
+    upd_local, fgp_local, _ = algorithmic_counts(cfg, rects, n_iter)
+    if dist:
+        t = torch.tensor([upd_local, fgp_local], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        upd, fgp_pi = float(t[0]), float(t[1])
+    else:
+        upd, fgp_pi = upd_local, fgp_local
+    ms_per_step = elapsed_ms / args.steps
+    value = cfg.n_roi / (ms_per_step / 1e3)
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return None
+
+    pk, pk_src = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # FP32 lanes x FMA, DESIGN.md §Roofline
+    # dominant kernel class over the timed region (rank 0's stream)
+    dom = max(ktimes, key=lambda k: ktimes[k][0])
+    dom_ms, dom_n = ktimes[dom]
+    avg_ms = dom_ms / max(dom_n, 1)
+    local_upd_per_step = upd_local
+    if dom == "fgp":
+        work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / max(dom_n, 1)
+    elif dom in ("fp", "bp"):
+        # each FP launch is one A (N_theta * P updates); each two-sinogram BP counts 2
+        work = JOSEPH_FLOPS_PER_UPDATE * local_upd_per_step * args.steps / max(ktimes["fp"][1] + ktimes["bp"][1], 1)
+    else:
+        work = 0.0
+    achieved = work / (avg_ms / 1e3) / 1e12
+    roofline = {"kernel": {"fgp": "k_fgp", "fp": "k_fp", "bp": "k_bp", "conv": "k_conv"}[dom],
+                "bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak_tflops, 1),
+                "unit": "TFLOP/s", "frac": round(achieved / alu_peak_tflops, 4), "traffic": None,
+                "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)",
+                "avg_launch_ms": round(avg_ms, 4), "launches": dom_n,
+                "share_of_step": round(dom_ms / elapsed_ms, 3)}
+    kshare = {k: {"ms_per_step": round(v[0] / args.steps, 3), "launches_per_step": v[1] // args.steps}
+              for k, v in ktimes.items()}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, budget_s=20.0)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.n}, {cfg.n_angles} angles, {cfg.n_det} det, "
+                               f"{cfg.n_roi} ROIs r={cfg.radius} m={cfg.margin}, {mode}, n={n_iter}"
+                               + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" else ""),
+                   "global_batch_rois": cfg.n_roi, "parallelism": f"roi-shard x{world}",
+                   "l2": "inputs larger than L2 (conv cache 417 MB + ROI state), no flush",
+                   "bank": "warm (per-geometry precompute, excluded)"},
+        "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
+        "fgp_gpix_it_s": round(fgp_pi / (ms_per_step / 1e3) / 1e9, 2),
+        "bank_ms": round(bank_ms, 2),
+        "kernels": kshare,
+        "gpu_launches": int(n_launch),
+        "e2e": {"value": round(cfg.n_roi / (e2e_ms / 1e3), 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(cfg.n_angles * cfg.n_det * 4),
+                "d2h_bytes_per_step": int(cfg.n * cfg.n * 4), "ms_per_step": round(e2e_ms, 3)},
+        "roofline": roofline,
+        "hbm_peak_gbs": pk.get("hbm_gbs"),
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return line
+
+
+# --------------------------------------------------------------------------- oracle (CPU)
+def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None):
+    """Time the fp64 oracle on a bounded sample of the same workload and
+    extrapolate to the full step: disc (whole) + conv cache (n_conv_k of n
+    filters, scaled) + one ROI for n_iter_sample of n iterations (scaled, x R)."""
+    import oracle
+    inp = synth.make_inputs(cfg)
+    p = inp.sino.astype(np.float64)
+    n = cfg.n
+    t0 = time.perf_counter()
+    pc, c, _, _ = oracle.disc(p, inp.angles, n)
+    t_disc = time.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    fake_bank = rng.standard_normal((n_conv_k, cfg.n_angles, cfg.n_det))
+    t0 = time.perf_counter()
+    oracle.conv_cache(fake_bank, pc)
+    t_conv = (time.perf_counter() - t0) * cfg.n_iter / n_conv_k
+    g = cfg.n_roi // 2 + cfg.n_roi // 32 if roi_index is None else roi_index
+    bconv = rng.standard_normal((n_iter_sample, cfg.n_angles, cfg.n_det)) * 1e-3
+    mode = "tv" if "tv" in cfg.solver else "box"
+    t0 = time.perf_counter()
+    oracle.local_solve(n, inp.angles, cfg.n_det, bconv, inp.centres[g:g + 1], cfg.radius, cfg.margin, mode=mode,
+                       lam=cfg.lam, n_fgp=cfg.n_fgp, disc_c=c, use_disc=True)
+    t_roi = (time.perf_counter() - t0) * cfg.n_iter / n_iter_sample
+    total = t_disc + t_conv + t_roi * cfg.n_roi
+    sample = (f"disc (full) + conv cache {n_conv_k}/{cfg.n_iter} filters (x{cfg.n_iter / n_conv_k:g}) + ROI #{g} "
+              f"{n_iter_sample}/{cfg.n_iter} iterations (x{cfg.n_iter / n_iter_sample:g}, x{cfg.n_roi} ROIs); "
+              f"measured {t_disc:.2f}+{t_conv * n_conv_k / cfg.n_iter:.2f}+{t_roi * n_iter_sample / cfg.n_iter:.2f} s")
+    return cfg.n_roi / total, sample, oracle.get_threads()
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    try:
+        v, sample, cores = oracle_sample(cfg)
+        return {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    except Exception as e:  # report, never fake
+        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    for _ in range(args.warmup):
+        oracle_sample(cfg, n_iter_sample=2, n_conv_k=1)
+    vals = []
+    t0 = time.perf_counter()
+    sample = ""
+    for _ in range(args.steps):
+        v, sample, cores = oracle_sample(cfg, n_iter_sample=2, n_conv_k=1)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(cfg.n_roi / value * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name} (fp64 CPU oracle, extrapolated from a bounded sample)"},
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": round(wall, 1)}
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    args = parse()
+    cfg = synth.config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

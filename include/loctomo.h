@@ -154,6 +154,15 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
 /* Number of kernels this library has launched so far (process-wide). */
 int64_t lt_launch_count(void);
 
+/* Per-kernel-class device timing (bench.py's roofline): when enabled, every
+ * launch of the Joseph forward (class 0), backprojection (1), FGP (2) and
+ * convolution (3) kernels is bracketed by CUDA events recorded on its launch
+ * stream.  lt_timing_read synchronizes on the recorded events, writes the
+ * summed milliseconds and launch counts per class (host arrays of 4) and
+ * clears the records. */
+void lt_timing_enable(int32_t on);
+int lt_timing_read(double* h_ms, int64_t* h_count);
+
 void lt_plan_destroy(lt_plan* plan);
 const char* lt_last_error(void);
 

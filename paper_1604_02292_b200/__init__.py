@@ -58,6 +58,8 @@ _SIGS = {
     "lt_global_tv": ([_P, _P, _I, _F, _I, _P, _P], _I),
     "lt_fgp_batch": ([_I, _I, _I, _P, _F, _I, _P, _P], _I),
     "lt_launch_count": ([], _i64),
+    "lt_timing_enable": ([_I], None),
+    "lt_timing_read": ([_P, _P], _I),
     "lt_plan_destroy": ([_P], None),
     "lt_last_error": ([], ctypes.c_char_p),
 }
@@ -92,6 +94,22 @@ def _cuda_f32(t: torch.Tensor, name: str) -> torch.Tensor:
 def launch_count() -> int:
     """Kernels launched by the library so far (process-wide)."""
     return int(_lib.lt_launch_count())
+
+
+KERNEL_CLASSES = ("fp", "bp", "fgp", "conv")
+
+
+def timing_enable(on: bool = True) -> None:
+    """Bracket every FP/BP/FGP/conv launch with CUDA events on its stream."""
+    _lib.lt_timing_enable(1 if on else 0)
+
+
+def timing_read() -> dict:
+    """{class: (total_ms, launches)} since the last read (synchronizes on the events)."""
+    ms = np.zeros(4, dtype=np.float64)
+    cnt = np.zeros(4, dtype=np.int64)
+    _chk(_lib.lt_timing_read(ms.ctypes.data, cnt.ctypes.data), "lt_timing_read")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
 
 
 def window_width(h: int) -> int:
@@ -137,7 +155,7 @@ class Plan:
 
     def __del__(self):
         p = getattr(self, "_p", None)
-        if p is not None and p.value:
+        if p is not None and p.value and _lib is not None:
             _lib.lt_plan_destroy(p)
             self._p = None
 

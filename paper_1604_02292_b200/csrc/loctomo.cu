@@ -45,6 +45,29 @@ int fail(int code, const char* fmt, ...) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// ---- optional per-kernel-class timing (CUDA events on the launch stream) ----
+enum { TC_FP = 0, TC_BP = 1, TC_FGP = 2, TC_CONV = 3, TC_N = 4 };
+struct TimerRec { int cls; cudaEvent_t a, b; };
+bool g_timing = false;
+std::vector<TimerRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t ev_get() {
+    if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+struct ScopedTimer {
+    int cls; cudaStream_t st; cudaEvent_t a = nullptr;
+    ScopedTimer(int c, cudaStream_t s) : cls(c), st(s) {
+        if (g_timing) { a = ev_get(); cudaEventRecord(a, st); }
+    }
+    ~ScopedTimer() {
+        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, st); g_recs.push_back({cls, a, b}); }
+    }
+};
+
 }  // namespace
 
 struct lt_plan {
@@ -118,6 +141,7 @@ int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, cons
               float* out, long long out_ts, const float* aux_in, float* aux_out, cudaStream_t st) {
     FpArgs f{img, imgT, img_ts, out, out_ts, aux_in, aux_out, (float)p.alpha};
     dim3 grid((t.Wwin + 127) / 128, p.na, t.ntiles);
+    ScopedTimer tm(TC_FP, st);
     if (mode == 0) k_fp<0><<<grid, 128, 0, st>>>(p.geo(), t, f);
     else if (mode == 1) k_fp<1><<<grid, 128, 0, st>>>(p.geo(), t, f);
     else k_fp<2><<<grid, 128, 0, st>>>(p.geo(), t, f);
@@ -130,6 +154,7 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
                 cudaStream_t st) {
     const int nsx = (t.T + 31) / 32;
     dim3 grid(nsx * nsx, t.ntiles);
+    ScopedTimer tm(TC_BP, st);
     k_bp<NS, MODE><<<grid, 256, 0, st>>>(p.geo(), t, s1, s2, e);
     LT_LAUNCHED();
     return LT_OK;
@@ -185,6 +210,7 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    ScopedTimer tm(TC_FGP, st);
     LT_CUDA(cudaLaunchKernelEx(&cfg, k_fgp, A));
     LT_LAUNCHED();
     return LT_OK;
@@ -225,6 +251,7 @@ int disc_correct(lt_plan& p, const float* d_sino, float* d_pc, float* d_cuser, c
 int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
     if (!p.bank_ready) return fail(LT_ERR_INVALID, "filter bank not computed (lt_filter_bank / lt_set_bank)");
     dim3 grid((p.nd + CV_DB - 1) / CV_DB, p.na, (p.n_iter + CV_KB - 1) / CV_KB);
+    ScopedTimer tm(TC_CONV, st);
     k_conv<<<grid, 256, 0, st>>>(p.na, p.nd, p.n_iter, p.P<float>(p.off.bank), d_pc, p.P<float>(p.off.conv));
     LT_LAUNCHED();
     return LT_OK;
@@ -350,6 +377,28 @@ int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot
 extern "C" {
 
 const char* lt_last_error(void) { return g_err.c_str(); }
+
+void lt_timing_enable(int32_t on) { g_timing = on != 0; }
+
+int lt_timing_read(double* h_ms, int64_t* h_count) {
+    double ms[TC_N] = {0, 0, 0, 0};
+    int64_t cnt[TC_N] = {0, 0, 0, 0};
+    for (auto& r : g_recs) {
+        float t = 0.f;
+        LT_CUDA(cudaEventSynchronize(r.b));
+        LT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.cls] += t;
+        cnt[r.cls] += 1;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    for (int k = 0; k < TC_N; ++k) {
+        if (h_ms) h_ms[k] = ms[k];
+        if (h_count) h_count[k] = cnt[k];
+    }
+    return LT_OK;
+}
 int64_t lt_launch_count(void) { return g_launches.load(); }
 
 int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angles, int32_t n_roi,
