@@ -162,6 +162,131 @@ __global__ void __launch_bounds__(128) k_fp(Geo g, Tiles t, FpArgs f) {
 }
 
 // ---------------------------------------------------------------------------
+// Forward projection W_{L'} for a batch of ROI tiles, shared-memory staged.
+// CTA = (tile r, group of up to FP_GA angles of one orientation); the CTA's
+// 256 threads own the group's rays (angle-major, window bins consecutive in
+// a warp).  The tile is streamed through shared memory in bands of FP_BL
+// lines (rows of y for row-driven angles, rows of the transposed twin for
+// column-driven ones; cp.async double buffering), and every ray accumulates
+// its Joseph taps for the lines of the band it crosses.  Same arithmetic as
+// k_fp (fp64 anchor per ray and band, fp32 offsets < 34 px).
+// ---------------------------------------------------------------------------
+constexpr int FP_GA = 8;     // angles per CTA
+constexpr int FP_BL = 32;    // lines per staged band
+constexpr int FP_U = 16;     // max rays per thread (FP_GA * Wwin <= 256 * FP_U)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(256) k_fp_roi(Geo g, Tiles t, FpArgs f, const int* __restrict__ groups) {
+    extern __shared__ float4 smf4[];
+    float* band = reinterpret_cast<float*>(smf4);          // [2][FP_BL][TP]
+    const int r = blockIdx.y, grp = blockIdx.x;
+    const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
+    __shared__ int sang[FP_GA];
+    if (threadIdx.x < FP_GA) sang[threadIdx.x] = groups[grp * FP_GA + threadIdx.x];
+    __syncthreads();
+    int nga = 0;
+    while (nga < FP_GA && sang[nga] >= 0) ++nga;
+    const int col = g.ang[sang[0]].col;
+    const TileT ti = t.tile[r];
+    const int lv0 = col ? ti.vc0 : ti.vr0, lv1 = col ? ti.vc1 : ti.vr1;
+    const int pv0 = col ? ti.vr0 : ti.vc0, pv1 = col ? ti.vr1 : ti.vc1;
+    const double Lc = 0.5 * (T - 1);
+    const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
+    const int nrays = nga * Wwin;
+
+    // per-ray state
+    float acc[FP_U];
+    double Pw[FP_U];
+    #pragma unroll
+    for (int u = 0; u < FP_U; ++u) {
+        acc[u] = 0.f;
+        const int q = threadIdx.x + 256 * u;
+        Pw[u] = 0.0;
+        if (q < nrays) {
+            const int ga = q / Wwin, w = q - ga * Wwin, a = sang[ga];
+            Pw[u] = Lc + ((double)w - t.tauc[r * na + a]) * g.A64[a];
+        }
+    }
+    // band staging (rows l0 .. l0+FP_BL of the padded source, whole TP width)
+    const int nb4 = FP_BL * TP / 4;
+    auto stage = [&](int buf, int l0) {
+        float* dst = band + buf * FP_BL * TP;
+        const int nl = min(FP_BL, T - l0);
+        const float* s0 = src + (long long)l0 * TP;
+        for (int e = threadIdx.x; e < nb4; e += 256) {
+            const int line = (e * 4) / TP;
+            if (line < nl) cp_async16(dst + e * 4, s0 + e * 4);
+        }
+        cp_async_commit();
+    };
+    const int lbeg = (lv0 / FP_BL) * FP_BL;
+    if (lbeg < lv1) stage(0, lbeg);
+    int buf = 0;
+    for (int l0 = lbeg; l0 < lv1; l0 += FP_BL, buf ^= 1) {
+        if (l0 + FP_BL < lv1) { stage(buf ^ 1, l0 + FP_BL); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        __syncthreads();
+        const float* sb = band + buf * FP_BL * TP + PADL;
+        #pragma unroll
+        for (int u = 0; u < FP_U; ++u) {
+            const int q = threadIdx.x + 256 * u;
+            if (q >= nrays) break;
+            const int ga = q / Wwin, w = q - ga * Wwin, a = sang[ga];
+            const int d = __ldg(t.d0 + r * na + a) + w;
+            if (d < 0 || d >= g.nd) continue;
+            const double B = g.B64[a];
+            // lines of this band the ray can touch: pos(l) in (pv0 - 1, pv1)
+            int la = max(l0, lv0), lb = min(l0 + FP_BL, lv1);
+            if (fabs(B) < 1e-12) {
+                if (!(Pw[u] > pv0 - 1.0 && Pw[u] < (double)pv1)) lb = la;
+            } else {
+                double l1 = Lc + ((pv0 - 1.0) - Pw[u]) / B, l2 = Lc + ((double)pv1 - Pw[u]) / B;
+                if (l1 > l2) { const double tmp = l1; l1 = l2; l2 = tmp; }
+                la = max(la, (int)floor(l1));
+                lb = min(lb, (int)ceil(l2) + 1);
+            }
+            if (la >= lb) continue;
+            const double p0 = Pw[u] + ((double)la - Lc) * B;
+            const double fb = floor(p0);
+            const float f0 = (float)(p0 - fb) - 0.5f;
+            const float Bf = (float)B;
+            const float* rowp = sb + (la - l0) * TP + (int)fb;
+            float a_ = 0.f;
+            const int cnt = lb - la;
+            #pragma unroll 4
+            for (int i = 0; i < cnt; ++i) {
+                const float tt = fmaf((float)i, Bf, f0);
+                const float rm = tt + MAGICF;
+                const int m = __float_as_int(rm) - MAGICI;
+                const float gg = tt - (rm - MAGICF);
+                const float* qp = rowp + i * TP + m;
+                const float v0 = qp[0], v1 = qp[1];
+                a_ = fmaf(0.5f, v0 + v1, a_);
+                a_ = fmaf(gg, v1 - v0, a_);
+            }
+            acc[u] += a_;
+        }
+        __syncthreads();
+    }
+    #pragma unroll
+    for (int u = 0; u < FP_U; ++u) {
+        const int q = threadIdx.x + 256 * u;
+        if (q >= nrays) break;
+        const int ga = q / Wwin, w = q - ga * Wwin, a = sang[ga];
+        const int d = __ldg(t.d0 + r * na + a) + w;
+        const float v = (d >= 0 && d < g.nd) ? acc[u] * g.ang[a].invc : 0.f;
+        f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Backprojection M_{L'} W^T (pixel driven, exact transpose of k_fp) with the
 // fused solver epilogues.  CTA = (tile r, 32x32 sub-tile); thread = 4 pixels
 // of one column.  Per chunk of CA angles the CTA stages, for each angle, the
@@ -312,20 +437,27 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
 // FGP TV prox (Beck & Teboulle, named at P:L661-663; A13/A14),
 // anisotropic, Neumann boundary on each tile's valid rectangle, fused with
 // the FISTA update of Alg. 3 (lines 7-9, corrected per A12).
-// One thread-block CLUSTER per tile: CTA k of K owns a band of RB rows; all
-// FGP state (b, r, s, p_old, q_old, z) lives in shared memory for all n_FGP
-// iterations; the one halo row each phase needs is read from the neighbour
-// CTA's shared memory (DSMEM).  Two cluster barriers per FGP iteration.
+//
+// One thread-block CLUSTER per tile, all FGP state in REGISTERS for all n_FGP
+// iterations.  Thread (j, g) of CTA k owns column j of a strip of FR = 16
+// consecutive rows (strip index k*G + g): b, r, s, p, q, z are 16-entry
+// register arrays.  Neighbours: row above/below = same thread (register) or
+// the adjacent strip's halo row in shared memory -- the CTA's own (g +- 1) or
+// the neighbour CTA's via DSMEM; column left/right = warp shuffle, or the
+// adjacent warp's lane-0/31 halo column in shared memory.  Two cluster
+// barriers per FGP iteration (z needs r above / s left; the dual step needs
+// z below / z right); halos are double buffered by iteration parity.
 // ---------------------------------------------------------------------------
+constexpr int FR = 16;
+
 struct FgpArgs {
     const float* b; int b_pitch; long long b_tstride;   // input image(s)
     const TileT* tiles;                                 // valid rect per tile (nullable: whole H x W)
     int H, W;                                           // when tiles == nullptr
-    int RB, WP;                                         // rows per CTA, smem row pitch
+    int G, NTW;                                         // strips per CTA, threads per strip row (32 | NTW)
     float lam; int nfgp;
-    int mode;                                           // 0: out = x; 1: FISTA epilogue
-    float* out; int out_pitch; long long out_tstride;
-    // FISTA epilogue (mode 1)
+    float* out; int out_pitch; long long out_tstride;   // MODE 0
+    // FISTA epilogue (MODE 1)
     const float* xs; float* xprev; long long p_tstride; int T;
     float* y; float* yT; long long y_tstride; int TP;
     float beta_o;
@@ -333,7 +465,22 @@ struct FgpArgs {
 
 __device__ __forceinline__ float clip1(float v) { return fminf(1.f, fmaxf(-1.f, v)); }
 
-__global__ void __launch_bounds__(256) k_fgp(FgpArgs A) {
+// Cluster barrier between the FGP phases.  LT_FGP_BARRIER 0: cg cluster.sync()
+// (release/acquire at cluster scope; ptxas emits MEMBAR.ALL.GPU);
+// 1: CTA-scope fence + relaxed arrive + acquire wait (experiment).
+#ifndef LT_FGP_BARRIER
+#define LT_FGP_BARRIER 0
+#endif
+__device__ __forceinline__ void fgp_cluster_barrier(cg::cluster_group& cl) {
+#if LT_FGP_BARRIER == 1
+    asm volatile("fence.acq_rel.cta;\n\tbarrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+#else
+    cl.sync();
+#endif
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512, 1) k_fgp(FgpArgs A) {
     extern __shared__ float sm[];
     cg::cluster_group cl = cg::this_cluster();
     const int K = (int)cl.num_blocks();
@@ -344,84 +491,110 @@ __global__ void __launch_bounds__(256) k_fgp(FgpArgs A) {
         const TileT ti = A.tiles[tile];
         vr0 = ti.vr0; vc0 = ti.vc0; Hv = ti.vr1 - ti.vr0; Wv = ti.vc1 - ti.vc0;
     }
-    const int RB = A.RB, WP = A.WP;
-    const int i0 = kr * RB;
-    const int nrows = max(0, min(Hv, i0 + RB) - i0);
-    float* sb = sm;
-    float* sr = sb + RB * WP;
-    float* ss = sr + RB * WP;
-    float* spo = ss + RB * WP;
-    float* sqo = spo + RB * WP;
-    float* sz = sqo + RB * WP;
-    const int tx = threadIdx.x, ty = threadIdx.y;   // blockDim (32, 8)
-    const float lam = A.lam;
+    const int G = A.G, NTW = A.NTW, nw = NTW >> 5;
+    const int j = threadIdx.x, g = threadIdx.y;
+    const int lane = j & 31, warp = j >> 5;
+    const int i0 = (kr * G + g) * FR;
+    const bool colv = j < Wv;
+    // shared-memory halos
+    float* hr = sm;                          // [2][G][NTW] last row of r per strip
+    float* hz = hr + 2 * G * NTW;            // [2][G][NTW] first row of z per strip
+    float* hp = hz + 2 * G * NTW;            // [G][NTW]    last row of p (epilogue)
+    float* cs = hp + G * NTW;                // [2][G][nw][FR] lane-31 column of s per warp
+    float* cz = cs + 2 * G * nw * FR;        // [2][G][nw][FR] lane-0 column of z per warp
+    float* cq = cz + 2 * G * nw * FR;        // [G][nw][FR]    lane-31 column of q (epilogue)
+    float* sb = cq + G * nw * FR;            // [G][FR][NTW]   the input b (read-only, keeps registers free)
+    const int nsm = 5 * G * NTW + 5 * G * nw * FR;
+    for (int e = threadIdx.y * NTW + threadIdx.x; e < nsm; e += NTW * G) sm[e] = 0.f;
 
-    for (int li = ty; li < RB; li += 8)
-        for (int j = tx; j < WP; j += 32) {
-            const int o = li * WP + j;
-            float bv = 0.f;
-            if (li < nrows && j < Wv)
-                bv = A.b[(long long)tile * A.b_tstride + (long long)(vr0 + i0 + li) * A.b_pitch + vc0 + j];
-            sb[o] = bv; sr[o] = 0.f; ss[o] = 0.f; spo[o] = 0.f; sqo[o] = 0.f; sz[o] = 0.f;
-        }
+    float r[FR], s[FR], p[FR], q[FR], z[FR];
+    float* bme = sb + g * FR * NTW + j;
+    const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)(vr0 + i0) * A.b_pitch + vc0 + j;
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) {
+        bme[k * NTW] = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
+        r[k] = 0.f; s[k] = 0.f; p[k] = 0.f; q[k] = 0.f;
+    }
+    unsigned pmask = 0, qmask = 0;      // bit k: p / q defined at row i0 + k
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) {
+        if (colv && i0 + k < Hv - 1) pmask |= 1u << k;
+        if (j < Wv - 1 && i0 + k < Hv) qmask |= 1u << k;
+    }
     cl.sync();
-    const float* prev_r = kr > 0 ? cl.map_shared_rank(sr, kr - 1) : nullptr;
-    const float* prev_po = kr > 0 ? cl.map_shared_rank(spo, kr - 1) : nullptr;
-    const float* next_z = kr + 1 < K ? cl.map_shared_rank(sz, kr + 1) : nullptr;
-    const int next_rows = max(0, min(Hv, i0 + 2 * RB) - (i0 + RB));
-
+    // neighbour strips' halo rows: same CTA (g-1 / g+1) or the adjacent CTA (DSMEM)
+    const float* hr_up = g > 0 ? hr + (g - 1) * NTW : (kr > 0 ? cl.map_shared_rank(hr, kr - 1) + (G - 1) * NTW : nullptr);
+    const float* hz_dn = g < G - 1 ? hz + (g + 1) * NTW : (kr < K - 1 ? cl.map_shared_rank(hz, kr + 1) : nullptr);
+    const float* hp_up = g > 0 ? hp + (g - 1) * NTW : (kr > 0 ? cl.map_shared_rank(hp, kr - 1) + (G - 1) * NTW : nullptr);
+    const int hstride = G * NTW;                 // halo parity stride
+    const int cstride = G * nw * FR;
+    const float lam = A.lam;
     const float gam = lam > 0.f ? 1.f / (8.f * lam) : 0.f;
     const int nit = lam > 0.f ? A.nfgp : 0;
-    double tk = 1.0;
+    float tk = 1.f;
     for (int it = 0; it < nit; ++it) {
-        // phase A: z = b - lam L(r, s)
-        for (int li = ty; li < nrows; li += 8) {
-            const int i = i0 + li;
-            for (int j = tx; j < Wv; j += 32) {
-                const int o = li * WP + j;
-                float rup = 0.f;
-                if (li > 0) rup = sr[o - WP];
-                else if (i > 0) rup = prev_r[(RB - 1) * WP + j];
-                const float sl = j > 0 ? ss[o - 1] : 0.f;
-                sz[o] = sb[o] - lam * (sr[o] + ss[o] - rup - sl);
-            }
+        const int cb = it & 1, pb = cb ^ 1;
+        // ---- phase A: z = b - lam L(r, s)
+        const float rabove = hr_up ? hr_up[pb * hstride + j] : 0.f;
+        const float* csl = cs + pb * cstride + (g * nw + warp - 1) * FR;
+        #pragma unroll
+        for (int k = 0; k < FR; ++k) {
+            const float rup = k > 0 ? r[k - 1] : rabove;
+            float sl = __shfl_up_sync(0xffffffffu, s[k], 1);
+            if (lane == 0) sl = warp > 0 ? csl[k] : 0.f;
+            z[k] = bme[k * NTW] - lam * (r[k] + s[k] - rup - sl);
         }
-        cl.sync();
-        // phase B: dual step, projection, momentum
-        const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tk * tk));
-        const float beta = (float)((tk - 1.0) / tn);
+        hz[cb * hstride + g * NTW + j] = z[0];
+        if (lane == 0) {
+            float* czw = cz + cb * cstride + (g * nw + warp) * FR;
+            #pragma unroll
+            for (int k = 0; k < FR; ++k) czw[k] = z[k];
+        }
+        fgp_cluster_barrier(cl);
+        // ---- phase B: dual ascent, projection on [-1,1], FGP momentum
+        const float tn = 0.5f * (1.f + sqrtf(1.f + 4.f * tk * tk));
+        const float beta = (tk - 1.f) / tn;
         tk = tn;
-        for (int li = ty; li < nrows; li += 8) {
-            const int i = i0 + li;
-            for (int j = tx; j < Wv; j += 32) {
-                const int o = li * WP + j;
-                const float zc = sz[o];
-                float pn = 0.f, qn = 0.f;
-                if (i < Hv - 1) {
-                    const float zd = (li + 1 < nrows) ? sz[o + WP] : next_z[j];
-                    pn = clip1(sr[o] + gam * (zc - zd));
-                }
-                if (j < Wv - 1) qn = clip1(ss[o] + gam * (zc - sz[o + 1]));
-                sr[o] = pn + beta * (pn - spo[o]);
-                ss[o] = qn + beta * (qn - sqo[o]);
-                spo[o] = pn;
-                sqo[o] = qn;
-            }
+        const float zbelow = hz_dn ? hz_dn[cb * hstride + j] : 0.f;
+        const float* czr = cz + cb * cstride + (g * nw + warp + 1) * FR;
+        #pragma unroll
+        for (int k = 0; k < FR; ++k) {
+            const float zd = k < FR - 1 ? z[k + 1] : zbelow;
+            float zr = __shfl_down_sync(0xffffffffu, z[k], 1);
+            if (lane == 31) zr = warp < nw - 1 ? czr[k] : 0.f;
+            const float pn = (pmask >> k) & 1u ? clip1(r[k] + gam * (z[k] - zd)) : 0.f;
+            const float qn = (qmask >> k) & 1u ? clip1(s[k] + gam * (z[k] - zr)) : 0.f;
+            r[k] = pn + beta * (pn - p[k]);
+            s[k] = qn + beta * (qn - q[k]);
+            p[k] = pn;
+            q[k] = qn;
         }
-        cl.sync();
+        hr[cb * hstride + g * NTW + j] = r[FR - 1];
+        if (lane == 31) {
+            float* csw = cs + cb * cstride + (g * nw + warp) * FR;
+            #pragma unroll
+            for (int k = 0; k < FR; ++k) csw[k] = s[k];
+        }
+        fgp_cluster_barrier(cl);
     }
-    (void)next_rows;
-    // x = b - lam L(p, q), then the epilogue
-    for (int li = ty; li < nrows; li += 8) {
-        const int i = i0 + li;
-        for (int j = tx; j < Wv; j += 32) {
-            const int o = li * WP + j;
-            float pup = 0.f;
-            if (li > 0) pup = spo[o - WP];
-            else if (i > 0) pup = prev_po[(RB - 1) * WP + j];
-            const float ql = j > 0 ? sqo[o - 1] : 0.f;
-            const float x = sb[o] - lam * (spo[o] + sqo[o] - pup - ql);
-            if (A.mode == 0) {
+    // ---- x = b - lam L(p, q), then the epilogue
+    hp[g * NTW + j] = p[FR - 1];
+    if (lane == 31) {
+        #pragma unroll
+        for (int k = 0; k < FR; ++k) cq[(g * nw + warp) * FR + k] = q[k];
+    }
+    cl.sync();
+    const float pabove = hp_up ? hp_up[j] : 0.f;
+    const float* cql = cq + (g * nw + warp - 1) * FR;
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) {
+        const float pup = k > 0 ? p[k - 1] : pabove;
+        float ql = __shfl_up_sync(0xffffffffu, q[k], 1);
+        if (lane == 0) ql = warp > 0 ? cql[k] : 0.f;
+        const float x = bme[k * NTW] - lam * (p[k] + q[k] - pup - ql);
+        const int i = i0 + k;
+        if (colv && i < Hv) {
+            if (MODE == 0) {
                 A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + j] = x;
             } else {
                 const int ti_ = vr0 + i, tj = vc0 + j;                 // tile-local coords

@@ -85,6 +85,8 @@ struct lt_plan {
     std::vector<TileT> tiles, gtile;
     std::vector<int> d0, gd0;
     std::vector<double> tauc, gtauc;
+    std::vector<int> fpgroups;    // [ngroups][FP_GA] angle indices of one orientation, -1 padded
+    int ngroups = 0;
     // workspace
     char* ws = nullptr;
     int64_t ws_bytes = 0;
@@ -92,7 +94,7 @@ struct lt_plan {
     int last_mode = -1;
     int stitch_cap = 0;           // max list entries
     struct {
-        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc;
+        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
@@ -149,6 +151,22 @@ int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, cons
     return LT_OK;
 }
 
+// ROI-batch forward projection (shared-memory staged; falls back to the
+// direct-read kernel when the staged band would not fit)
+int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
+                  float* out, long long out_ts, cudaStream_t st) {
+    const size_t smem = (size_t)2 * FP_BL * t.TP * sizeof(float);
+    if (smem > 160 * 1024 || (long long)FP_GA * t.Wwin > 256LL * FP_U)
+        return launch_fp(p, 0, t, img, imgT, img_ts, out, out_ts, nullptr, nullptr, st);
+    LT_CUDA(cudaFuncSetAttribute(k_fp_roi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
+    dim3 grid(p.ngroups, t.ntiles);
+    ScopedTimer tm(TC_FP, st);
+    k_fp_roi<<<grid, 256, smem, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
 template <int NS, int MODE>
 int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const SinoView& s2, const BpEpi& e,
                 cudaStream_t st) {
@@ -175,43 +193,47 @@ SinoView view_win(const float* base, int Wwin, int na) {
     return SinoView{base, (long long)na * Wwin, Wwin, 0, Wwin};
 }
 
-// FGP cluster configuration: K CTAs, RB rows each, pitch WP, 6 arrays in smem
-int fgp_config(int rows, int cols, int* K, int* RB, int* WP, size_t* smem) {
-    const int wp = cols;
-    for (int k = 1; k <= 16; k *= 2) {
-        const int rb = (rows + k - 1) / k;
-        const size_t bytes = (size_t)6 * rb * wp * sizeof(float);
-        if (bytes <= 200 * 1024) {
-            *K = k; *RB = rb; *WP = wp; *smem = bytes;
-            return LT_OK;
-        }
-    }
-    return fail(LT_ERR_INVALID, "FGP tile %dx%d too large for a 16-CTA cluster", rows, cols);
+// FGP cluster configuration (k_fgp): NTW threads per strip row (one per
+// column), strips of FR rows, G strips per CTA (<= 512 threads), K CTAs per
+// cluster covering all rows of a tile.
+struct FgpCfg { int NTW, G, K; size_t smem; };
+
+int fgp_config(int rows, int cols, FgpCfg* c) {
+    if (rows < 1 || cols < 1 || cols > 512) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
+    const int ntw = 32 * ((cols + 31) / 32);
+    const int strips = (rows + FR - 1) / FR;
+    const int G = std::max(1, std::min(strips, 512 / ntw));
+    const int K = (strips + G - 1) / G;
+    if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
+    const int nw = ntw / 32;
+    c->NTW = ntw; c->G = G; c->K = K;
+    c->smem = (size_t)(5 * G * ntw + 5 * G * nw * FR + G * FR * ntw) * sizeof(float);
+    return LT_OK;
 }
 
+template <int MODE>
 int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
-    int K, RB, WP;
-    size_t smem;
-    if (int rc = fgp_config(rows, cols, &K, &RB, &WP, &smem)) return rc;
-    A.RB = RB;
-    A.WP = WP;
-    LT_CUDA(cudaFuncSetAttribute(k_fgp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (K > 8) LT_CUDA(cudaFuncSetAttribute(k_fgp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    FgpCfg c;
+    if (int rc = fgp_config(rows, cols, &c)) return rc;
+    A.G = c.G;
+    A.NTW = c.NTW;
+    LT_CUDA(cudaFuncSetAttribute(k_fgp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+    if (c.K > 8) LT_CUDA(cudaFuncSetAttribute(k_fgp<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
-    cfg.gridDim = dim3(K, ntiles, 1);
-    cfg.blockDim = dim3(32, 8, 1);
-    cfg.dynamicSmemBytes = smem;
+    cfg.gridDim = dim3(c.K, ntiles, 1);
+    cfg.blockDim = dim3(c.NTW, c.G, 1);
+    cfg.dynamicSmemBytes = c.smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = K;
+    attr[0].val.clusterDim.x = c.K;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ScopedTimer tm(TC_FGP, st);
-    LT_CUDA(cudaLaunchKernelEx(&cfg, k_fgp, A));
+    LT_CUDA(cudaLaunchKernelEx(&cfg, k_fgp<MODE>, A));
     LT_LAUNCHED();
     return LT_OK;
 }
@@ -283,7 +305,7 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
             if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vb, vb, e, st)) return rc; }
             else { if (int rc = launch_bp_t<1, BP_TV>(p, t, vb, vb, e, st)) return rc; }
         } else {
-            if (int rc = launch_fp(p, 0, t, y, yT, yts, s, (long long)p.na * p.Wwin, nullptr, nullptr, st)) return rc;
+            if (int rc = launch_fp_roi(p, t, y, yT, yts, s, (long long)p.na * p.Wwin, st)) return rc;
             const SinoView vs = view_win(s, p.Wwin, p.na);
             if (mode == 0) { if (int rc = launch_bp_t<2, BP_BOX>(p, t, vb, vs, e, st)) return rc; }
             else { if (int rc = launch_bp_t<2, BP_TV>(p, t, vb, vs, e, st)) return rc; }
@@ -296,11 +318,11 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
             memset(&A, 0, sizeof A);
             A.b = p.P<float>(p.off.v); A.b_pitch = p.T; A.b_tstride = p.ptile();
             A.tiles = p.P<TileT>(p.off.tiles);
-            A.lam = lam; A.nfgp = nfgp; A.mode = 1;
+            A.lam = lam; A.nfgp = nfgp;
             A.xs = p.P<float>(p.off.xs); A.xprev = p.P<float>(p.off.xprev); A.p_tstride = p.ptile(); A.T = p.T;
             A.y = y; A.yT = yT; A.y_tstride = yts; A.TP = p.TP;
             A.beta_o = (float)beta;
-            if (int rc = launch_fgp(A, p.T, p.T, p.R, st)) return rc;
+            if (int rc = launch_fgp<1>(A, p.T, p.T, p.R, st)) return rc;
         }
     }
     p.last_mode = mode;
@@ -422,7 +444,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
             return fail(LT_ERR_INVALID, "ROI %d core outside the grid", r);
     lt_plan* p = new lt_plan();
     p->n = n; p->na = n_angles; p->nd = n_det; p->nroi_all = n_roi; p->radius = radius; p->margin = margin;
-    p->h = radius + margin; p->T = 2 * p->h; p->TP = p->T + PADL + PADR;
+    p->h = radius + margin; p->T = 2 * p->h; p->TP = (p->T + PADL + PADR + 3) & ~3;   // 16-byte rows (cp.async)
     p->Wwin = window_width(p->h);
     p->n_iter = n_iter; p->flags = flags; p->rank = rank; p->world = world;
     p->GT = n; p->GTP = n + PADL + PADR;
@@ -484,6 +506,20 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         // tile centre point (x, y) = (cc - N/2, N/2 - cr)
         tile_window(*p, cc - 0.5 * n, 0.5 * n - cr, p->Wwin, &p->d0[(size_t)q * n_angles], &p->tauc[(size_t)q * n_angles]);
     }
+    // forward-projection angle groups: one orientation per group
+    for (int o = 0; o < 2; ++o) {
+        std::vector<int> cur;
+        for (int a = 0; a < n_angles; ++a)
+            if (p->angf[a].col == o) {
+                cur.push_back(a);
+                if ((int)cur.size() == FP_GA) { p->fpgroups.insert(p->fpgroups.end(), cur.begin(), cur.end()); cur.clear(); }
+            }
+        if (!cur.empty()) {
+            cur.resize(FP_GA, -1);
+            p->fpgroups.insert(p->fpgroups.end(), cur.begin(), cur.end());
+        }
+    }
+    p->ngroups = (int)p->fpgroups.size() / FP_GA;
     // global tile: the whole grid, window = the full detector
     {
         TileT t;
@@ -506,6 +542,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.cs64 = take(n_angles * 8); f.sn64 = take(n_angles * 8); f.A64 = take(n_angles * 8); f.B64 = take(n_angles * 8);
     f.tiles = take(R * sizeof(TileT)); f.d0 = take(R * n_angles * 4); f.tauc = take(R * n_angles * 8);
     f.gtile = take(sizeof(TileT)); f.gd0 = take(n_angles * 4); f.gtauc = take(n_angles * 8);
+    f.fpgroups = take(p->fpgroups.size() * 4);
     f.bank = take((size_t)n_iter * ns * fs); f.conv = take((size_t)n_iter * ns * fs);
     f.pc = take(ns * fs); f.wd = take(ns * fs); f.wdsum = take(n_angles * 8); f.psum = take(n_angles * 8);
     f.discc64 = take(8); f.discc32 = take(4); f.err = take(4);
@@ -548,6 +585,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(up(p->off.gtile, p->gtile.data(), sizeof(TileT)));
     LT_CUDA(up(p->off.gd0, p->gd0.data(), na * 4));
     LT_CUDA(up(p->off.gtauc, p->gtauc.data(), na * 8));
+    LT_CUDA(up(p->off.fpgroups, p->fpgroups.data(), p->fpgroups.size() * 4));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.discc32, 0, 4, st));
     LT_CUDA(cudaStreamSynchronize(st));
@@ -653,7 +691,7 @@ int lt_project(const lt_plan* cp, int32_t roi, const float* d_img, float* d_sino
     // single-tile view of this ROI's tables
     Tiles t = p->roi_tiles();
     t.tile += roi; t.d0 += (size_t)roi * p->na; t.tauc += (size_t)roi * p->na; t.ntiles = 1;
-    if (int rc = launch_fp(*p, 0, t, tt, ttT, 0, tw, 0, nullptr, nullptr, st)) return rc;
+    if (int rc = launch_fp_roi(*p, t, tt, ttT, 0, tw, 0, st)) return rc;
     k_scatter_win<<<dim3((p->nd + 255) / 256, p->na), 256, 0, st>>>(p->na, p->nd, p->Wwin, t.d0, tw, d_sino);
     LT_LAUNCHED();
     return LT_OK;
@@ -706,8 +744,8 @@ int lt_tv_solve(lt_plan* p, const float* d_sino, float lambda, int32_t n_fgp, fl
     if (int rc = check_plan(p)) return rc;
     if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
     if (!(lambda >= 0.f) || n_fgp < 1) return fail(LT_ERR_INVALID, "lambda >= 0 and n_fgp >= 1 required");
-    int K, RB, WP; size_t sm;
-    if (int rc = fgp_config(p->T, p->T, &K, &RB, &WP, &sm)) return rc;
+    FgpCfg fc;
+    if (int rc = fgp_config(p->T, p->T, &fc)) return rc;
     if (p->R == 0) return LT_OK;
     return solve(*p, 1, d_sino, lambda, 0.f, n_fgp, d_cores, (cudaStream_t)stream);
 }
@@ -839,9 +877,9 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
     memset(&A, 0, sizeof A);
     A.b = d_in; A.b_pitch = w; A.b_tstride = (long long)h * w;
     A.tiles = nullptr; A.H = h; A.W = w;
-    A.lam = lambda; A.nfgp = n_fgp; A.mode = 0;
+    A.lam = lambda; A.nfgp = n_fgp;
     A.out = d_out; A.out_pitch = w; A.out_tstride = (long long)h * w;
-    return launch_fgp(A, h, w, count, (cudaStream_t)stream);
+    return launch_fgp<0>(A, h, w, count, (cudaStream_t)stream);
 }
 
 void lt_plan_destroy(lt_plan* p) { delete p; }
