@@ -171,9 +171,9 @@ __global__ void __launch_bounds__(128) k_fp(Geo g, Tiles t, FpArgs f) {
 // its Joseph taps for the lines of the band it crosses.  Same arithmetic as
 // k_fp (fp64 anchor per ray and band, fp32 offsets < 34 px).
 // ---------------------------------------------------------------------------
-constexpr int FP_GA = 8;     // angles per CTA
-constexpr int FP_BL = 32;    // lines per staged band
-constexpr int FP_U = 16;     // max rays per thread (FP_GA * Wwin <= 256 * FP_U)
+constexpr int FP_GA = 8;     // angles per CTA (one warp per angle)
+constexpr int FP_BL = 16;    // lines per staged band
+constexpr int FP_U = 12;     // rays per lane: window width <= 32 * FP_U
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -183,46 +183,73 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+constexpr int FP_P = 264;    // shared-memory band pitch (floats): tiles up to T = 256
+
+// one ray through the 32 lines of a staged band: Joseph taps at
+// pos(i) = base + f0 + 0.5 + i*B, fully unrolled, row offsets are immediates
+__device__ __forceinline__ unsigned opaque_u32(unsigned x) {
+    unsigned y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));   // keeps ptxas from splitting the folded bias
+    return y;
+}
+
+template <bool CLAMP>
+__device__ __forceinline__ float fp_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
+    // a shuffled copy is not rematerialized by ptxas, so the folded bias stays in one register
+    const unsigned rowbase = __shfl_sync(0xffffffffu, rowbase_, threadIdx.x & 31);
+    float acc = 0.f;
+    #pragma unroll
+    for (int i = 0; i < FP_BL; ++i) {
+        float tt = fmaf((float)i, Bf, f0);
+        if (CLAMP) tt = fminf(fmaxf(tt, lo), hi);
+        const float rm = tt + MAGICF;
+        unsigned addr;
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(__float_as_int(rm)), "r"(rowbase));
+        const float gg = tt - (rm - MAGICF);
+        float v0, v1;
+        const unsigned ai = addr + (unsigned)(i * FP_P * 4);
+        asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];" : "=f"(v0), "=f"(v1) : "r"(ai));
+        acc = fmaf(0.5f, v0 + v1, acc);
+        acc = fmaf(gg, v1 - v0, acc);
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(256) k_fp_roi(Geo g, Tiles t, FpArgs f, const int* __restrict__ groups) {
     extern __shared__ float4 smf4[];
-    float* band = reinterpret_cast<float*>(smf4);          // [2][FP_BL][TP]
+    float* band = reinterpret_cast<float*>(smf4);          // [2][FP_BL][FP_P]
     const int r = blockIdx.y, grp = blockIdx.x;
     const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
-    __shared__ int sang[FP_GA];
-    if (threadIdx.x < FP_GA) sang[threadIdx.x] = groups[grp * FP_GA + threadIdx.x];
-    __syncthreads();
-    int nga = 0;
-    while (nga < FP_GA && sang[nga] >= 0) ++nga;
-    const int col = g.ang[sang[0]].col;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a = groups[grp * FP_GA + warp];                 // this warp's angle (-1: idle warp)
+    const int a0 = groups[grp * FP_GA];
+    const int col = g.ang[a0].col;
     const TileT ti = t.tile[r];
     const int lv0 = col ? ti.vc0 : ti.vr0, lv1 = col ? ti.vc1 : ti.vr1;
     const int pv0 = col ? ti.vr0 : ti.vc0, pv1 = col ? ti.vr1 : ti.vc1;
     const double Lc = 0.5 * (T - 1);
     const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
-    const int nrays = nga * Wwin;
-
-    // per-ray state
-    float acc[FP_U];
-    double Pw[FP_U];
-    #pragma unroll
-    for (int u = 0; u < FP_U; ++u) {
-        acc[u] = 0.f;
-        const int q = threadIdx.x + 256 * u;
-        Pw[u] = 0.0;
-        if (q < nrays) {
-            const int ga = q / Wwin, w = q - ga * Wwin, a = sang[ga];
-            Pw[u] = Lc + ((double)w - t.tauc[r * na + a]) * g.A64[a];
-        }
+    double A = 0.0, B = 0.0, tauc = 0.0;
+    int d0 = 0;
+    if (a >= 0) {
+        A = g.A64[a]; B = g.B64[a];
+        tauc = t.tauc[r * na + a];
+        d0 = __ldg(t.d0 + r * na + a);
     }
-    // band staging (rows l0 .. l0+FP_BL of the padded source, whole TP width)
-    const int nb4 = FP_BL * TP / 4;
+    const float Bf = (float)B;
+    __shared__ float sacc[FP_GA][32 * FP_U];                 // per-ray accumulators
+    for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += 256) (&sacc[0][0])[e] = 0.f;
+    float* acc = sacc[warp];
+
+    const int q4 = TP / 4;       // float4 per staged line
     auto stage = [&](int buf, int l0) {
-        float* dst = band + buf * FP_BL * TP;
+        float* dst = band + buf * FP_BL * FP_P;
         const int nl = min(FP_BL, T - l0);
         const float* s0 = src + (long long)l0 * TP;
-        for (int e = threadIdx.x; e < nb4; e += 256) {
-            const int line = (e * 4) / TP;
-            if (line < nl) cp_async16(dst + e * 4, s0 + e * 4);
+        for (int e = threadIdx.x; e < FP_BL * q4; e += 256) {
+            const int line = e / q4, c4 = e - line * q4;
+            if (line < nl) cp_async16(dst + line * FP_P + c4 * 4, s0 + (long long)line * TP + c4 * 4);
+            else reinterpret_cast<float4*>(dst + line * FP_P)[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         cp_async_commit();
     };
@@ -233,56 +260,46 @@ __global__ void __launch_bounds__(256) k_fp_roi(Geo g, Tiles t, FpArgs f, const 
         if (l0 + FP_BL < lv1) { stage(buf ^ 1, l0 + FP_BL); cp_async_wait<1>(); }
         else cp_async_wait<0>();
         __syncthreads();
-        const float* sb = band + buf * FP_BL * TP + PADL;
-        #pragma unroll
-        for (int u = 0; u < FP_U; ++u) {
-            const int q = threadIdx.x + 256 * u;
-            if (q >= nrays) break;
-            const int ga = q / Wwin, w = q - ga * Wwin, a = sang[ga];
-            const int d = __ldg(t.d0 + r * na + a) + w;
-            if (d < 0 || d >= g.nd) continue;
-            const double B = g.B64[a];
-            // lines of this band the ray can touch: pos(l) in (pv0 - 1, pv1)
-            int la = max(l0, lv0), lb = min(l0 + FP_BL, lv1);
-            if (fabs(B) < 1e-12) {
-                if (!(Pw[u] > pv0 - 1.0 && Pw[u] < (double)pv1)) lb = la;
-            } else {
-                double l1 = Lc + ((pv0 - 1.0) - Pw[u]) / B, l2 = Lc + ((double)pv1 - Pw[u]) / B;
-                if (l1 > l2) { const double tmp = l1; l1 = l2; l2 = tmp; }
-                la = max(la, (int)floor(l1));
-                lb = min(lb, (int)ceil(l2) + 1);
+        if (a >= 0) {
+            const unsigned sbase = (unsigned)__cvta_generic_to_shared(band + buf * FP_BL * FP_P + PADL);
+            const double Bl = (double)(FP_BL - 1) * B;
+            #pragma unroll 1
+            for (int u = 0; u < FP_U; ++u) {
+                const int w = lane + 32 * u;
+                const int d = d0 + w;
+                const bool ray = w < Wwin && d >= 0 && d < g.nd;
+                // position (pixel index along the line) of the ray at the band's first line
+                const double p0 = Lc + ((double)w - tauc) * A + ((double)l0 - Lc) * B;
+                const double pmin = fmin(p0, p0 + Bl), pmax = fmax(p0, p0 + Bl);
+                const bool useful = ray && pmax > pv0 - 2.0 && pmin < (double)pv1 + 1.0;
+                if (!__any_sync(0xffffffffu, useful)) continue;
+                const bool safe = pmin >= -3.0 && pmax <= (double)T + 1.5;
+                const double fb = floor(p0);
+                // lanes without a useful ray read a fixed in-bounds spot (pos = 0, step 0)
+                const int ib = useful ? (int)fb : 0;
+                const float f0 = useful ? (float)(p0 - fb) - 0.5f : -0.5f;
+                const float Bu = useful ? Bf : 0.f;
+                // rowbase folds the magic-number bias: addr = rowbase + 4*bits(tt + MAGIC)
+                const unsigned rowbase = sbase + 4u * (unsigned)(ib - MAGICI);
+                float v;
+                if (__all_sync(0xffffffffu, safe || !useful)) {
+                    v = fp_band_ray<false>(rowbase, f0, Bu, 0.f, 0.f);
+                } else {
+                    // clamp into the zero padding: pos in [-3, T + 2) relative to ib
+                    const float lo = (float)(-3 - ib) - 0.5f, hi = (float)(T + 2 - ib) - 0.5f;
+                    v = fp_band_ray<true>(rowbase, f0, Bu, lo, hi);
+                }
+                if (useful) acc[w] += v;
             }
-            if (la >= lb) continue;
-            const double p0 = Pw[u] + ((double)la - Lc) * B;
-            const double fb = floor(p0);
-            const float f0 = (float)(p0 - fb) - 0.5f;
-            const float Bf = (float)B;
-            const float* rowp = sb + (la - l0) * TP + (int)fb;
-            float a_ = 0.f;
-            const int cnt = lb - la;
-            #pragma unroll 4
-            for (int i = 0; i < cnt; ++i) {
-                const float tt = fmaf((float)i, Bf, f0);
-                const float rm = tt + MAGICF;
-                const int m = __float_as_int(rm) - MAGICI;
-                const float gg = tt - (rm - MAGICF);
-                const float* qp = rowp + i * TP + m;
-                const float v0 = qp[0], v1 = qp[1];
-                a_ = fmaf(0.5f, v0 + v1, a_);
-                a_ = fmaf(gg, v1 - v0, a_);
-            }
-            acc[u] += a_;
         }
         __syncthreads();
     }
-    #pragma unroll
-    for (int u = 0; u < FP_U; ++u) {
-        const int q = threadIdx.x + 256 * u;
-        if (q >= nrays) break;
-        const int ga = q / Wwin, w = q - ga * Wwin, a = sang[ga];
-        const int d = __ldg(t.d0 + r * na + a) + w;
-        const float v = (d >= 0 && d < g.nd) ? acc[u] * g.ang[a].invc : 0.f;
-        f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = v;
+    if (a >= 0) {
+        const float invc = g.ang[a].invc;
+        for (int w = lane; w < Wwin; w += 32) {
+            const int d = d0 + w;
+            f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = (d >= 0 && d < g.nd) ? acc[w] * invc : 0.f;
+        }
     }
 }
 
@@ -356,22 +373,26 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
             sw[q][w] = make_float2(v1, v2);
         }
         __syncthreads();
+        const unsigned swbase = opaque_u32((unsigned)__cvta_generic_to_shared(&sw[0][0]) - 8u * (unsigned)MAGICI);
         #pragma unroll 2
         for (int q = 0; q < ca; ++q) {
             const float4 A4 = sa[q];
             const float t0 = fmaf(dx, A4.x, fmaf(-dy0, A4.y, sanch[q]));
-            const float2* row = sw[q];
+            const unsigned rowb = opaque_u32(swbase + (unsigned)(q * BP_SW * 8));
             #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const float tt = fmaf(-(float)p, A4.y, t0);
                 const float rm = tt + MAGICF;
-                const int m = __float_as_int(rm) - MAGICI;
                 const float gg = tt - (rm - MAGICF);
+                unsigned addr;
+                asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(addr) : "r"(__float_as_int(rm)), "r"(rowb));
                 const float w0 = fmaxf(0.f, fmaf(-gg, A4.w, A4.z));
                 const float w1 = fmaxf(0.f, fmaf(gg, A4.w, A4.z));
-                const float2 b0 = row[m], b1 = row[m + 1];
-                g1[p] = fmaf(w0, b0.x, fmaf(w1, b1.x, g1[p]));
-                if (NS == 2) g2[p] = fmaf(w0, b0.y, fmaf(w1, b1.y, g2[p]));
+                float b0x, b0y, b1x, b1y;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%4];\n\tld.shared.v2.f32 {%2, %3}, [%4+8];"
+                             : "=f"(b0x), "=f"(b0y), "=f"(b1x), "=f"(b1y) : "r"(addr));
+                g1[p] = fmaf(w0, b0x, fmaf(w1, b1x, g1[p]));
+                if (NS == 2) g2[p] = fmaf(w0, b0y, fmaf(w1, b1y, g2[p]));
             }
         }
     }
@@ -479,9 +500,36 @@ __device__ __forceinline__ void fgp_cluster_barrier(cg::cluster_group& cl) {
 #endif
 }
 
+// DSMEM push with transaction-count completion (sm_90+): a producer stores one
+// float into a neighbour CTA's shared memory and the bytes complete on the
+// neighbour's mbarrier; the consumer waits on its own mbarrier (acquire).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa(unsigned a, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_f32(unsigned remote, float v, unsigned remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];"
+                 ::"r"(remote), "f"(v), "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(512, 1) k_fgp(FgpArgs A) {
-    extern __shared__ float sm[];
+__global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
+    extern __shared__ __align__(16) float sm[];
     cg::cluster_group cl = cg::this_cluster();
     const int K = (int)cl.num_blocks();
     const int kr = (int)cl.block_rank();
@@ -496,16 +544,25 @@ __global__ void __launch_bounds__(512, 1) k_fgp(FgpArgs A) {
     const int lane = j & 31, warp = j >> 5;
     const int i0 = (kr * G + g) * FR;
     const bool colv = j < Wv;
-    // shared-memory halos
-    float* hr = sm;                          // [2][G][NTW] last row of r per strip
+    const bool has_up = kr > 0, has_dn = kr < K - 1;
+    // shared memory
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm);   // [0,1] r from above, [2,3] z from below
+    float* rx_r = sm + 8;                    // [2][NTW] last r row of the CTA above (st.async target)
+    float* rx_z = rx_r + 2 * NTW;            // [2][NTW] first z row of the CTA below
+    float* hr = rx_z + 2 * NTW;              // [2][G][NTW] last row of r per strip
     float* hz = hr + 2 * G * NTW;            // [2][G][NTW] first row of z per strip
     float* hp = hz + 2 * G * NTW;            // [G][NTW]    last row of p (epilogue)
-    float* cs = hp + G * NTW;                // [2][G][nw][FR] lane-31 column of s per warp
-    float* cz = cs + 2 * G * nw * FR;        // [2][G][nw][FR] lane-0 column of z per warp
-    float* cq = cz + 2 * G * nw * FR;        // [G][nw][FR]    lane-31 column of q (epilogue)
-    float* sb = cq + G * nw * FR;            // [G][FR][NTW]   the input b (read-only, keeps registers free)
-    const int nsm = 5 * G * NTW + 5 * G * nw * FR;
-    for (int e = threadIdx.y * NTW + threadIdx.x; e < nsm; e += NTW * G) sm[e] = 0.f;
+    float* cs = hp + G * NTW;                // [2][G][nw+1][FR] slot w+1: lane-31 column of s of warp w; slot 0 zero
+    float* cz = cs + 2 * G * (nw + 1) * FR;  // [2][G][nw+1][FR] slot w: lane-0 column of z of warp w; slot nw zero
+    float* cq = cz + 2 * G * (nw + 1) * FR;  // [G][nw][FR]    lane-31 column of q (epilogue)
+    float* sb = cq + G * nw * FR;            // [G][FR][NTW]   the input b
+    const int nzero = 4 * NTW + 5 * G * NTW + 4 * G * (nw + 1) * FR + G * nw * FR;
+    const int tid = g * NTW + j, nthr = NTW * G;
+    for (int e = tid; e < nzero; e += nthr) rx_r[e] = 0.f;
+    if (tid == 0) {
+        for (int q = 0; q < 4; ++q) mbar_init(smem_u32(bars + q), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     float r[FR], s[FR], p[FR], q[FR], z[FR];
     float* bme = sb + g * FR * NTW + j;
@@ -515,67 +572,137 @@ __global__ void __launch_bounds__(512, 1) k_fgp(FgpArgs A) {
         bme[k * NTW] = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
         r[k] = 0.f; s[k] = 0.f; p[k] = 0.f; q[k] = 0.f;
     }
-    unsigned pmask = 0, qmask = 0;      // bit k: p / q defined at row i0 + k
-    #pragma unroll
-    for (int k = 0; k < FR; ++k) {
-        if (colv && i0 + k < Hv - 1) pmask |= 1u << k;
-        if (j < Wv - 1 && i0 + k < Hv) qmask |= 1u << k;
-    }
-    cl.sync();
-    // neighbour strips' halo rows: same CTA (g-1 / g+1) or the adjacent CTA (DSMEM)
-    const float* hr_up = g > 0 ? hr + (g - 1) * NTW : (kr > 0 ? cl.map_shared_rank(hr, kr - 1) + (G - 1) * NTW : nullptr);
-    const float* hz_dn = g < G - 1 ? hz + (g + 1) * NTW : (kr < K - 1 ? cl.map_shared_rank(hz, kr + 1) : nullptr);
-    const float* hp_up = g > 0 ? hp + (g - 1) * NTW : (kr > 0 ? cl.map_shared_rank(hp, kr - 1) + (G - 1) * NTW : nullptr);
-    const int hstride = G * NTW;                 // halo parity stride
-    const int cstride = G * nw * FR;
+    // step sizes with the boundary masks folded in: gamma = 0 where the dual
+    // component does not exist (p: rows >= Hv-1 or invalid column; q: column
+    // >= Wv-1 or invalid row); a dual that starts at 0 with step 0 stays 0.
     const float lam = A.lam;
     const float gam = lam > 0.f ? 1.f / (8.f * lam) : 0.f;
+    const float gq_col = (j < Wv - 1) ? gam : 0.f;
+    const float gp_col = colv ? gam : 0.f;
+    const int kp = Hv - 1 - i0;                 // rows k < kp have p
+    const int kq = Hv - i0;                     // rows k < kq have q
+    cl.sync();
+    const unsigned up_rank = has_up ? kr - 1 : kr, dn_rank = has_dn ? kr + 1 : kr;
+    // remote targets: my last strip pushes r to the CTA below, my first strip pushes z to the CTA above
+    const unsigned rem_rx_r = mapa(smem_u32(rx_r + j), dn_rank);
+    const unsigned rem_bar_r = mapa(smem_u32(bars + 0), dn_rank);
+    const unsigned rem_rx_z = mapa(smem_u32(rx_z + j), up_rank);
+    const unsigned rem_bar_z = mapa(smem_u32(bars + 2), up_rank);
+    const unsigned row_bytes = NTW * 4;
+    const int hstride = G * NTW;
+    const int cstride = G * (nw + 1) * FR;
     const int nit = lam > 0.f ? A.nfgp : 0;
     float tk = 1.f;
     for (int it = 0; it < nit; ++it) {
         const int cb = it & 1, pb = cb ^ 1;
+        if (tid == 0) {
+            if (has_dn) mbar_expect_tx(smem_u32(bars + 2 + cb), row_bytes);   // z row of it, from below
+            if (has_up) mbar_expect_tx(smem_u32(bars + cb), row_bytes);       // r row of it, from above
+        }
         // ---- phase A: z = b - lam L(r, s)
-        const float rabove = hr_up ? hr_up[pb * hstride + j] : 0.f;
-        const float* csl = cs + pb * cstride + (g * nw + warp - 1) * FR;
+
+        // left neighbour s: shuffle; lane 0 takes the previous warp's lane-31 column
+        // (zeros for warp 0: slot 0 of the halo array is a permanent zero pad)
         #pragma unroll
-        for (int k = 0; k < FR; ++k) {
-            const float rup = k > 0 ? r[k - 1] : rabove;
-            float sl = __shfl_up_sync(0xffffffffu, s[k], 1);
-            if (lane == 0) sl = warp > 0 ? csl[k] : 0.f;
-            z[k] = bme[k * NTW] - lam * (r[k] + s[k] - rup - sl);
-        }
-        hz[cb * hstride + g * NTW + j] = z[0];
+        for (int k = 0; k < FR; ++k) z[k] = __shfl_up_sync(0xffffffffu, s[k], 1);
         if (lane == 0) {
-            float* czw = cz + cb * cstride + (g * nw + warp) * FR;
+            const float4* csl = reinterpret_cast<const float4*>(cs + pb * cstride + (g * (nw + 1) + warp) * FR);
             #pragma unroll
-            for (int k = 0; k < FR; ++k) czw[k] = z[k];
+            for (int k = 0; k < FR; k += 4) {
+                const float4 h = csl[k / 4];
+                z[k] = h.x; z[k + 1] = h.y; z[k + 2] = h.z; z[k + 3] = h.w;
+            }
         }
-        fgp_cluster_barrier(cl);
+        // row 0 first (it needs the row above, possibly from the CTA above) and push
+        // it at once, so the exchange overlaps rows 1..FR-1
+        {
+            float rabove = 0.f;
+            if (g > 0) {
+                rabove = hr[pb * hstride + (g - 1) * NTW + j];
+            } else if (has_up && it > 0) {
+                mbar_wait(smem_u32(bars + pb), ((it - 1) >> 1) & 1);
+                rabove = rx_r[pb * NTW + j];
+            }
+            z[0] = bme[0] - lam * (r[0] + s[0] - rabove - z[0]);
+            if (g == 0 && has_up) st_async_f32(rem_rx_z + cb * row_bytes, z[0], rem_bar_z + cb * 8);
+            hz[cb * hstride + g * NTW + j] = z[0];
+        }
+        #pragma unroll
+        for (int k = 1; k < FR; ++k) z[k] = bme[k * NTW] - lam * (r[k] + s[k] - r[k - 1] - z[k]);
+        if (lane == 0) {
+            float* czw = cz + cb * cstride + (g * (nw + 1) + warp) * FR;
+            #pragma unroll
+            for (int k = 0; k < FR; k += 4) *reinterpret_cast<float4*>(czw + k) = make_float4(z[k], z[k + 1], z[k + 2], z[k + 3]);
+        }
+        __syncthreads();
         // ---- phase B: dual ascent, projection on [-1,1], FGP momentum
         const float tn = 0.5f * (1.f + sqrtf(1.f + 4.f * tk * tk));
         const float beta = (tk - 1.f) / tn;
         tk = tn;
-        const float zbelow = hz_dn ? hz_dn[cb * hstride + j] : 0.f;
-        const float* czr = cz + cb * cstride + (g * nw + warp + 1) * FR;
+
+        // right neighbour z: shuffle; lane 31 takes the next warp's lane-0 column
+        // (the slot after the last warp is a permanent zero pad); qn below reuses s as scratch
+        float zr[FR];
         #pragma unroll
-        for (int k = 0; k < FR; ++k) {
-            const float zd = k < FR - 1 ? z[k + 1] : zbelow;
-            float zr = __shfl_down_sync(0xffffffffu, z[k], 1);
-            if (lane == 31) zr = warp < nw - 1 ? czr[k] : 0.f;
-            const float pn = (pmask >> k) & 1u ? clip1(r[k] + gam * (z[k] - zd)) : 0.f;
-            const float qn = (qmask >> k) & 1u ? clip1(s[k] + gam * (z[k] - zr)) : 0.f;
-            r[k] = pn + beta * (pn - p[k]);
-            s[k] = qn + beta * (qn - q[k]);
+        for (int k = 0; k < FR; ++k) zr[k] = __shfl_down_sync(0xffffffffu, z[k], 1);
+        if (lane == 31) {
+            const float4* czr = reinterpret_cast<const float4*>(cz + cb * cstride + (g * (nw + 1) + warp + 1) * FR);
+            #pragma unroll
+            for (int k = 0; k < FR; k += 4) {
+                const float4 h = czr[k / 4];
+                zr[k] = h.x; zr[k + 1] = h.y; zr[k + 2] = h.z; zr[k + 3] = h.w;
+            }
+        }
+        // last row first (it needs the row below, possibly from the CTA below) and push it
+        {
+            constexpr int k = FR - 1;
+            float zbelow = 0.f;
+            if (g < G - 1) {
+                zbelow = hz[cb * hstride + (g + 1) * NTW + j];
+            } else if (has_dn) {
+                mbar_wait(smem_u32(bars + 2 + cb), (it >> 1) & 1);
+                zbelow = rx_z[cb * NTW + j];
+            }
+            const float gp = k < kp ? gp_col : 0.f;
+            const float gq = k < kq ? gq_col : 0.f;
+            const float pn = clip1(fmaf(gp, z[k] - zbelow, r[k]));
+            const float qn = clip1(fmaf(gq, z[k] - zr[k], s[k]));
+            r[k] = fmaf(beta, pn - p[k], pn);
+            s[k] = fmaf(beta, qn - q[k], qn);
             p[k] = pn;
             q[k] = qn;
+            if (g == G - 1 && has_dn) st_async_f32(rem_rx_r + cb * row_bytes, r[k], rem_bar_r + cb * 8);
+            hr[cb * hstride + g * NTW + j] = r[k];
         }
-        hr[cb * hstride + g * NTW + j] = r[FR - 1];
-        if (lane == 31) {
-            float* csw = cs + cb * cstride + (g * nw + warp) * FR;
+        if (kq >= FR && kp >= FR) {             // interior strip: no row masks
             #pragma unroll
-            for (int k = 0; k < FR; ++k) csw[k] = s[k];
+            for (int k = 0; k < FR - 1; ++k) {
+                const float pn = clip1(fmaf(gp_col, z[k] - z[k + 1], r[k]));
+                const float qn = clip1(fmaf(gq_col, z[k] - zr[k], s[k]));
+                r[k] = fmaf(beta, pn - p[k], pn);
+                s[k] = fmaf(beta, qn - q[k], qn);
+                p[k] = pn;
+                q[k] = qn;
+            }
+        } else {
+            #pragma unroll
+            for (int k = 0; k < FR - 1; ++k) {
+                const float gp = k < kp ? gp_col : 0.f;
+                const float gq = k < kq ? gq_col : 0.f;
+                const float pn = clip1(fmaf(gp, z[k] - z[k + 1], r[k]));
+                const float qn = clip1(fmaf(gq, z[k] - zr[k], s[k]));
+                r[k] = fmaf(beta, pn - p[k], pn);
+                s[k] = fmaf(beta, qn - q[k], qn);
+                p[k] = pn;
+                q[k] = qn;
+            }
         }
-        fgp_cluster_barrier(cl);
+        if (lane == 31) {
+            float* csw = cs + cb * cstride + (g * (nw + 1) + warp + 1) * FR;
+            #pragma unroll
+            for (int k = 0; k < FR; k += 4) *reinterpret_cast<float4*>(csw + k) = make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]);
+        }
+        __syncthreads();
     }
     // ---- x = b - lam L(p, q), then the epilogue
     hp[g * NTW + j] = p[FR - 1];
@@ -584,6 +711,7 @@ __global__ void __launch_bounds__(512, 1) k_fgp(FgpArgs A) {
         for (int k = 0; k < FR; ++k) cq[(g * nw + warp) * FR + k] = q[k];
     }
     cl.sync();
+    const float* hp_up = g > 0 ? hp + (g - 1) * NTW : (has_up ? cl.map_shared_rank(hp, kr - 1) + (G - 1) * NTW : nullptr);
     const float pabove = hp_up ? hp_up[j] : 0.f;
     const float* cql = cq + (g * nw + warp - 1) * FR;
     #pragma unroll

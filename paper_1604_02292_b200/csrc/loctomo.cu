@@ -155,8 +155,8 @@ int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, cons
 // direct-read kernel when the staged band would not fit)
 int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
                   float* out, long long out_ts, cudaStream_t st) {
-    const size_t smem = (size_t)2 * FP_BL * t.TP * sizeof(float);
-    if (smem > 160 * 1024 || (long long)FP_GA * t.Wwin > 256LL * FP_U)
+    const size_t smem = (size_t)2 * FP_BL * FP_P * sizeof(float);
+    if (t.TP > FP_P || t.Wwin > 32 * FP_U)
         return launch_fp(p, 0, t, img, imgT, img_ts, out, out_ts, nullptr, nullptr, st);
     LT_CUDA(cudaFuncSetAttribute(k_fp_roi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
@@ -199,15 +199,15 @@ SinoView view_win(const float* base, int Wwin, int na) {
 struct FgpCfg { int NTW, G, K; size_t smem; };
 
 int fgp_config(int rows, int cols, FgpCfg* c) {
-    if (rows < 1 || cols < 1 || cols > 512) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
+    if (rows < 1 || cols < 1 || cols > 256) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
     const int ntw = 32 * ((cols + 31) / 32);
     const int strips = (rows + FR - 1) / FR;
-    const int G = std::max(1, std::min(strips, 512 / ntw));
+    const int G = std::max(1, std::min(strips, 256 / ntw));
     const int K = (strips + G - 1) / G;
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
     const int nw = ntw / 32;
     c->NTW = ntw; c->G = G; c->K = K;
-    c->smem = (size_t)(5 * G * ntw + 5 * G * nw * FR + G * FR * ntw) * sizeof(float);
+    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FR + G * nw * FR + G * FR * ntw) * sizeof(float);
     return LT_OK;
 }
 
