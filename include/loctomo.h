@@ -118,7 +118,7 @@ int lt_get_conv(const lt_plan* plan, float* d_out, void* stream);
 int lt_sirt_solve(lt_plan* plan, const float* d_sino, float lo, float hi, float* d_cores, void* stream);
 
 /* Local FISTA-TV (Alg. 3, FISTA update per DESIGN.md A12, FGP prox A13/A14).
- * lambda >= 0, n_fgp >= 1. */
+ * lambda >= 0, 1 <= n_fgp <= 4096; extended ROI side 2h <= 256. */
 int lt_tv_solve(lt_plan* plan, const float* d_sino, float lambda, int32_t n_fgp, float* d_cores, void* stream);
 
 /* Extended-ROI results of the last solve: [local_count][2h][2h], the valid

@@ -743,7 +743,7 @@ int lt_sirt_solve(lt_plan* p, const float* d_sino, float lo, float hi, float* d_
 int lt_tv_solve(lt_plan* p, const float* d_sino, float lambda, int32_t n_fgp, float* d_cores, void* stream) {
     if (int rc = check_plan(p)) return rc;
     if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
-    if (!(lambda >= 0.f) || n_fgp < 1) return fail(LT_ERR_INVALID, "lambda >= 0 and n_fgp >= 1 required");
+    if (!(lambda >= 0.f) || n_fgp < 1 || n_fgp > 4096) return fail(LT_ERR_INVALID, "lambda >= 0 and 1 <= n_fgp <= 4096 required");
     FgpCfg fc;
     if (int rc = fgp_config(p->T, p->T, &fc)) return rc;
     if (p->R == 0) return LT_OK;
@@ -869,7 +869,7 @@ int lt_global_tv(lt_plan* p, const float* d_sino, int32_t n_iter, float lambda, 
 
 int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda, int32_t n_fgp, float* d_out,
                  void* stream) {
-    if (h < 1 || w < 1 || count < 0 || !(lambda >= 0.f) || n_fgp < 1 || h > 256 || w > 256)
+    if (h < 1 || w < 1 || count < 0 || !(lambda >= 0.f) || n_fgp < 1 || n_fgp > 4096 || h > 256 || w > 256)
         return fail(LT_ERR_INVALID, "bad FGP arguments");
     if (count == 0) return LT_OK;
     if (!d_in || !d_out) return fail(LT_ERR_INVALID, "null pointer");
