@@ -469,7 +469,6 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
 // barriers per FGP iteration (z needs r above / s left; the dual step needs
 // z below / z right); halos are double buffered by iteration parity.
 // ---------------------------------------------------------------------------
-constexpr int FR = 16;
 
 struct FgpArgs {
     const float* b; int b_pitch; long long b_tstride;   // input image(s)
@@ -527,8 +526,8 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
+template <int MODE, int FR, int NT>
+__global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     extern __shared__ __align__(16) float sm[];
     cg::cluster_group cl = cg::this_cluster();
     const int K = (int)cl.num_blocks();
@@ -555,21 +554,27 @@ __global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
     float* cs = hp + G * NTW;                // [2][G][nw+1][FR] slot w+1: lane-31 column of s of warp w; slot 0 zero
     float* cz = cs + 2 * G * (nw + 1) * FR;  // [2][G][nw+1][FR] slot w: lane-0 column of z of warp w; slot nw zero
     float* cq = cz + 2 * G * (nw + 1) * FR;  // [G][nw][FR]    lane-31 column of q (epilogue)
-    float* sb = cq + G * nw * FR;            // [G][FR][NTW]   the input b
+    float* sbeta = cq + G * nw * FR;         // [nfgp] FGP momentum coefficients
     const int nzero = 4 * NTW + 5 * G * NTW + 4 * G * (nw + 1) * FR + G * nw * FR;
     const int tid = g * NTW + j, nthr = NTW * G;
     for (int e = tid; e < nzero; e += nthr) rx_r[e] = 0.f;
     if (tid == 0) {
-        for (int q = 0; q < 4; ++q) mbar_init(smem_u32(bars + q), 1);
+        for (int q_ = 0; q_ < 4; ++q_) mbar_init(smem_u32(bars + q_), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // t_0 = 1, t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2, beta_k = (t_k - 1)/t_{k+1}  (Beck & Teboulle)
+        float tk = 1.f;
+        for (int it = 0; it < A.nfgp; ++it) {
+            const float tn = 0.5f * (1.f + sqrtf(1.f + 4.f * tk * tk));
+            sbeta[it] = (tk - 1.f) / tn;
+            tk = tn;
+        }
     }
 
-    float r[FR], s[FR], p[FR], q[FR], z[FR];
-    float* bme = sb + g * FR * NTW + j;
+    float b[FR], r[FR], s[FR], p[FR], q[FR], z[FR];
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)(vr0 + i0) * A.b_pitch + vc0 + j;
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
-        bme[k * NTW] = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
+        b[k] = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
         r[k] = 0.f; s[k] = 0.f; p[k] = 0.f; q[k] = 0.f;
     }
     // step sizes with the boundary masks folded in: gamma = 0 where the dual
@@ -592,25 +597,29 @@ __global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
     const int hstride = G * NTW;
     const int cstride = G * (nw + 1) * FR;
     const int nit = lam > 0.f ? A.nfgp : 0;
-    float tk = 1.f;
+    const unsigned bar0 = smem_u32(bars);     // r from above: bar0 + 8*parity; z from below: bar0 + 16 + 8*parity
     for (int it = 0; it < nit; ++it) {
         const int cb = it & 1, pb = cb ^ 1;
         if (tid == 0) {
-            if (has_dn) mbar_expect_tx(smem_u32(bars + 2 + cb), row_bytes);   // z row of it, from below
-            if (has_up) mbar_expect_tx(smem_u32(bars + cb), row_bytes);       // r row of it, from above
+            if (has_dn) mbar_expect_tx(bar0 + 16 + 8 * cb, row_bytes);   // z row of it, from below
+            if (has_up) mbar_expect_tx(bar0 + 8 * cb, row_bytes);        // r row of it, from above
         }
         // ---- phase A: z = b - lam L(r, s)
 
         // left neighbour s: shuffle; lane 0 takes the previous warp's lane-31 column
         // (zeros for warp 0: slot 0 of the halo array is a permanent zero pad)
-        #pragma unroll
-        for (int k = 0; k < FR; ++k) z[k] = __shfl_up_sync(0xffffffffu, s[k], 1);
-        if (lane == 0) {
-            const float4* csl = reinterpret_cast<const float4*>(cs + pb * cstride + (g * (nw + 1) + warp) * FR);
+        {
+            // lane 0 reads the halo slot of this warp, the others the zero pad slot
+            const float4* csl = reinterpret_cast<const float4*>(cs + pb * cstride + (g * (nw + 1) + (lane == 0 ? warp : 0)) * FR);
             #pragma unroll
             for (int k = 0; k < FR; k += 4) {
                 const float4 h = csl[k / 4];
-                z[k] = h.x; z[k + 1] = h.y; z[k + 2] = h.z; z[k + 3] = h.w;
+                const float hv[4] = {h.x, h.y, h.z, h.w};
+                #pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float sh = __shfl_up_sync(0xffffffffu, s[k + e], 1);
+                    z[k + e] = lane == 0 ? hv[e] : sh;
+                }
             }
         }
         // row 0 first (it needs the row above, possibly from the CTA above) and push
@@ -620,15 +629,15 @@ __global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
             if (g > 0) {
                 rabove = hr[pb * hstride + (g - 1) * NTW + j];
             } else if (has_up && it > 0) {
-                mbar_wait(smem_u32(bars + pb), ((it - 1) >> 1) & 1);
+                mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
                 rabove = rx_r[pb * NTW + j];
             }
-            z[0] = bme[0] - lam * (r[0] + s[0] - rabove - z[0]);
+            z[0] = b[0] - lam * (r[0] + s[0] - rabove - z[0]);
             if (g == 0 && has_up) st_async_f32(rem_rx_z + cb * row_bytes, z[0], rem_bar_z + cb * 8);
             hz[cb * hstride + g * NTW + j] = z[0];
         }
         #pragma unroll
-        for (int k = 1; k < FR; ++k) z[k] = bme[k * NTW] - lam * (r[k] + s[k] - r[k - 1] - z[k]);
+        for (int k = 1; k < FR; ++k) z[k] = b[k] - lam * (r[k] + s[k] - r[k - 1] - z[k]);
         if (lane == 0) {
             float* czw = cz + cb * cstride + (g * (nw + 1) + warp) * FR;
             #pragma unroll
@@ -636,21 +645,23 @@ __global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
         }
         __syncthreads();
         // ---- phase B: dual ascent, projection on [-1,1], FGP momentum
-        const float tn = 0.5f * (1.f + sqrtf(1.f + 4.f * tk * tk));
-        const float beta = (tk - 1.f) / tn;
-        tk = tn;
+        const float beta = sbeta[it];
 
         // right neighbour z: shuffle; lane 31 takes the next warp's lane-0 column
         // (the slot after the last warp is a permanent zero pad); qn below reuses s as scratch
         float zr[FR];
-        #pragma unroll
-        for (int k = 0; k < FR; ++k) zr[k] = __shfl_down_sync(0xffffffffu, z[k], 1);
-        if (lane == 31) {
-            const float4* czr = reinterpret_cast<const float4*>(cz + cb * cstride + (g * (nw + 1) + warp + 1) * FR);
+        {
+            // lane 31 reads the next warp's slot, the others the zero pad slot after the last warp
+            const float4* czr = reinterpret_cast<const float4*>(cz + cb * cstride + (g * (nw + 1) + (lane == 31 ? warp + 1 : nw)) * FR);
             #pragma unroll
             for (int k = 0; k < FR; k += 4) {
                 const float4 h = czr[k / 4];
-                zr[k] = h.x; zr[k + 1] = h.y; zr[k + 2] = h.z; zr[k + 3] = h.w;
+                const float hv[4] = {h.x, h.y, h.z, h.w};
+                #pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float zh = __shfl_down_sync(0xffffffffu, z[k + e], 1);
+                    zr[k + e] = lane == 31 ? hv[e] : zh;
+                }
             }
         }
         // last row first (it needs the row below, possibly from the CTA below) and push it
@@ -660,7 +671,7 @@ __global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
             if (g < G - 1) {
                 zbelow = hz[cb * hstride + (g + 1) * NTW + j];
             } else if (has_dn) {
-                mbar_wait(smem_u32(bars + 2 + cb), (it >> 1) & 1);
+                mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
                 zbelow = rx_z[cb * NTW + j];
             }
             const float gp = k < kp ? gp_col : 0.f;
@@ -719,7 +730,7 @@ __global__ void __launch_bounds__(256, 1) k_fgp(FgpArgs A) {
         const float pup = k > 0 ? p[k - 1] : pabove;
         float ql = __shfl_up_sync(0xffffffffu, q[k], 1);
         if (lane == 0) ql = warp > 0 ? cql[k] : 0.f;
-        const float x = bme[k * NTW] - lam * (p[k] + q[k] - pup - ql);
+        const float x = b[k] - lam * (p[k] + q[k] - pup - ql);
         const int i = i0 + k;
         if (colv && i < Hv) {
             if (MODE == 0) {

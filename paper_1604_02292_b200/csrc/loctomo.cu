@@ -194,31 +194,34 @@ SinoView view_win(const float* base, int Wwin, int na) {
 }
 
 // FGP cluster configuration (k_fgp): NTW threads per strip row (one per
-// column), strips of FR rows, G strips per CTA (<= 512 threads), K CTAs per
-// cluster covering all rows of a tile.
-struct FgpCfg { int NTW, G, K; size_t smem; };
+// column), strips of FR rows, G strips per CTA (<= NT threads), K CTAs per
+// cluster covering all rows of a tile.  FR = 8 (512-thread CTAs, 16 warps per
+// SM) by default; LT_FGP_FR=16 selects 16-row strips in 256-thread CTAs.
+struct FgpCfg { int NTW, G, K, FR, NT; size_t smem; };
 
-int fgp_config(int rows, int cols, FgpCfg* c) {
+int fgp_config(int rows, int cols, int nfgp, FgpCfg* c) {
     if (rows < 1 || cols < 1 || cols > 256) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
+    static int fr_env = -1;
+    if (fr_env < 0) { const char* e = getenv("LT_FGP_FR"); fr_env = (e && atoi(e) == 16) ? 16 : 8; }
+    const int FRv = fr_env, NT = FRv == 8 ? 512 : 256;
     const int ntw = 32 * ((cols + 31) / 32);
-    const int strips = (rows + FR - 1) / FR;
-    const int G = std::max(1, std::min(strips, 256 / ntw));
+    const int strips = (rows + FRv - 1) / FRv;
+    const int G = std::max(1, std::min(strips, NT / ntw));
     const int K = (strips + G - 1) / G;
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
     const int nw = ntw / 32;
-    c->NTW = ntw; c->G = G; c->K = K;
-    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FR + G * nw * FR + G * FR * ntw) * sizeof(float);
+    c->NTW = ntw; c->G = G; c->K = K; c->FR = FRv; c->NT = NT;
+    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv + std::max(nfgp, 1)) * sizeof(float);
     return LT_OK;
 }
 
-template <int MODE>
-int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
-    FgpCfg c;
-    if (int rc = fgp_config(rows, cols, &c)) return rc;
+template <int MODE, int FRv, int NT>
+int launch_fgp_t(FgpArgs A, const FgpCfg& c, int ntiles, cudaStream_t st) {
     A.G = c.G;
     A.NTW = c.NTW;
-    LT_CUDA(cudaFuncSetAttribute(k_fgp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
-    if (c.K > 8) LT_CUDA(cudaFuncSetAttribute(k_fgp<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    auto kern = k_fgp<MODE, FRv, NT>;
+    LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+    if (c.K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3(c.K, ntiles, 1);
@@ -233,9 +236,17 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ScopedTimer tm(TC_FGP, st);
-    LT_CUDA(cudaLaunchKernelEx(&cfg, k_fgp<MODE>, A));
+    LT_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     LT_LAUNCHED();
     return LT_OK;
+}
+
+template <int MODE>
+int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
+    FgpCfg c;
+    if (int rc = fgp_config(rows, cols, A.nfgp, &c)) return rc;
+    if (c.FR == 8) return launch_fgp_t<MODE, 8, 512>(A, c, ntiles, st);
+    return launch_fgp_t<MODE, 16, 256>(A, c, ntiles, st);
 }
 
 dim3 grid2d(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }
@@ -745,7 +756,7 @@ int lt_tv_solve(lt_plan* p, const float* d_sino, float lambda, int32_t n_fgp, fl
     if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
     if (!(lambda >= 0.f) || n_fgp < 1 || n_fgp > 4096) return fail(LT_ERR_INVALID, "lambda >= 0 and 1 <= n_fgp <= 4096 required");
     FgpCfg fc;
-    if (int rc = fgp_config(p->T, p->T, &fc)) return rc;
+    if (int rc = fgp_config(p->T, p->T, n_fgp, &fc)) return rc;
     if (p->R == 0) return LT_OK;
     return solve(*p, 1, d_sino, lambda, 0.f, n_fgp, d_cores, (cudaStream_t)stream);
 }
