@@ -145,19 +145,14 @@ def run_ours(args, cfg):
     sino_host = torch.from_numpy(inp.sino).pin_memory()
     sino = sino_host.cuda()
     side = 2 * cfg.radius
-    max_local = -(-cfg.n_roi // world)
-    cores = torch.zeros(max_local, side, side, device="cuda")
-    image = torch.empty(cfg.n, cfg.n, device="cuda")
-    gathered = torch.empty(world * max_local, side, side, device="cuda") if world > 1 else None
-    # slot -> global ROI table for the gathered layout
-    slot_roi = np.full(world * max_local, -1, dtype=np.int32)
+    from paper_1604_02292_b200 import dist as ltd
     if world > 1:
-        all_local = [None] * world
-        dist.all_gather_object(all_local, plan.local_rois.tolist())
-        for g, lst in enumerate(all_local):
-            slot_roi[g * max_local:g * max_local + len(lst)] = lst
+        spr, slot_roi = ltd.setup_combine(plan)
     else:
-        slot_roi[:plan.R] = plan.local_rois
+        spr, slot_roi = plan.R, np.asarray(plan.local_rois, dtype=np.int32)
+    cores = torch.zeros(spr, side, side, device="cuda")
+    image = torch.empty(cfg.n, cfg.n, device="cuda")
+    gathered = torch.empty(world * spr, side, side, device="cuda") if world > 1 else None
 
     def step():
         out = cores[:plan.R]
@@ -166,10 +161,10 @@ def run_ours(args, cfg):
         else:
             plan.sirt_solve(sino, 0.0, math.inf, out=out)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, cores)
+            ltd.gather_cores(cores, out=gathered)          # NCCL all-gather over NVLink
             plan.combine(gathered, slot_roi, out=image)
         else:
-            plan.combine(cores[:plan.R], slot_roi[:plan.R], out=image)
+            plan.combine(cores[:plan.R], slot_roi, out=image)
 
     for _ in range(args.warmup):
         step()

@@ -1,0 +1,64 @@
+"""Multi-GPU combine plumbing: ROIs are partitioned by
+``lt_roi_setup(rank, world)``; each rank solves its ROIs, the cores are
+all-gathered into fixed slots (``max_local`` per rank, ROI-index ordered
+within a rank) and every rank stitches the same image with ``lt_combine_rois``
+(ascending global ROI order => bitwise identical for every world size).
+
+torch.distributed provides the collective (NCCL on GPUs; gloo works for the
+CPU tests of this host logic).  No arithmetic of the method lives here.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+import numpy as np
+import torch
+
+
+def max_local(n_roi: int, world: int) -> int:
+    """Slots per rank: the LPT partition gives every rank at most ceil(R / world) + 1 ROIs."""
+    return -(-n_roi // world) + (1 if world > 1 else 0)
+
+
+def slot_table(local_lists: Sequence[Sequence[int]], slots_per_rank: int) -> np.ndarray:
+    """Global ROI index of every gathered slot (-1 = empty)."""
+    world = len(local_lists)
+    out = np.full(world * slots_per_rank, -1, dtype=np.int32)
+    for g, lst in enumerate(local_lists):
+        if len(lst) > slots_per_rank:
+            raise ValueError(f"rank {g} holds {len(lst)} ROIs > {slots_per_rank} slots")
+        out[g * slots_per_rank:g * slots_per_rank + len(lst)] = np.asarray(lst, dtype=np.int32)
+    return out
+
+
+def exchange_local_lists(local_rois: Sequence[int], group=None) -> List[List[int]]:
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    lists: List = [None] * world
+    dist.all_gather_object(lists, [int(v) for v in local_rois], group=group)
+    return lists
+
+
+def gather_cores(cores_slots: torch.Tensor, group=None, out: torch.Tensor = None) -> torch.Tensor:
+    """All-gather this rank's padded slot block [slots_per_rank, side, side]
+    into [world * slots_per_rank, side, side] (rank-major)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty((world * cores_slots.shape[0],) + tuple(cores_slots.shape[1:]),
+                          dtype=cores_slots.dtype, device=cores_slots.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, cores_slots.contiguous(), group=group)
+    else:
+        parts = list(out.chunk(world, dim=0))
+        dist.all_gather(parts, cores_slots.contiguous(), group=group)
+    return out
+
+
+def setup_combine(plan, group=None) -> Tuple[int, np.ndarray]:
+    """(slots_per_rank, slot -> global ROI table) for a plan of this rank."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    spr = max_local(len(plan.centres), world)
+    lists = exchange_local_lists(plan.local_rois, group) if world > 1 else [list(plan.local_rois)]
+    return spr, slot_table(lists, spr)
