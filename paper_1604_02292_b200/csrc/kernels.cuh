@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <stdint.h>
+#include <type_traits>
 
 namespace lt {
 namespace cg = cooperative_groups;
@@ -598,16 +599,15 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     const int cstride = G * (nw + 1) * FR;
     const int nit = lam > 0.f ? A.nfgp : 0;
     const unsigned bar0 = smem_u32(bars);     // r from above: bar0 + 8*parity; z from below: bar0 + 16 + 8*parity
-    for (int it = 0; it < nit; ++it) {
-        const int cb = it & 1, pb = cb ^ 1;
+    // one FGP iteration; CB = parity of the iteration (compile time, so every
+    // halo address below is loop invariant)
+    auto fgp_iter = [&](int it, auto cbc) {
+        constexpr int cb = decltype(cbc)::value, pb = cb ^ 1;
         if (tid == 0) {
             if (has_dn) mbar_expect_tx(bar0 + 16 + 8 * cb, row_bytes);   // z row of it, from below
             if (has_up) mbar_expect_tx(bar0 + 8 * cb, row_bytes);        // r row of it, from above
         }
         // ---- phase A: z = b - lam L(r, s)
-
-        // left neighbour s: shuffle; lane 0 takes the previous warp's lane-31 column
-        // (zeros for warp 0: slot 0 of the halo array is a permanent zero pad)
         {
             // lane 0 reads the halo slot of this warp, the others the zero pad slot
             const float4* csl = reinterpret_cast<const float4*>(cs + pb * cstride + (g * (nw + 1) + (lane == 0 ? warp : 0)) * FR);
@@ -646,9 +646,6 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
         __syncthreads();
         // ---- phase B: dual ascent, projection on [-1,1], FGP momentum
         const float beta = sbeta[it];
-
-        // right neighbour z: shuffle; lane 31 takes the next warp's lane-0 column
-        // (the slot after the last warp is a permanent zero pad); qn below reuses s as scratch
         float zr[FR];
         {
             // lane 31 reads the next warp's slot, the others the zero pad slot after the last warp
@@ -714,7 +711,13 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
             for (int k = 0; k < FR; k += 4) *reinterpret_cast<float4*>(csw + k) = make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]);
         }
         __syncthreads();
+    };
+    int it = 0;
+    for (; it + 1 < nit; it += 2) {
+        fgp_iter(it, std::integral_constant<int, 0>{});
+        fgp_iter(it + 1, std::integral_constant<int, 1>{});
     }
+    if (it < nit) fgp_iter(it, std::integral_constant<int, 0>{});
     // ---- x = b - lam L(p, q), then the epilogue
     hp[g * NTW + j] = p[FR - 1];
     if (lane == 31) {

@@ -93,6 +93,11 @@ struct lt_plan {
     bool bound = false, bank_ready = false, wd_ready = false;
     int last_mode = -1;
     int stitch_cap = 0;           // max list entries
+    // ROI-batch pipelining: the local ROIs are split into groups whose
+    // iteration chains run on separate streams and overlap on the device
+    int nsplit = 1;
+    cudaStream_t gst[2] = {nullptr, nullptr};
+    cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     struct {
         size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
@@ -291,15 +296,17 @@ int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
 }
 
 // the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
-int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st) {
-    const Tiles t = p.roi_tiles();
+// one ROI group (tiles [t0, t0 + cnt)) through all n iterations on stream st
+int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st) {
+    Tiles t = p.roi_tiles();
+    t.tile += t0; t.d0 += (size_t)t0 * p.na; t.tauc += (size_t)t0 * p.na; t.ntiles = cnt;
     const long long yts = p.ytile();
-    float* y = p.P<float>(p.off.y);
-    float* yT = p.P<float>(p.off.yT);
-    float* s = p.P<float>(p.off.s);
-    LT_CUDA(cudaMemsetAsync(y, 0, (size_t)p.R * yts * sizeof(float), st));
-    LT_CUDA(cudaMemsetAsync(yT, 0, (size_t)p.R * yts * sizeof(float), st));
-    if (mode == 1) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
+    float* y = p.P<float>(p.off.y) + t0 * yts;
+    float* yT = p.P<float>(p.off.yT) + t0 * yts;
+    float* s = p.P<float>(p.off.s) + (long long)t0 * p.na * p.Wwin;
+    float* v = p.P<float>(p.off.v) + t0 * p.ptile();
+    float* xs = p.P<float>(p.off.xs) + t0 * p.ptile();
+    float* xprev = p.P<float>(p.off.xprev) + t0 * p.ptile();
     const long long ns = (long long)p.na * p.nd;
     const bool disc = (p.flags & LT_DISC_ON) != 0;
     double tk = 1.0;
@@ -307,7 +314,7 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
         const float* bk = p.P<float>(p.off.conv) + (long long)k * ns;
         BpEpi e = epi0();
         e.y = y; e.yT = yT; e.y_tstride = yts;
-        e.v = p.P<float>(p.off.v); e.xs = p.P<float>(p.off.xs); e.p_tstride = p.ptile();
+        e.v = v; e.xs = xs; e.p_tstride = p.ptile();
         e.discc = p.P<float>(p.off.discc32); e.use_disc = disc;
         e.alpha = (float)p.alpha; e.lo = lo; e.hi = hi; e.last = (k == p.n_iter - 1);
         const SinoView vb = view_full(bk, p.nd);
@@ -327,14 +334,40 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
             tk = tn;
             FgpArgs A;
             memset(&A, 0, sizeof A);
-            A.b = p.P<float>(p.off.v); A.b_pitch = p.T; A.b_tstride = p.ptile();
-            A.tiles = p.P<TileT>(p.off.tiles);
+            A.b = v; A.b_pitch = p.T; A.b_tstride = p.ptile();
+            A.tiles = p.P<TileT>(p.off.tiles) + t0;
             A.lam = lam; A.nfgp = nfgp;
-            A.xs = p.P<float>(p.off.xs); A.xprev = p.P<float>(p.off.xprev); A.p_tstride = p.ptile(); A.T = p.T;
+            A.xs = xs; A.xprev = xprev; A.p_tstride = p.ptile(); A.T = p.T;
             A.y = y; A.yT = yT; A.y_tstride = yts; A.TP = p.TP;
             A.beta_o = (float)beta;
-            if (int rc = launch_fgp<1>(A, p.T, p.T, p.R, st)) return rc;
+            if (int rc = launch_fgp<1>(A, p.T, p.T, cnt, st)) return rc;
         }
+    }
+    return LT_OK;
+}
+
+// the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
+int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st) {
+    const long long yts = p.ytile();
+    LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.y), 0, (size_t)p.R * yts * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.yT), 0, (size_t)p.R * yts * sizeof(float), st));
+    if (mode == 1) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
+    const int ng = (p.nsplit > 1 && p.R >= 2 && p.gst[0]) ? 2 : 1;
+    if (ng == 1) {
+        if (int rc = group_iterations(p, 0, p.R, mode, lo, hi, lam, nfgp, st)) return rc;
+    } else {
+        // fork: both group streams wait for the work already queued on st
+        LT_CUDA(cudaEventRecord(p.gev[2], st));
+        const int half = (p.R + 1) / 2;
+        for (int g = 0; g < 2; ++g) {
+            LT_CUDA(cudaStreamWaitEvent(p.gst[g], p.gev[2], 0));
+            const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
+            if (int rc = group_iterations(p, t0, cnt, mode, lo, hi, lam, nfgp, p.gst[g])) return rc;
+            LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
+        }
+        // join
+        LT_CUDA(cudaStreamWaitEvent(st, p.gev[0], 0));
+        LT_CUDA(cudaStreamWaitEvent(st, p.gev[1], 0));
     }
     p.last_mode = mode;
     return LT_OK;
@@ -600,6 +633,12 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.discc32, 0, 4, st));
     LT_CUDA(cudaStreamSynchronize(st));
+    if (!p->gst[0]) {
+        const char* e = getenv("LT_SPLIT");
+        p->nsplit = (e && atoi(e) == 1) ? 1 : 2;
+        for (int g = 0; g < 2; ++g) LT_CUDA(cudaStreamCreateWithFlags(&p->gst[g], cudaStreamNonBlocking));
+        for (int g = 0; g < 3; ++g) LT_CUDA(cudaEventCreateWithFlags(&p->gev[g], cudaEventDisableTiming));
+    }
     p->bound = true;
     p->bank_ready = p->wd_ready = false;
     return LT_OK;
@@ -893,6 +932,13 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
     return launch_fgp<0>(A, h, w, count, (cudaStream_t)stream);
 }
 
-void lt_plan_destroy(lt_plan* p) { delete p; }
+void lt_plan_destroy(lt_plan* p) {
+    if (!p) return;
+    for (int g = 0; g < 2; ++g)
+        if (p->gst[g]) cudaStreamDestroy(p->gst[g]);
+    for (int g = 0; g < 3; ++g)
+        if (p->gev[g]) cudaEventDestroy(p->gev[g]);
+    delete p;
+}
 
 }  // extern "C"
