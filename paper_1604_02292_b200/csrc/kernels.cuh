@@ -486,6 +486,11 @@ struct FgpArgs {
 
 __device__ __forceinline__ float clip1(float v) { return fminf(1.f, fmaxf(-1.f, v)); }
 
+// FGP momentum coefficients beta_k = (t_k - 1)/t_{k+1}, t_0 = 1,
+// t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2 (Beck & Teboulle), computed on the host in fp64
+constexpr int FGP_MAX_IT = 4096;
+__constant__ float c_fgp_beta[FGP_MAX_IT];
+
 // Cluster barrier between the FGP phases.  LT_FGP_BARRIER 0: cg cluster.sync()
 // (release/acquire at cluster scope; ptxas emits MEMBAR.ALL.GPU);
 // 1: CTA-scope fence + relaxed arrive + acquire wait (experiment).
@@ -527,6 +532,11 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
 }
 
+// The duals are stored shifted, p' = (p + 1)/2 in [0, 1] (likewise q, r, s):
+// the projection onto [-1, 1] becomes the .SAT modifier of one FFMA, the
+// FGP momentum is affine-invariant, and L(p, q) = 2 L(p', q') because the
+// constant shifts cancel in the divergence.  A dual that does not exist
+// (outside the valid rectangle, last row / column) is p' = 1/2.
 template <int MODE, int FR, int NT>
 __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     extern __shared__ __align__(16) float sm[];
@@ -555,20 +565,18 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     float* cs = hp + G * NTW;                // [2][G][nw+1][FR] slot w+1: lane-31 column of s of warp w; slot 0 zero
     float* cz = cs + 2 * G * (nw + 1) * FR;  // [2][G][nw+1][FR] slot w: lane-0 column of z of warp w; slot nw zero
     float* cq = cz + 2 * G * (nw + 1) * FR;  // [G][nw][FR]    lane-31 column of q (epilogue)
-    float* sbeta = cq + G * nw * FR;         // [nfgp] FGP momentum coefficients
     const int nzero = 4 * NTW + 5 * G * NTW + 4 * G * (nw + 1) * FR + G * nw * FR;
     const int tid = g * NTW + j, nthr = NTW * G;
-    for (int e = tid; e < nzero; e += nthr) rx_r[e] = 0.f;
+    for (int e = tid; e < nzero; e += nthr) {
+        // z halos (rx_z, hz, cz) start at 0; dual halos (rx_r, hr, hp, cs, cq) at the shifted zero 1/2
+        const float* a_ = rx_r + e;
+        const bool zbuf = (a_ >= rx_z && a_ < rx_z + 2 * NTW) || (a_ >= hz && a_ < hz + 2 * G * NTW) ||
+                          (a_ >= cz && a_ < cz + 2 * G * (nw + 1) * FR);
+        rx_r[e] = zbuf ? 0.f : 0.5f;
+    }
     if (tid == 0) {
         for (int q_ = 0; q_ < 4; ++q_) mbar_init(smem_u32(bars + q_), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        // t_0 = 1, t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2, beta_k = (t_k - 1)/t_{k+1}  (Beck & Teboulle)
-        float tk = 1.f;
-        for (int it = 0; it < A.nfgp; ++it) {
-            const float tn = 0.5f * (1.f + sqrtf(1.f + 4.f * tk * tk));
-            sbeta[it] = (tk - 1.f) / tn;
-            tk = tn;
-        }
     }
 
     float b[FR], r[FR], s[FR], p[FR], q[FR], z[FR];
@@ -576,13 +584,14 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         b[k] = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
-        r[k] = 0.f; s[k] = 0.f; p[k] = 0.f; q[k] = 0.f;
+        r[k] = 0.5f; s[k] = 0.5f; p[k] = 0.5f; q[k] = 0.5f;
     }
     // step sizes with the boundary masks folded in: gamma = 0 where the dual
     // component does not exist (p: rows >= Hv-1 or invalid column; q: column
     // >= Wv-1 or invalid row); a dual that starts at 0 with step 0 stays 0.
     const float lam = A.lam;
-    const float gam = lam > 0.f ? 1.f / (8.f * lam) : 0.f;
+    const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
+    const float gam = lam > 0.f ? 1.f / (16.f * lam) : 0.f;   // step 1/(8 lam) on p = 2p' - 1
     const float gq_col = (j < Wv - 1) ? gam : 0.f;
     const float gp_col = colv ? gam : 0.f;
     const int kp = Hv - 1 - i0;                 // rows k < kp have p
@@ -625,19 +634,19 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
         // row 0 first (it needs the row above, possibly from the CTA above) and push
         // it at once, so the exchange overlaps rows 1..FR-1
         {
-            float rabove = 0.f;
+            float rabove = 0.5f;
             if (g > 0) {
                 rabove = hr[pb * hstride + (g - 1) * NTW + j];
             } else if (has_up && it > 0) {
                 mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
                 rabove = rx_r[pb * NTW + j];
             }
-            z[0] = b[0] - lam * (r[0] + s[0] - rabove - z[0]);
+            z[0] = b[0] - lam2 * (r[0] + s[0] - rabove - z[0]);
             if (g == 0 && has_up) st_async_f32(rem_rx_z + cb * row_bytes, z[0], rem_bar_z + cb * 8);
             hz[cb * hstride + g * NTW + j] = z[0];
         }
         #pragma unroll
-        for (int k = 1; k < FR; ++k) z[k] = b[k] - lam * (r[k] + s[k] - r[k - 1] - z[k]);
+        for (int k = 1; k < FR; ++k) z[k] = b[k] - lam2 * (r[k] + s[k] - r[k - 1] - z[k]);
         if (lane == 0) {
             float* czw = cz + cb * cstride + (g * (nw + 1) + warp) * FR;
             #pragma unroll
@@ -645,7 +654,7 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
         }
         __syncthreads();
         // ---- phase B: dual ascent, projection on [-1,1], FGP momentum
-        const float beta = sbeta[it];
+        const float beta = c_fgp_beta[it];
         float zr[FR];
         {
             // lane 31 reads the next warp's slot, the others the zero pad slot after the last warp
@@ -673,8 +682,8 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
             }
             const float gp = k < kp ? gp_col : 0.f;
             const float gq = k < kq ? gq_col : 0.f;
-            const float pn = clip1(fmaf(gp, z[k] - zbelow, r[k]));
-            const float qn = clip1(fmaf(gq, z[k] - zr[k], s[k]));
+            const float pn = __saturatef(fmaf(gp, z[k] - zbelow, r[k]));
+            const float qn = __saturatef(fmaf(gq, z[k] - zr[k], s[k]));
             r[k] = fmaf(beta, pn - p[k], pn);
             s[k] = fmaf(beta, qn - q[k], qn);
             p[k] = pn;
@@ -685,8 +694,8 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
         if (kq >= FR && kp >= FR) {             // interior strip: no row masks
             #pragma unroll
             for (int k = 0; k < FR - 1; ++k) {
-                const float pn = clip1(fmaf(gp_col, z[k] - z[k + 1], r[k]));
-                const float qn = clip1(fmaf(gq_col, z[k] - zr[k], s[k]));
+                const float pn = __saturatef(fmaf(gp_col, z[k] - z[k + 1], r[k]));
+                const float qn = __saturatef(fmaf(gq_col, z[k] - zr[k], s[k]));
                 r[k] = fmaf(beta, pn - p[k], pn);
                 s[k] = fmaf(beta, qn - q[k], qn);
                 p[k] = pn;
@@ -697,8 +706,8 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
             for (int k = 0; k < FR - 1; ++k) {
                 const float gp = k < kp ? gp_col : 0.f;
                 const float gq = k < kq ? gq_col : 0.f;
-                const float pn = clip1(fmaf(gp, z[k] - z[k + 1], r[k]));
-                const float qn = clip1(fmaf(gq, z[k] - zr[k], s[k]));
+                const float pn = __saturatef(fmaf(gp, z[k] - z[k + 1], r[k]));
+                const float qn = __saturatef(fmaf(gq, z[k] - zr[k], s[k]));
                 r[k] = fmaf(beta, pn - p[k], pn);
                 s[k] = fmaf(beta, qn - q[k], qn);
                 p[k] = pn;
@@ -726,14 +735,14 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     }
     cl.sync();
     const float* hp_up = g > 0 ? hp + (g - 1) * NTW : (has_up ? cl.map_shared_rank(hp, kr - 1) + (G - 1) * NTW : nullptr);
-    const float pabove = hp_up ? hp_up[j] : 0.f;
+    const float pabove = hp_up ? hp_up[j] : 0.5f;
     const float* cql = cq + (g * nw + warp - 1) * FR;
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const float pup = k > 0 ? p[k - 1] : pabove;
         float ql = __shfl_up_sync(0xffffffffu, q[k], 1);
-        if (lane == 0) ql = warp > 0 ? cql[k] : 0.f;
-        const float x = b[k] - lam * (p[k] + q[k] - pup - ql);
+        if (lane == 0) ql = warp > 0 ? cql[k] : 0.5f;
+        const float x = b[k] - lam2 * (p[k] + q[k] - pup - ql);
         const int i = i0 + k;
         if (colv && i < Hv) {
             if (MODE == 0) {

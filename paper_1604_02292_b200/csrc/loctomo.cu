@@ -206,9 +206,10 @@ struct FgpCfg { int NTW, G, K, FR, NT; size_t smem; };
 
 int fgp_config(int rows, int cols, int nfgp, FgpCfg* c) {
     if (rows < 1 || cols < 1 || cols > 256) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
-    static int fr_env = -1;
+    static int fr_env = -1, nt_env = -1;
     if (fr_env < 0) { const char* e = getenv("LT_FGP_FR"); fr_env = (e && atoi(e) == 16) ? 16 : 8; }
-    const int FRv = fr_env, NT = FRv == 8 ? 512 : 256;
+    if (nt_env < 0) { const char* e = getenv("LT_FGP_NT"); nt_env = (e && atoi(e) == 1024) ? 1024 : 512; }
+    const int FRv = fr_env, NT = FRv == 8 ? nt_env : 256;
     const int ntw = 32 * ((cols + 31) / 32);
     const int strips = (rows + FRv - 1) / FRv;
     const int G = std::max(1, std::min(strips, NT / ntw));
@@ -216,7 +217,8 @@ int fgp_config(int rows, int cols, int nfgp, FgpCfg* c) {
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
     const int nw = ntw / 32;
     c->NTW = ntw; c->G = G; c->K = K; c->FR = FRv; c->NT = NT;
-    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv + std::max(nfgp, 1)) * sizeof(float);
+    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv) * sizeof(float);
+    (void)nfgp;
     return LT_OK;
 }
 
@@ -246,10 +248,29 @@ int launch_fgp_t(FgpArgs A, const FgpCfg& c, int ntiles, cudaStream_t st) {
     return LT_OK;
 }
 
+// host-computed FGP momentum table in constant memory (uploaded when n_FGP grows)
+int ensure_fgp_beta(int nfgp, cudaStream_t st) {
+    static int have = 0;
+    static float tab[FGP_MAX_IT];
+    if (nfgp <= have) return LT_OK;
+    double t = 1.0;
+    for (int k = 0; k < FGP_MAX_IT; ++k) {
+        const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+        tab[k] = (float)((t - 1.0) / tn);
+        t = tn;
+    }
+    LT_CUDA(cudaMemcpyToSymbolAsync(c_fgp_beta, tab, sizeof tab, 0, cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    have = FGP_MAX_IT;
+    return LT_OK;
+}
+
 template <int MODE>
 int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     FgpCfg c;
     if (int rc = fgp_config(rows, cols, A.nfgp, &c)) return rc;
+    if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
+    if (c.FR == 8 && c.NT == 1024) return launch_fgp_t<MODE, 8, 1024>(A, c, ntiles, st);
     if (c.FR == 8) return launch_fgp_t<MODE, 8, 512>(A, c, ntiles, st);
     return launch_fgp_t<MODE, 16, 256>(A, c, ntiles, st);
 }
