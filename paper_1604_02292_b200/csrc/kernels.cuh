@@ -579,11 +579,18 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
-    float b[FR], r[FR], s[FR], p[FR], q[FR], z[FR];
+    // 1024-thread CTAs (NT = 1024, full 256-column tiles) keep b in shared memory
+    // to stay within 64 registers; the others keep it in registers
+    constexpr bool BSM = NT >= 1024;
+    constexpr int BNT = 256;                    // NTW of the BSM variant
+    float breg[BSM ? 1 : FR], r[FR], s[FR], p[FR], q[FR], z[FR];
+    float* bsm = cq + G * nw * FR + (g * FR) * BNT + j;     // [G][FR][256] (BSM only)
+    auto bval = [&](int k) -> float { if constexpr (BSM) return bsm[k * BNT]; else return breg[k]; };
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)(vr0 + i0) * A.b_pitch + vc0 + j;
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
-        b[k] = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
+        const float bv = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
+        if constexpr (BSM) bsm[k * BNT] = bv; else breg[k] = bv;
         r[k] = 0.5f; s[k] = 0.5f; p[k] = 0.5f; q[k] = 0.5f;
     }
     // step sizes with the boundary masks folded in: gamma = 0 where the dual
@@ -641,12 +648,12 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
                 mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
                 rabove = rx_r[pb * NTW + j];
             }
-            z[0] = b[0] - lam2 * (r[0] + s[0] - rabove - z[0]);
+            z[0] = bval(0) - lam2 * (r[0] + s[0] - rabove - z[0]);
             if (g == 0 && has_up) st_async_f32(rem_rx_z + cb * row_bytes, z[0], rem_bar_z + cb * 8);
             hz[cb * hstride + g * NTW + j] = z[0];
         }
         #pragma unroll
-        for (int k = 1; k < FR; ++k) z[k] = b[k] - lam2 * (r[k] + s[k] - r[k - 1] - z[k]);
+        for (int k = 1; k < FR; ++k) z[k] = bval(k) - lam2 * (r[k] + s[k] - r[k - 1] - z[k]);
         if (lane == 0) {
             float* czw = cz + cb * cstride + (g * (nw + 1) + warp) * FR;
             #pragma unroll
@@ -742,7 +749,7 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
         const float pup = k > 0 ? p[k - 1] : pabove;
         float ql = __shfl_up_sync(0xffffffffu, q[k], 1);
         if (lane == 0) ql = warp > 0 ? cql[k] : 0.5f;
-        const float x = b[k] - lam2 * (p[k] + q[k] - pup - ql);
+        const float x = bval(k) - lam2 * (p[k] + q[k] - pup - ql);
         const int i = i0 + k;
         if (colv && i < Hv) {
             if (MODE == 0) {

@@ -209,15 +209,15 @@ int fgp_config(int rows, int cols, int nfgp, FgpCfg* c) {
     static int fr_env = -1, nt_env = -1;
     if (fr_env < 0) { const char* e = getenv("LT_FGP_FR"); fr_env = (e && atoi(e) == 16) ? 16 : 8; }
     if (nt_env < 0) { const char* e = getenv("LT_FGP_NT"); nt_env = (e && atoi(e) == 1024) ? 1024 : 512; }
-    const int FRv = fr_env, NT = FRv == 8 ? nt_env : 256;
     const int ntw = 32 * ((cols + 31) / 32);
+    const int FRv = fr_env, NT = FRv == 8 ? ((nt_env == 1024 && ntw == 256) ? 1024 : 512) : 256;
     const int strips = (rows + FRv - 1) / FRv;
     const int G = std::max(1, std::min(strips, NT / ntw));
     const int K = (strips + G - 1) / G;
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
     const int nw = ntw / 32;
     c->NTW = ntw; c->G = G; c->K = K; c->FR = FRv; c->NT = NT;
-    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv) * sizeof(float);
+    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv + (NT >= 1024 ? G * FRv * 256 : 0)) * sizeof(float);
     (void)nfgp;
     return LT_OK;
 }
