@@ -257,10 +257,21 @@ def run_ours(args, cfg):
     else:
         work = 0.0
     achieved = work / (avg_ms / 1e3) / 1e12
-    roofline = {"kernel": {"fgp": "k_fgp", "fp": "k_fp", "bp": "k_bp", "conv": "k_conv"}[dom],
+    kname = {"fgp": "k_fgp", "fp": "k_fp_roi", "bp": "k_bp", "conv": "k_conv"}[dom]
+    traffic = None
+    try:   # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            tj = json.load(f)
+        if kname in tj:
+            traffic = {"bytes_per_launch": tj[kname]["dram_bytes_per_launch"], "source": tj[kname]["source"]}
+    except Exception:
+        traffic = None
+    roofline = {"kernel": kname,
                 "bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak_tflops, 1),
-                "unit": "TFLOP/s", "frac": round(achieved / alu_peak_tflops, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved / alu_peak_tflops, 4), "traffic": traffic,
                 "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)",
+                "work_per_unit": ("21 FP32 flops per pixel-iteration" if dom == "fgp" else
+                                  f"{JOSEPH_FLOPS_PER_UPDATE:g} FP32 flops per pixel-angle update"),
                 "avg_launch_ms": round(avg_ms, 4), "launches": dom_n,
                 "share_of_step": round(dom_ms / elapsed_ms, 3)}
     kshare = {k: {"ms_per_step": round(v[0] / args.steps, 3), "launches_per_step": v[1] // args.steps}

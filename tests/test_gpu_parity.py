@@ -267,3 +267,50 @@ def test_determinism_and_empty(lt):
     assert empty.R == 0
     empty.filter_bank()
     assert empty.sirt_solve(gpu(inp.sino)).shape == (0, 24, 24)
+
+
+def test_tv_solve_C2_full(lt, orc):
+    """C2 exactly as configured: 512^2, 64 angles, 16 seeded ROIs, TV lambda 0.05,
+    200 iterations x 100 FGP iterations, disc on; every ROI core vs the oracle."""
+    cfg = synth.config("C2")
+    inp = synth.make_inputs("C2")
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.tv_solve(gpu(inp.sino), cfg.lam, cfg.n_fgp))
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, inp.centres, cfg.radius, cfg.margin,
+                       cfg.n_iter, mode="tv", lam=cfg.lam, n_fgp=cfg.n_fgp)
+    for q, g in enumerate(plan.local_rois):
+        assert relerr(cores[q], ref[g]) <= 1e-3, g
+    # combine of the full batch vs the oracle's stitch of the oracle cores
+    img = cpu(plan.combine(gpu(cores), plan.local_rois))
+    assert relerr(img, orc.stitch(cfg.n, inp.centres, cfg.radius, ref)) <= 1e-3
+
+
+def test_full_size_C5_sampled(lt, orc):
+    """C5 geometry (4096^2, 256 angles, 5793 bins) with the full 1024-ROI batch,
+    nonneg SIRT, n = 3; 6 sampled ROIs against the oracle."""
+    cfg = synth.config("C5")
+    inp = synth.make_inputs("C5")
+    n_iter = 3
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.sirt_solve(gpu(inp.sino), 0.0, math.inf))
+    sample = np.array([0, 31, 992, 1023, 500, 529])
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, inp.centres[sample], cfg.radius,
+                       cfg.margin, n_iter, mode="box")
+    for k, g in enumerate(sample):
+        q = int(np.nonzero(plan.local_rois == g)[0][0])
+        assert relerr(cores[q], ref[k]) <= 1e-3, g
+
+
+def test_host_buffer_entry_matches_device_path(lt):
+    """lt_solve_host (the e2e entry bench.py times) == device solve + combine."""
+    cfg = synth.config("C1")
+    inp = synth.make_inputs("C1")
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, 20)
+    plan.filter_bank()
+    cores = plan.sirt_solve(gpu(inp.sino), 0.0, math.inf)
+    img_dev = cpu(plan.combine(cores, plan.local_rois))
+    img_host = plan.solve_host("sirt", torch.from_numpy(inp.sino).pin_memory(), 0.0, math.inf)
+    torch.cuda.synchronize()
+    assert np.array_equal(img_host.numpy().astype(np.float64), img_dev)
