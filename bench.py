@@ -258,17 +258,19 @@ def run_ours(args, cfg):
         work = 0.0
     achieved = work / (avg_ms / 1e3) / 1e12
     kname = {"fgp": "k_fgp", "fp": "k_fp_roi", "bp": "k_bp", "conv": "k_conv"}[dom]
-    traffic = None
+    traffic, traffic_src = None, None
     try:   # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
             tj = json.load(f)
         if kname in tj:
-            traffic = {"bytes_per_launch": tj[kname]["dram_bytes_per_launch"], "source": tj[kname]["source"]}
+            traffic = float(tj[kname]["dram_bytes_per_launch"])
+            traffic_src = tj[kname]["source"]
     except Exception:
         traffic = None
     roofline = {"kernel": kname,
                 "bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak_tflops, 1),
                 "unit": "TFLOP/s", "frac": round(achieved / alu_peak_tflops, 4), "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                 "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)",
                 "work_per_unit": ("21 FP32 flops per pixel-iteration" if dom == "fgp" else
                                   f"{JOSEPH_FLOPS_PER_UPDATE:g} FP32 flops per pixel-angle update"),
