@@ -581,17 +581,26 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
 
     // 1024-thread CTAs (NT = 1024, full 256-column tiles) keep b in shared memory
     // to stay within 64 registers; the others keep it in registers
+    // 1024-thread CTAs (NT = 1024, full 256-column tiles, 32 rows per CTA) keep
+    // b, p, q in shared memory (each is touched once per iteration) and r, s, z
+    // in registers, to stay within 64 registers; the others keep all in registers
     constexpr bool BSM = NT >= 1024;
     constexpr int BNT = 256;                    // NTW of the BSM variant
-    float breg[BSM ? 1 : FR], r[FR], s[FR], p[FR], q[FR], z[FR];
+    float breg[BSM ? 1 : FR], r[FR], s[FR], preg[BSM ? 1 : FR], qreg[BSM ? 1 : FR], z[FR];
     float* bsm = cq + G * nw * FR + (g * FR) * BNT + j;     // [G][FR][256] (BSM only)
+    float* psm = bsm + G * FR * BNT;                          // [G][FR][256]
+    float* qsm = psm + G * FR * BNT;                          // [G][FR][256]
     auto bval = [&](int k) -> float { if constexpr (BSM) return bsm[k * BNT]; else return breg[k]; };
+    auto pval = [&](int k) -> float { if constexpr (BSM) return psm[k * BNT]; else return preg[k]; };
+    auto qval = [&](int k) -> float { if constexpr (BSM) return qsm[k * BNT]; else return qreg[k]; };
+    auto pset = [&](int k, float v) { if constexpr (BSM) psm[k * BNT] = v; else preg[k] = v; };
+    auto qset = [&](int k, float v) { if constexpr (BSM) qsm[k * BNT] = v; else qreg[k] = v; };
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)(vr0 + i0) * A.b_pitch + vc0 + j;
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const float bv = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
         if constexpr (BSM) bsm[k * BNT] = bv; else breg[k] = bv;
-        r[k] = 0.5f; s[k] = 0.5f; p[k] = 0.5f; q[k] = 0.5f;
+        r[k] = 0.5f; s[k] = 0.5f; pset(k, 0.5f); qset(k, 0.5f);
     }
     // step sizes with the boundary masks folded in: gamma = 0 where the dual
     // component does not exist (p: rows >= Hv-1 or invalid column; q: column
@@ -691,10 +700,10 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
             const float gq = k < kq ? gq_col : 0.f;
             const float pn = __saturatef(fmaf(gp, z[k] - zbelow, r[k]));
             const float qn = __saturatef(fmaf(gq, z[k] - zr[k], s[k]));
-            r[k] = fmaf(beta, pn - p[k], pn);
-            s[k] = fmaf(beta, qn - q[k], qn);
-            p[k] = pn;
-            q[k] = qn;
+            r[k] = fmaf(beta, pn - pval(k), pn);
+            s[k] = fmaf(beta, qn - qval(k), qn);
+            pset(k, pn);
+            qset(k, qn);
             if (g == G - 1 && has_dn) st_async_f32(rem_rx_r + cb * row_bytes, r[k], rem_bar_r + cb * 8);
             hr[cb * hstride + g * NTW + j] = r[k];
         }
@@ -703,10 +712,10 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
             for (int k = 0; k < FR - 1; ++k) {
                 const float pn = __saturatef(fmaf(gp_col, z[k] - z[k + 1], r[k]));
                 const float qn = __saturatef(fmaf(gq_col, z[k] - zr[k], s[k]));
-                r[k] = fmaf(beta, pn - p[k], pn);
-                s[k] = fmaf(beta, qn - q[k], qn);
-                p[k] = pn;
-                q[k] = qn;
+                r[k] = fmaf(beta, pn - pval(k), pn);
+                s[k] = fmaf(beta, qn - qval(k), qn);
+                pset(k, pn);
+                qset(k, qn);
             }
         } else {
             #pragma unroll
@@ -715,10 +724,10 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
                 const float gq = k < kq ? gq_col : 0.f;
                 const float pn = __saturatef(fmaf(gp, z[k] - z[k + 1], r[k]));
                 const float qn = __saturatef(fmaf(gq, z[k] - zr[k], s[k]));
-                r[k] = fmaf(beta, pn - p[k], pn);
-                s[k] = fmaf(beta, qn - q[k], qn);
-                p[k] = pn;
-                q[k] = qn;
+                r[k] = fmaf(beta, pn - pval(k), pn);
+                s[k] = fmaf(beta, qn - qval(k), qn);
+                pset(k, pn);
+                qset(k, qn);
             }
         }
         if (lane == 31) {
@@ -735,6 +744,9 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     }
     if (it < nit) fgp_iter(it, std::integral_constant<int, 0>{});
     // ---- x = b - lam L(p, q), then the epilogue
+    float p[FR], q[FR];
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) { p[k] = pval(k); q[k] = qval(k); }
     hp[g * NTW + j] = p[FR - 1];
     if (lane == 31) {
         #pragma unroll

@@ -96,8 +96,10 @@ struct lt_plan {
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
     int nsplit = 1;
-    cudaStream_t gst[2] = {nullptr, nullptr};
+    cudaStream_t gst[2] = {nullptr, nullptr};        // per group: projector work (low priority)
+    cudaStream_t fst[2] = {nullptr, nullptr};        // per group: FGP (high priority)
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t pev[2] = {nullptr, nullptr}, fev[2] = {nullptr, nullptr};
     struct {
         size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
@@ -217,7 +219,7 @@ int fgp_config(int rows, int cols, int nfgp, FgpCfg* c) {
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
     const int nw = ntw / 32;
     c->NTW = ntw; c->G = G; c->K = K; c->FR = FRv; c->NT = NT;
-    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv + (NT >= 1024 ? G * FRv * 256 : 0)) * sizeof(float);
+    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv + (NT >= 1024 ? 3 * G * FRv * 256 : 0)) * sizeof(float);
     (void)nfgp;
     return LT_OK;
 }
@@ -318,7 +320,8 @@ int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
 
 // the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
 // one ROI group (tiles [t0, t0 + cnt)) through all n iterations on stream st
-int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st) {
+int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st,
+                     cudaStream_t fst = nullptr, cudaEvent_t pev = nullptr, cudaEvent_t fev = nullptr) {
     Tiles t = p.roi_tiles();
     t.tile += t0; t.d0 += (size_t)t0 * p.na; t.tauc += (size_t)t0 * p.na; t.ntiles = cnt;
     const long long yts = p.ytile();
@@ -339,6 +342,7 @@ int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, 
         e.discc = p.P<float>(p.off.discc32); e.use_disc = disc;
         e.alpha = (float)p.alpha; e.lo = lo; e.hi = hi; e.last = (k == p.n_iter - 1);
         const SinoView vb = view_full(bk, p.nd);
+        if (fst && k > 0) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));    // previous FGP of this group
         if (k == 0) {
             // y^0 = 0: W_{L'} y^0 = 0, single-sinogram gather
             if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vb, vb, e, st)) return rc; }
@@ -361,9 +365,17 @@ int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, 
             A.xs = xs; A.xprev = xprev; A.p_tstride = p.ptile(); A.T = p.T;
             A.y = y; A.yT = yT; A.y_tstride = yts; A.TP = p.TP;
             A.beta_o = (float)beta;
-            if (int rc = launch_fgp<1>(A, p.T, p.T, cnt, st)) return rc;
+            if (fst) {
+                LT_CUDA(cudaEventRecord(pev, st));
+                LT_CUDA(cudaStreamWaitEvent(fst, pev, 0));
+                if (int rc = launch_fgp<1>(A, p.T, p.T, cnt, fst)) return rc;
+                LT_CUDA(cudaEventRecord(fev, fst));
+            } else {
+                if (int rc = launch_fgp<1>(A, p.T, p.T, cnt, st)) return rc;
+            }
         }
     }
+    if (fst && mode == 1) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));      // the group's stream ends after its last FGP
     return LT_OK;
 }
 
@@ -383,7 +395,10 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
         for (int g = 0; g < 2; ++g) {
             LT_CUDA(cudaStreamWaitEvent(p.gst[g], p.gev[2], 0));
             const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
-            if (int rc = group_iterations(p, t0, cnt, mode, lo, hi, lam, nfgp, p.gst[g])) return rc;
+            const bool prio = p.fst[g] && mode == 1;
+            if (prio) LT_CUDA(cudaStreamWaitEvent(p.fst[g], p.gev[2], 0));
+            if (int rc = group_iterations(p, t0, cnt, mode, lo, hi, lam, nfgp, p.gst[g], prio ? p.fst[g] : nullptr,
+                                          p.pev[g], p.fev[g])) return rc;
             LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
         }
         // join
@@ -657,7 +672,16 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     if (!p->gst[0]) {
         const char* e = getenv("LT_SPLIT");
         p->nsplit = (e && atoi(e) == 1) ? 1 : 2;
-        for (int g = 0; g < 2; ++g) LT_CUDA(cudaStreamCreateWithFlags(&p->gst[g], cudaStreamNonBlocking));
+        int lo_prio = 0, hi_prio = 0;
+        LT_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        const char* pe = getenv("LT_PRIO");
+        const bool use_prio = !(pe && atoi(pe) == 0);
+        for (int g = 0; g < 2; ++g) {
+            LT_CUDA(cudaStreamCreateWithPriority(&p->gst[g], cudaStreamNonBlocking, lo_prio));
+            if (use_prio) LT_CUDA(cudaStreamCreateWithPriority(&p->fst[g], cudaStreamNonBlocking, hi_prio));
+            LT_CUDA(cudaEventCreateWithFlags(&p->pev[g], cudaEventDisableTiming));
+            LT_CUDA(cudaEventCreateWithFlags(&p->fev[g], cudaEventDisableTiming));
+        }
         for (int g = 0; g < 3; ++g) LT_CUDA(cudaEventCreateWithFlags(&p->gev[g], cudaEventDisableTiming));
     }
     p->bound = true;
@@ -955,8 +979,12 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
 
 void lt_plan_destroy(lt_plan* p) {
     if (!p) return;
-    for (int g = 0; g < 2; ++g)
+    for (int g = 0; g < 2; ++g) {
         if (p->gst[g]) cudaStreamDestroy(p->gst[g]);
+        if (p->fst[g]) cudaStreamDestroy(p->fst[g]);
+        if (p->pev[g]) cudaEventDestroy(p->pev[g]);
+        if (p->fev[g]) cudaEventDestroy(p->fev[g]);
+    }
     for (int g = 0; g < 3; ++g)
         if (p->gev[g]) cudaEventDestroy(p->gev[g]);
     delete p;
