@@ -327,6 +327,8 @@ enum BpMode {
 };
 
 struct BpEpi {
+    const int* blist;                                      // sub-tile list (nullable: all sub-tiles of the tile)
+    const float* xsg; int xsg_pitch;                       // global x_s^k = W^T b_k image (BOX/TV with NS <= 1)
     float* out; long long out_tstride; int out_pitch;     // plain outputs
     float* y; float* yT; long long y_tstride;              // padded tile images (state)
     float* v; float* xs; long long p_tstride;              // plain [T][T] (TV)
@@ -344,7 +346,8 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     const int r = blockIdx.y;
     const int T = t.T, na = g.na;
     const int nsx = (T + 31) >> 5;
-    const int sty = blockIdx.x / nsx, stx = blockIdx.x - sty * nsx;
+    const int sub = e.blist ? __ldg(e.blist + blockIdx.x) : (int)blockIdx.x;
+    const int sty = sub / nsx, stx = sub - sty * nsx;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int pj = stx * 32 + tx;
     const int pi0 = sty * 32 + ty * 4;
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     const float dx = (float)tx - 15.5f, dy0 = (float)(ty * 4) - 15.5f;
 
     float g1[4] = {0.f, 0.f, 0.f, 0.f}, g2[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int a0 = 0; a0 < na; a0 += BP_CA) {
+    for (int a0 = 0; a0 < (NS > 0 ? na : 0); a0 += BP_CA) {
         const int ca = min(BP_CA, na - a0);
         __syncthreads();
         for (int q = threadIdx.x; q < ca; q += blockDim.x) {
@@ -423,9 +426,17 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
                     const int u = 2 * gj - n + 1, v = 2 * gi - n + 1;   // 2x, 2y of the pixel centre
                     dval = (u * u + v * v <= n * n) ? discc : 0.f;      // D: centred disc, diameter N
                 }
-                xs = g1[p] + dval;                                       // x_s^k = FBP_L(p_c, u_k) + c D
+                float wts;                                               // (W_{L'}^T W_{L'} y)_j
+                if (e.xsg) {
+                    // x_s^k = M_{L'} W^T b_k: the global backprojection, read at this pixel
+                    xs = __ldg(e.xsg + (long long)(ti.row0 + i) * e.xsg_pitch + (ti.col0 + j)) + dval;
+                    wts = NS >= 1 ? g1[p] : 0.f;
+                } else {
+                    xs = g1[p] + dval;                                   // x_s^k = FBP_L(p_c, u_k) + c D
+                    wts = NS == 2 ? g2[p] : 0.f;
+                }
                 yv = e.y[pp];
-                const float S = xs + yv - e.alpha * g2[p];               // S(x^{k-1}) split
+                const float S = xs + yv - e.alpha * wts;                 // S(x^{k-1}) split
                 if (MODE == BP_BOX) {
                     const float x = fminf(fmaxf(S, e.lo), e.hi);         // eq. sirtbox
                     val = e.last ? x : x - xs;                           // y^k = clamp(S) - x_s^k
@@ -775,6 +786,308 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
                 A.xprev[pl] = x;
                 A.y[(long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + tj] = yv;
                 A.yT[(long long)tile * A.y_tstride + (long long)tj * A.TP + PADL + ti_] = yv;
+            }
+        }
+    }
+    cl.sync();   // keep shared memory alive until every neighbour has read its halo
+}
+
+// ---------------------------------------------------------------------------
+// k_fgp2: the same FGP + FISTA epilogue as k_fgp, laid out for the sm_100
+// paired FP32 datapath (FFMA2 / FADD2: two fp32 lanes per instruction).
+//
+// Warp w of CTA k owns FR full rows (rows (k*NW + w)*FR ...) of the tile, 256
+// columns wide; lane l owns the 8 consecutive columns 8l..8l+7 of each row, as
+// four column pairs.  Vertical neighbours are the same lane (aligned pairs ->
+// paired instructions); the horizontal neighbour across a lane boundary comes
+// by one warp shuffle per row and direction.  Rows crossing warps go through
+// shared memory, rows crossing CTAs through DSMEM (st.async + mbarrier), as in
+// k_fgp.  Per pixel-iteration ~8 issue slots (k_fgp: ~30).
+//
+// Masks (A13, Neumann boundary on the valid rectangle H_v x W_v):
+// p exists for rows i < H_v - 1 (warp-uniform per row), q for columns
+// j < W_v - 1 (per-column step register).  Pixels outside the valid rectangle
+// carry finite garbage that no valid pixel reads.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
+// row storage in shared memory: column 8l + c of a 256-wide row at
+// (c >> 2) * 128 + 4l + (c & 3), so each lane moves its octet as two
+// conflict-free 128-bit accesses
+__device__ __forceinline__ void row_st(float* row, int lane, const float2 (&v)[4]) {
+    reinterpret_cast<float4*>(row)[lane] = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+    reinterpret_cast<float4*>(row + 128)[lane] = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+}
+__device__ __forceinline__ void row_ld(const float* row, int lane, float2 (&v)[4]) {
+    const float4 a = reinterpret_cast<const float4*>(row)[lane];
+    const float4 b = reinterpret_cast<const float4*>(row + 128)[lane];
+    v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
+    v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_v4(unsigned remote, float4 v, unsigned remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(remote), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void row_push(unsigned remote_row, int lane, const float2 (&v)[4], unsigned remote_bar) {
+    st_async_v4(remote_row + 16u * lane, make_float4(v[0].x, v[0].y, v[1].x, v[1].y), remote_bar);
+    st_async_v4(remote_row + 512u + 16u * lane, make_float4(v[2].x, v[2].y, v[3].x, v[3].y), remote_bar);
+}
+
+constexpr int FGP2_ROW = 256;     // columns per warp row (32 lanes x 8)
+template <int V> struct Parity { __device__ __forceinline__ operator int() const { return V; } };
+
+template <int FR, int NW>
+struct Fgp2Smem {
+    static constexpr int bars = 0;                             // 4 x u64: r from above [2], z from below [2]
+    static constexpr int wbar = 8;                             // [NW][4] u64: r row of warp w ready [2], z row [2]
+    static constexpr int rx_r = wbar + 8 * NW;                 // [2][256] r row pushed by the CTA above
+    static constexpr int rx_z = rx_r + 2 * FGP2_ROW;           // [2][256] z row pushed by the CTA below
+    static constexpr int hr = rx_z + 2 * FGP2_ROW;             // [2][NW][256] last r row of each warp
+    static constexpr int hz = hr + 2 * NW * FGP2_ROW;          // [2][NW][256] first z row of each warp
+    static constexpr int hp = hz + 2 * NW * FGP2_ROW;          // [NW][256] last p row (epilogue)
+    static constexpr int total = hp + NW * FGP2_ROW;
+};
+
+template <int MODE, int FR, int NW, int SYNC>
+__global__ void __launch_bounds__(NW * 32, 1) k_fgp2(FgpArgs A) {
+    using SM = Fgp2Smem<FR, NW>;
+    extern __shared__ __align__(16) float sm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int K = (int)cl.num_blocks();
+    const int kr = (int)cl.block_rank();
+    const int tile = blockIdx.y;
+    int vr0 = 0, vc0 = 0, Hv = A.H, Wv = A.W;
+    if (A.tiles) {
+        const TileT ti = A.tiles[tile];
+        vr0 = ti.vr0; vc0 = ti.vc0; Hv = ti.vr1 - ti.vr0; Wv = ti.vc1 - ti.vc0;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i0 = (kr * NW + w) * FR;          // first row of this warp (valid-rectangle coordinates)
+    const int x0 = lane * 8;                    // first column of this lane
+    const bool has_up = kr > 0, has_dn = kr < K - 1;
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + SM::bars);
+    float* rx_r = sm + SM::rx_r;
+    float* rx_z = sm + SM::rx_z;
+    float* hr = sm + SM::hr;
+    float* hz = sm + SM::hz;
+    float* hp = sm + SM::hp;
+    for (int e = threadIdx.x; e < SM::total - SM::rx_r; e += NW * 32) {
+        const int o = SM::rx_r + e;
+        const bool zb = (o >= SM::rx_z && o < SM::hr) || (o >= SM::hz && o < SM::hp);
+        sm[o] = zb ? 0.f : 0.5f;               // z halos start at 0, dual halos at the shifted zero 1/2
+    }
+    unsigned long long* wbar = reinterpret_cast<unsigned long long*>(sm + SM::wbar);
+    if (threadIdx.x == 0) {
+        for (int q_ = 0; q_ < 4; ++q_) mbar_init(smem_u32(bars + q_), 1);
+        for (int q_ = 0; q_ < 4 * NW; ++q_) mbar_init(smem_u32(wbar + q_), 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // warp-to-warp signals (no CTA barrier in the iteration loop): warp w
+    // arrives on wr(w, parity) after storing its last r row, on wz(w, parity)
+    // after storing its first z row; its neighbours wait on them
+    const unsigned wbar0 = smem_u32(wbar);
+    auto wr = [&](int ww, int par) { return wbar0 + 8u * (4 * ww + par); };
+    auto wz = [&](int ww, int par) { return wbar0 + 8u * (4 * ww + 2 + par); };
+
+    float2 b[FR][4], r[FR][4], s[FR][4], p[FR][4], q[FR][4], z[FR][4];
+    const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)vr0 * A.b_pitch + vc0;
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) {
+        const int i = i0 + k;
+        #pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) {
+            const int x = x0 + 2 * c2;
+            const bool rv = i < Hv;
+            const float bx = (rv && x < Wv) ? __ldg(bsrc + (long long)i * A.b_pitch + x) : 0.f;
+            const float by = (rv && x + 1 < Wv) ? __ldg(bsrc + (long long)i * A.b_pitch + x + 1) : 0.f;
+            b[k][c2] = make_float2(bx, by);
+            r[k][c2] = f2s(0.5f); s[k][c2] = f2s(0.5f); p[k][c2] = f2s(0.5f); q[k][c2] = f2s(0.5f);
+        }
+    }
+    const float lam = A.lam;
+    const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
+    const float gam = lam > 0.f ? 1.f / (16.f * lam) : 0.f;
+    // q step per column (0 where q does not exist: j >= W_v - 1)
+    float gq[8];
+    #pragma unroll
+    for (int c = 0; c < 8; ++c) gq[c] = (x0 + c < Wv - 1) ? gam : 0.f;
+    float2 gq2[4];
+    #pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) gq2[c2] = make_float2(gq[2 * c2], gq[2 * c2 + 1]);
+    cl.sync();
+    const unsigned up_rank = has_up ? kr - 1 : kr, dn_rank = has_dn ? kr + 1 : kr;
+    const unsigned rem_rx_r = mapa(smem_u32(rx_r), dn_rank);      // my last warp's r row -> CTA below
+    const unsigned rem_bar_r = mapa(smem_u32(bars + 0), dn_rank);
+    const unsigned rem_rx_z = mapa(smem_u32(rx_z), up_rank);      // my first warp's z row -> CTA above
+    const unsigned rem_bar_z = mapa(smem_u32(bars + 2), up_rank);
+    constexpr unsigned row_bytes = FGP2_ROW * 4;
+    const int nit = lam > 0.f ? A.nfgp : 0;
+    const unsigned bar0 = smem_u32(bars);
+    const float2 nl2 = f2s(-lam2);
+    // p step per row of this warp (0 where p does not exist: i >= H_v - 1)
+    float gp[FR];
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) gp[k] = (i0 + k < Hv - 1) ? gam : 0.f;
+
+    // SYNC 0: CTA barrier after each phase; 1: warp-to-warp mbarrier signals
+    // (parity cb: compile-time in the barrier variant, so every halo address is loop invariant)
+    auto fgp_iter = [&](int it, auto cbv) {
+        const int cb = cbv, pb = cb ^ 1;
+        if (lane == 0) {   // the consuming warp arms its DSMEM receive buffers
+            if (w == NW - 1 && has_dn) mbar_expect_tx(bar0 + 16 + 8 * cb, row_bytes);   // z row of it, from below
+            if (w == 0 && has_up) mbar_expect_tx(bar0 + 8 * cb, row_bytes);             // r row of it, from above
+        }
+        // ---- phase A: z = b - lam2 L(r, s); row 0 first (its upper neighbour
+        // may come from another warp or CTA) and publish it at once
+        #pragma unroll
+        for (int k = 0; k < FR; ++k) {
+            float2 rup[4];
+            if (k > 0) {
+                #pragma unroll
+                for (int c2 = 0; c2 < 4; ++c2) rup[c2] = r[k - 1][c2];
+            } else if (w > 0 && it > 0) {
+                if constexpr (SYNC == 1) mbar_wait(wr(w - 1, pb), ((it - 1) >> 1) & 1);
+                row_ld(hr + (pb * NW + w - 1) * FGP2_ROW, lane, rup);
+            } else if (w == 0 && has_up && it > 0) {
+                mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
+                row_ld(rx_r + pb * FGP2_ROW, lane, rup);
+            } else {
+                #pragma unroll
+                for (int c2 = 0; c2 < 4; ++c2) rup[c2] = f2s(0.5f);
+            }
+            float sl = __shfl_up_sync(0xffffffffu, s[k][3].y, 1);
+            if (lane == 0) sl = 0.5f;
+            // z = b - lam2 (r - rup) - lam2 s + lam2 s_left
+            float2 t[4];
+            #pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) {
+                t[c2] = f2fma(nl2, f2sub(r[k][c2], rup[c2]), b[k][c2]);
+                t[c2] = f2fma(nl2, s[k][c2], t[c2]);
+            }
+            z[k][0].x = fmaf(lam2, sl, t[0].x);
+            z[k][0].y = fmaf(lam2, s[k][0].x, t[0].y);
+            #pragma unroll
+            for (int c2 = 1; c2 < 4; ++c2) {
+                z[k][c2].x = fmaf(lam2, s[k][c2 - 1].y, t[c2].x);
+                z[k][c2].y = fmaf(lam2, s[k][c2].x, t[c2].y);
+            }
+            if (k == 0) {
+                if (w == 0 && has_up) row_push(rem_rx_z + cb * row_bytes, lane, z[0], rem_bar_z + cb * 8);
+                if (w > 0) {
+                    row_st(hz + (cb * NW + w) * FGP2_ROW, lane, z[0]);
+                    if constexpr (SYNC == 1) mbar_arrive(wz(w, cb));
+                }
+            }
+        }
+        if constexpr (SYNC == 0) __syncthreads();
+        // ---- phase B: dual ascent, projection on [0, 1] (shifted), FGP momentum;
+        // last row first and publish it
+        const float beta = c_fgp_beta[it];
+        const float2 beta2 = f2s(beta);
+        #pragma unroll
+        for (int kk = 0; kk < FR; ++kk) {
+            const int k = (kk + FR - 1) % FR;     // FR-1, 0, 1, ..., FR-2
+            float2 zb[4];
+            if (k < FR - 1) {
+                #pragma unroll
+                for (int c2 = 0; c2 < 4; ++c2) zb[c2] = z[k + 1][c2];
+            } else if (w < NW - 1) {
+                if constexpr (SYNC == 1) mbar_wait(wz(w + 1, cb), (it >> 1) & 1);
+                row_ld(hz + (cb * NW + w + 1) * FGP2_ROW, lane, zb);
+            } else if (has_dn) {
+                mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
+                row_ld(rx_z + cb * FGP2_ROW, lane, zb);
+            } else {
+                #pragma unroll
+                for (int c2 = 0; c2 < 4; ++c2) zb[c2] = f2s(0.f);
+            }
+            const float zr = __shfl_down_sync(0xffffffffu, z[k][0].x, 1);   // lane 31: masked by gq
+            const float gpk = gp[k];
+            const float2 gp2 = f2s(gpk);
+            #pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) {
+                // p' = sat(r + g (z - z_below)), q' = sat(s + g (z - z_right))
+                const float2 tp = f2fma(gp2, z[k][c2], r[k][c2]);
+                const float2 tq = f2fma(gq2[c2], z[k][c2], s[k][c2]);
+                const float zrx = z[k][c2].y;
+                const float zry = c2 < 3 ? z[k][c2 + 1].x : zr;
+                float2 pn, qn;
+                pn.x = __saturatef(fmaf(-gpk, zb[c2].x, tp.x));
+                pn.y = __saturatef(fmaf(-gpk, zb[c2].y, tp.y));
+                qn.x = __saturatef(fmaf(-gq[2 * c2], zrx, tq.x));
+                qn.y = __saturatef(fmaf(-gq[2 * c2 + 1], zry, tq.y));
+                r[k][c2] = f2fma(beta2, f2sub(pn, p[k][c2]), pn);
+                s[k][c2] = f2fma(beta2, f2sub(qn, q[k][c2]), qn);
+                p[k][c2] = pn;
+                q[k][c2] = qn;
+            }
+            if (k == FR - 1) {
+                if (w == NW - 1 && has_dn) row_push(rem_rx_r + cb * row_bytes, lane, r[FR - 1], rem_bar_r + cb * 8);
+                if (w < NW - 1) {
+                    row_st(hr + (cb * NW + w) * FGP2_ROW, lane, r[FR - 1]);
+                    if constexpr (SYNC == 1) mbar_arrive(wr(w, cb));
+                }
+            }
+        }
+        if constexpr (SYNC == 0) __syncthreads();
+    };
+    if constexpr (SYNC == 0) {
+        int it = 0;
+        for (; it + 1 < nit; it += 2) {
+            fgp_iter(it, Parity<0>{});
+            fgp_iter(it + 1, Parity<1>{});
+        }
+        if (it < nit) fgp_iter(it, Parity<0>{});
+    } else {
+        #pragma unroll 1
+        for (int it = 0; it < nit; ++it) fgp_iter(it, it & 1);
+    }
+
+    // ---- x = b - lam2 L(p', q'), then the epilogue
+    row_st(hp + w * FGP2_ROW, lane, p[FR - 1]);
+    cl.sync();
+    float2 pup0[4];
+    if (w > 0) row_ld(hp + (w - 1) * FGP2_ROW, lane, pup0);
+    else if (has_up) row_ld(cl.map_shared_rank(hp, kr - 1) + (NW - 1) * FGP2_ROW, lane, pup0);
+    else {
+        #pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) pup0[c2] = f2s(0.5f);
+    }
+    #pragma unroll
+    for (int k = 0; k < FR; ++k) {
+        const int i = i0 + k;
+        float ql = __shfl_up_sync(0xffffffffu, q[k][3].y, 1);
+        if (lane == 0) ql = 0.5f;
+        float xv[8];
+        #pragma unroll
+        for (int c2 = 0; c2 < 4; ++c2) {
+            const float2 pu = k > 0 ? p[k - 1][c2] : pup0[c2];
+            const float qlx = c2 > 0 ? q[k][c2 - 1].y : ql;
+            xv[2 * c2] = b[k][c2].x - lam2 * (p[k][c2].x + q[k][c2].x - pu.x - qlx);
+            xv[2 * c2 + 1] = b[k][c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
+        }
+        if (i < Hv) {
+            #pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int j = x0 + c;
+                if (j >= Wv) continue;
+                const float x = xv[c];
+                if (MODE == 0) {
+                    A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + j] = x;
+                } else {
+                    const int ti_ = vr0 + i, tj = vc0 + j;
+                    const long long pl = (long long)tile * A.p_tstride + (long long)ti_ * A.T + tj;
+                    const float xp = A.xprev[pl];
+                    const float rr = x + A.beta_o * (x - xp);             // FISTA extrapolation (A12)
+                    const float yv = rr - A.xs[pl];                         // x_L^k = r - x_s^k
+                    A.xprev[pl] = x;
+                    A.y[(long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + tj] = yv;
+                    A.yT[(long long)tile * A.y_tstride + (long long)tj * A.TP + PADL + ti_] = yv;
+                }
             }
         }
     }

@@ -86,6 +86,9 @@ struct lt_plan {
     std::vector<int> d0, gd0;
     std::vector<double> tauc, gtauc;
     std::vector<int> fpgroups;    // [ngroups][FP_GA] angle indices of one orientation, -1 padded
+    // 32x32 image blocks that the global x_s^k backprojection must cover: list 0 for
+    // all local ROIs, lists 1 and 2 for the two pipelined ROI groups (halves)
+    std::vector<int> xsblk[3];
     int ngroups = 0;
     // workspace
     char* ws = nullptr;
@@ -105,6 +108,7 @@ struct lt_plan {
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
+        size_t xsblk[3], xsg[2];
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -176,9 +180,10 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
 
 template <int NS, int MODE>
 int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const SinoView& s2, const BpEpi& e,
-                cudaStream_t st) {
+                cudaStream_t st, int nblist = 0) {
     const int nsx = (t.T + 31) / 32;
-    dim3 grid(nsx * nsx, t.ntiles);
+    if (e.blist && nblist == 0) return LT_OK;
+    dim3 grid(e.blist ? nblist : nsx * nsx, t.ntiles);
     ScopedTimer tm(TC_BP, st);
     k_bp<NS, MODE><<<grid, 256, 0, st>>>(p.geo(), t, s1, s2, e);
     LT_LAUNCHED();
@@ -267,11 +272,65 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
     return LT_OK;
 }
 
+// k_fgp2 (paired-FP32 layout): NW warps of FR full rows per CTA, K CTAs per
+// cluster.  LT_FGP2_CFG = "4x8" (default), "2x8", "2x16" (FR x NW);
+// LT_FGP2_SYNC = 1 replaces the per-phase CTA barrier by warp-to-warp mbarriers.
+template <int MODE, int FR, int NW, int SYNC>
+int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
+    const int K = (rows + NW * FR - 1) / (NW * FR);
+    if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
+    const size_t smem = (size_t)Fgp2Smem<FR, NW>::total * sizeof(float);
+    auto kern = k_fgp2<MODE, FR, NW, SYNC>;
+    LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(K, ntiles, 1);
+    cfg.blockDim = dim3(NW * 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ScopedTimer tm(TC_FGP, st);
+    LT_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int fgp_version() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("LT_FGP_V"); v = (e && atoi(e) == 1) ? 1 : 2; }
+    return v;
+}
+
 template <int MODE>
 int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
+    if (rows < 1 || cols < 1 || cols > 256) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
+    if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
+    if (fgp_version() == 2) {
+        static int cfgv = -1;
+        if (cfgv < 0) {
+            const char* e = getenv("LT_FGP2_CFG");
+            cfgv = !e ? 1 : !strcmp(e, "2x8") ? 2 : !strcmp(e, "2x16") ? 0 : 1;
+        }
+        static int syncv = -1;
+        if (syncv < 0) { const char* e = getenv("LT_FGP2_SYNC"); syncv = (e && atoi(e) == 1) ? 1 : 0; }
+        if (syncv == 1) {
+            if (cfgv == 1) return launch_fgp2_t<MODE, 4, 8, 1>(A, rows, ntiles, st);
+            if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 1>(A, rows, ntiles, st);
+            return launch_fgp2_t<MODE, 2, 16, 1>(A, rows, ntiles, st);
+        }
+        if (cfgv == 1) return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
+        if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
+        return launch_fgp2_t<MODE, 2, 16, 0>(A, rows, ntiles, st);
+    }
     FgpCfg c;
     if (int rc = fgp_config(rows, cols, A.nfgp, &c)) return rc;
-    if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
     if (c.FR == 8 && c.NT == 1024) return launch_fgp_t<MODE, 8, 1024>(A, c, ntiles, st);
     if (c.FR == 8) return launch_fgp_t<MODE, 8, 512>(A, c, ntiles, st);
     return launch_fgp_t<MODE, 16, 256>(A, c, ntiles, st);
@@ -320,8 +379,8 @@ int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
 
 // the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
 // one ROI group (tiles [t0, t0 + cnt)) through all n iterations on stream st
-int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st,
-                     cudaStream_t fst = nullptr, cudaEvent_t pev = nullptr, cudaEvent_t fev = nullptr) {
+int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp,
+                     cudaStream_t st, cudaStream_t fst = nullptr, cudaEvent_t pev = nullptr, cudaEvent_t fev = nullptr) {
     Tiles t = p.roi_tiles();
     t.tile += t0; t.d0 += (size_t)t0 * p.na; t.tauc += (size_t)t0 * p.na; t.ntiles = cnt;
     const long long yts = p.ytile();
@@ -333,25 +392,38 @@ int group_iterations(lt_plan& p, int t0, int cnt, int mode, float lo, float hi, 
     float* xprev = p.P<float>(p.off.xprev) + t0 * p.ptile();
     const long long ns = (long long)p.na * p.nd;
     const bool disc = (p.flags & LT_DISC_ON) != 0;
+    // x_s^k = M_{L'} W^T b_k for every ROI of the group comes from one global
+    // backprojection over the image blocks the group's extended ROIs cover
+    // (the extended ROIs overlap, so this is ~4x less work than per ROI)
+    float* xsg = p.P<float>(p.off.xsg[gl == 2 ? 1 : 0]);
+    const int* blist = p.P<int>(p.off.xsblk[gl]);
+    const int nbl = (int)p.xsblk[gl].size();
     double tk = 1.0;
     for (int k = 0; k < p.n_iter; ++k) {
         const float* bk = p.P<float>(p.off.conv) + (long long)k * ns;
+        {   // (independent of y: overlaps the previous FGP of this group)
+            BpEpi ex = epi0();
+            ex.blist = blist; ex.out = xsg; ex.out_pitch = p.n;
+            const SinoView vb = view_full(bk, p.nd);
+            if (int rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(p, p.glob_tiles(), vb, vb, ex, st, nbl)) return rc;
+        }
+        if (fst && k > 0) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));    // previous FGP of this group
         BpEpi e = epi0();
+        e.xsg = xsg; e.xsg_pitch = p.n;
         e.y = y; e.yT = yT; e.y_tstride = yts;
         e.v = v; e.xs = xs; e.p_tstride = p.ptile();
         e.discc = p.P<float>(p.off.discc32); e.use_disc = disc;
         e.alpha = (float)p.alpha; e.lo = lo; e.hi = hi; e.last = (k == p.n_iter - 1);
-        const SinoView vb = view_full(bk, p.nd);
-        if (fst && k > 0) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));    // previous FGP of this group
         if (k == 0) {
-            // y^0 = 0: W_{L'} y^0 = 0, single-sinogram gather
-            if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vb, vb, e, st)) return rc; }
-            else { if (int rc = launch_bp_t<1, BP_TV>(p, t, vb, vb, e, st)) return rc; }
+            // y^0 = 0: W_{L'} y^0 = 0, no gather
+            const SinoView v0 = view_full(bk, p.nd);
+            if (mode == 0) { if (int rc = launch_bp_t<0, BP_BOX>(p, t, v0, v0, e, st)) return rc; }
+            else { if (int rc = launch_bp_t<0, BP_TV>(p, t, v0, v0, e, st)) return rc; }
         } else {
             if (int rc = launch_fp_roi(p, t, y, yT, yts, s, (long long)p.na * p.Wwin, st)) return rc;
             const SinoView vs = view_win(s, p.Wwin, p.na);
-            if (mode == 0) { if (int rc = launch_bp_t<2, BP_BOX>(p, t, vb, vs, e, st)) return rc; }
-            else { if (int rc = launch_bp_t<2, BP_TV>(p, t, vb, vs, e, st)) return rc; }
+            if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vs, vs, e, st)) return rc; }
+            else { if (int rc = launch_bp_t<1, BP_TV>(p, t, vs, vs, e, st)) return rc; }
         }
         if (mode == 1) {
             const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
@@ -387,7 +459,7 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
     if (mode == 1) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
     const int ng = (p.nsplit > 1 && p.R >= 2 && p.gst[0]) ? 2 : 1;
     if (ng == 1) {
-        if (int rc = group_iterations(p, 0, p.R, mode, lo, hi, lam, nfgp, st)) return rc;
+        if (int rc = group_iterations(p, 0, 0, p.R, mode, lo, hi, lam, nfgp, st)) return rc;
     } else {
         // fork: both group streams wait for the work already queued on st
         LT_CUDA(cudaEventRecord(p.gev[2], st));
@@ -397,7 +469,7 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
             const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
             const bool prio = p.fst[g] && mode == 1;
             if (prio) LT_CUDA(cudaStreamWaitEvent(p.fst[g], p.gev[2], 0));
-            if (int rc = group_iterations(p, t0, cnt, mode, lo, hi, lam, nfgp, p.gst[g], prio ? p.fst[g] : nullptr,
+            if (int rc = group_iterations(p, 1 + g, t0, cnt, mode, lo, hi, lam, nfgp, p.gst[g], prio ? p.fst[g] : nullptr,
                                           p.pev[g], p.fev[g])) return rc;
             LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
         }
@@ -600,6 +672,23 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         }
     }
     p->ngroups = (int)p->fpgroups.size() / FP_GA;
+    // x_s block lists: blocks meeting any valid extended rect
+    {
+        const int nbk = (n + 31) / 32;
+        const int half = (p->R + 1) / 2;
+        const int ranges[3][2] = {{0, p->R}, {0, half}, {half, p->R}};
+        for (int l = 0; l < 3; ++l) {
+            std::vector<char> need((size_t)nbk * nbk, 0);
+            for (int q = ranges[l][0]; q < ranges[l][1]; ++q) {
+                const TileT& t = p->tiles[q];
+                const int r0 = t.row0 + t.vr0, r1 = t.row0 + t.vr1, c0 = t.col0 + t.vc0, c1 = t.col0 + t.vc1;
+                for (int by = r0 / 32; by <= (r1 - 1) / 32; ++by)
+                    for (int bx = c0 / 32; bx <= (c1 - 1) / 32; ++bx) need[(size_t)by * nbk + bx] = 1;
+            }
+            for (int b = 0; b < nbk * nbk; ++b)
+                if (need[b]) p->xsblk[l].push_back(b);
+        }
+    }
     // global tile: the whole grid, window = the full detector
     {
         TileT t;
@@ -632,6 +721,8 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.gqo = take(nn * fs); f.gz = take(nn * fs); f.gxprev = take(nn * fs);
     f.y = take(R * ytile * fs); f.yT = take(R * ytile * fs); f.s = take(R * n_angles * p->Wwin * fs);
     f.v = take(R * ptile * fs); f.xs = take(R * ptile * fs); f.xprev = take(R * ptile * fs);
+    for (int l = 0; l < 3; ++l) f.xsblk[l] = take(std::max<size_t>(p->xsblk[l].size(), 1) * 4);
+    for (int l = 0; l < 2; ++l) f.xsg[l] = take((size_t)n * n * fs);
     f.tt = take(ytile * fs); f.ttT = take(ytile * fs); f.tw = take((size_t)n_angles * p->Wwin * fs);
     f.st_off = take(((size_t)nb * nb + 1) * 4); f.st_lst = take((size_t)p->stitch_cap * 4);
     f.st_r0 = take((size_t)n_roi * std::max(1, world) * 4 + 4); f.st_c0 = take((size_t)n_roi * std::max(1, world) * 4 + 4);
@@ -666,6 +757,8 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(up(p->off.gd0, p->gd0.data(), na * 4));
     LT_CUDA(up(p->off.gtauc, p->gtauc.data(), na * 8));
     LT_CUDA(up(p->off.fpgroups, p->fpgroups.data(), p->fpgroups.size() * 4));
+    for (int l = 0; l < 3; ++l)
+        if (!p->xsblk[l].empty()) LT_CUDA(up(p->off.xsblk[l], p->xsblk[l].data(), p->xsblk[l].size() * 4));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.discc32, 0, 4, st));
     LT_CUDA(cudaStreamSynchronize(st));

@@ -1,9 +1,11 @@
-"""FGP time vs cluster size: same pixel count, tiles of H x 256 (H = 16..256)."""
-import sys
+"""FGP time vs cluster size: same pixel count (256 x 256^2), tiles of H x 256
+(H = 32..256), so the effect of the cross-CTA (DSMEM) chain is isolated."""
+import os, sys
 sys.path.insert(0, '.')
 import torch
 import paper_1604_02292_b200 as lt
-for H in (16, 32, 64, 128, 256):
+tag = f"V={os.environ.get('LT_FGP_V', '2')} cfg={os.environ.get('LT_FGP2_CFG', '-')} sync={os.environ.get('LT_FGP2_SYNC', '0')}"
+for H in (32, 64, 128, 256):
     x = torch.rand(256 * 256 // H, H, 256, device='cuda')
     for _ in range(2): lt.fgp_batch(x, 0.05, 100)
     torch.cuda.synchronize()
@@ -11,4 +13,4 @@ for H in (16, 32, 64, 128, 256):
     e0.record()
     for _ in range(3): lt.fgp_batch(x, 0.05, 100)
     e1.record(); torch.cuda.synchronize()
-    print(f"H={H:4d} tiles={x.shape[0]:5d}: {e0.elapsed_time(e1)/3:.3f} ms")
+    print(f"{tag} H={H:4d} tiles={x.shape[0]:5d}: {e0.elapsed_time(e1)/3:.3f} ms")
