@@ -305,16 +305,181 @@ __global__ void __launch_bounds__(256) k_fp_roi(Geo g, Tiles t, FpArgs f, const 
 }
 
 // ---------------------------------------------------------------------------
-// Backprojection M_{L'} W^T (pixel driven, exact transpose of k_fp) with the
-// fused solver epilogues.  CTA = (tile r, 32x32 sub-tile); thread = 4 pixels
-// of one column.  Per chunk of CA angles the CTA stages, for each angle, the
-// SW-bin sub-window of each source sinogram that its sub-tile can reach
-// (interleaved float2 for the two-sinogram gather of the local iteration),
-// then every pixel gathers its 2 hat taps per angle from shared memory.
-// Anchors: tau at the sub-tile centre in fp64, fp32 offsets <= 15.5 px.
+// k_fp_roi2: the same W_{L'} as k_fp_roi, restructured for the sm_100 FP32
+// datapath and the shared-memory crossbar:
+//  * the band is staged as interpolation pairs (S[m], D[m]) = (v[m] + v[m+1],
+//    v[m+1] - v[m]) (one 64-bit entry per pixel, built once per band and shared
+//    by the CTA's 8 angles), so a Joseph step is one LDS.64 and two FP ops:
+//    2 * lerp(v, pos) = S[m] + g D[m], g = 2 (pos - m) - 1;
+//  * the position / index / fraction arithmetic runs on line pairs (FFMA2, FADD2);
+//  * per band each warp visits only the rays that cross the band's valid
+//    pixels (the range is computed in fp64), not the whole window.
+// Staging: the next band's raw lines are prefetched into registers while the
+// current band is marched, then transformed into the single (S, D) buffer.
 // ---------------------------------------------------------------------------
-constexpr int BP_CA = 64;   // angles per staged chunk
-constexpr int BP_SW = 52;   // bins per angle per sub-tile (>= 32*sqrt2 + 4)
+constexpr int FP2_BL = 16;       // lines per band
+constexpr int FP2_P = 272;       // (S, D) entries per staged line (>= T + PADL + PADR)
+constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16;  // float4 chunks per thread per band (16 threads per line)
+
+template <bool CLAMP>
+__device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
+    const unsigned rowbase = __shfl_sync(0xffffffffu, rowbase_, threadIdx.x & 31);
+    float acc = 0.f;
+    #pragma unroll
+    for (int i = 0; i < FP2_BL; i += 2) {
+        float2 tt = make_float2(fmaf((float)i, Bf, f0), fmaf((float)(i + 1), Bf, f0));   // immediates
+        if (CLAMP) {
+            tt.x = fminf(fmaxf(tt.x, lo), hi);
+            tt.y = fminf(fmaxf(tt.y, lo), hi);
+        }
+        const float2 rm = __fadd2_rn(tt, make_float2(MAGICF, MAGICF));           // round(tt) in the low bits
+        const float2 k2 = __ffma2_rn(rm, make_float2(-2.f, -2.f), make_float2(2.f * MAGICF, 2.f * MAGICF));   // -2 round(tt)
+        const float2 g = __ffma2_rn(tt, make_float2(2.f, 2.f), k2);             // 2 (tt - round(tt)) in [-1, 1]
+        unsigned a0, a1;
+        asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(a0) : "r"(__float_as_int(rm.x)), "r"(rowbase));
+        asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(a1) : "r"(__float_as_int(rm.y)), "r"(rowbase));
+        float s0, d0, s1, d1;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s0), "=f"(d0) : "r"(a0 + (unsigned)(i * FP2_P * 8)));
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s1), "=f"(d1) : "r"(a1 + (unsigned)((i + 1) * FP2_P * 8)));
+        acc = fmaf(g.x, d0, acc + s0);
+        acc = fmaf(g.y, d1, acc + s1);
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, const int* __restrict__ groups) {
+    extern __shared__ float4 smf4[];
+    float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][FP2_P] (S, D), entry 0 = pixel -PADL
+    float* sacc = reinterpret_cast<float*>(sd + FP2_BL * FP2_P);  // [FP_GA][32 * FP_U] per-ray accumulators
+    const int r = blockIdx.y, grp = blockIdx.x;
+    const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a = groups[grp * FP_GA + warp];                     // this warp's angle (-1: idle warp)
+    const int a0 = groups[grp * FP_GA];
+    const int col = g.ang[a0].col;
+    const TileT ti = t.tile[r];
+    const int lv0 = col ? ti.vc0 : ti.vr0, lv1 = col ? ti.vc1 : ti.vr1;
+    const int pv0 = col ? ti.vr0 : ti.vc0, pv1 = col ? ti.vr1 : ti.vc1;
+    const double Lc = 0.5 * (T - 1);
+    const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
+    double A = 0.0, B = 0.0, tauc = 0.0;
+    int d0 = 0;
+    if (a >= 0) {
+        A = g.A64[a]; B = g.B64[a];
+        tauc = t.tauc[r * na + a];
+        d0 = __ldg(t.d0 + r * na + a);
+    }
+    const float Bf = (float)B;
+    float* acc = sacc + warp * (32 * FP_U);
+    for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += 256) sacc[e] = 0.f;
+    // rays with a detector bin: w in [wv0, wv1)
+    const int wv0 = max(0, -d0), wv1 = min(Wwin, g.nd - d0);
+
+    // staging map (no division): thread = (line tid / 16, chunks c4 = tid % 16 + 16 u)
+    const int q4 = TP / 4;                        // float4 chunks per raw line
+    const int sline = threadIdx.x >> 4, sc0 = threadIdx.x & 15;
+    float4 raw[FP2_CPT];
+    float nxt[FP2_CPT];
+    auto fetch = [&](int l0) {                    // raw lines l0.. of the band into registers
+        const bool lok = l0 + sline < T;
+        const float* rp0 = src + (long long)(l0 + sline) * TP;
+        #pragma unroll
+        for (int u = 0; u < FP2_CPT; ++u) {
+            const int c4 = sc0 + 16 * u;
+            raw[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            nxt[u] = 0.f;
+            if (lok && c4 < q4) {
+                raw[u] = __ldg(reinterpret_cast<const float4*>(rp0 + c4 * 4));
+                if (c4 + 1 < q4) nxt[u] = __ldg(rp0 + c4 * 4 + 4);
+            }
+        }
+    };
+    auto transform = [&]() {                      // registers -> (S, D) buffer
+        #pragma unroll
+        for (int u = 0; u < FP2_CPT; ++u) {
+            const int c4 = sc0 + 16 * u;
+            if (c4 < q4) {
+                const float4 v = raw[u];
+                float4* dst = reinterpret_cast<float4*>(sd + sline * FP2_P + c4 * 4);
+                dst[0] = make_float4(v.x + v.y, v.y - v.x, v.y + v.z, v.z - v.y);
+                dst[1] = make_float4(v.z + v.w, v.w - v.z, v.w + nxt[u], nxt[u] - v.w);
+            }
+        }
+    };
+    const int lbeg = (lv0 / FP2_BL) * FP2_BL;
+    if (lbeg < lv1) { fetch(lbeg); transform(); }
+    __syncthreads();
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd + PADL);     // entry of pixel 0
+    for (int l0 = lbeg; l0 < lv1; l0 += FP2_BL) {
+        const bool more = l0 + FP2_BL < lv1;
+        if (more) fetch(l0 + FP2_BL);
+        if (a >= 0) {
+            // rays meeting the valid pixels (pv0 - 1, pv1) on some line of the band
+            const double P0 = Lc - tauc * A + ((double)l0 - Lc) * B;           // p(w, l0) = P0 + w A
+            const double P1 = P0 + (double)(FP2_BL - 1) * B;                   // p(w, l0 + 15) = P1 + w A
+            const double ia = 1.0 / A;
+            const double e1 = (pv0 - 1.0 - P0) * ia, e2 = (pv1 - P0) * ia;
+            const double e3 = (pv0 - 1.0 - P1) * ia, e4 = (pv1 - P1) * ia;
+            const int wlo = max(wv0, (int)floor(fmin(fmin(e1, e2), fmin(e3, e4))) - 1);
+            const int whi = min(wv1, (int)ceil(fmax(fmax(e1, e2), fmax(e3, e4))) + 2);
+            const float Af = (float)A;
+            const float Bl = (float)((FP2_BL - 1) * B);
+            for (int wb = wlo; wb < whi; wb += 32) {
+                const int w = wb + lane;
+                const bool ray = w < whi;
+                // position (pixel index) on line l0: fp64 anchor at the group's
+                // middle ray, fp32 offset |(lane - 16) A| <= 23 px
+                const double pc = P0 + (double)(wb + 16) * A;
+                const double fbc = floor(pc);
+                const float pos = fmaf((float)(lane - 16), Af, (float)(pc - fbc));
+                const float fl = floorf(pos);
+                const int ib = ray ? (int)fbc + (int)fl : 0;
+                const float f0 = ray ? (pos - fl) - 0.5f : -0.5f;
+                const float Bu = ray ? Bf : 0.f;
+                const float pa = (float)ib + f0 + 0.5f, pe = pa + Bl;
+                const bool safe = !ray || (fminf(pa, pe) >= -3.f && fmaxf(pa, pe) <= (float)T + 1.5f);
+                const unsigned rowbase = sbase + 8u * (unsigned)(ib - MAGICI);
+                float v;
+                if (__all_sync(0xffffffffu, safe)) {
+                    v = fp2_band_ray<false>(rowbase, f0, Bu, 0.f, 0.f);
+                } else {
+                    const float lo = (float)(-3 - ib) - 0.5f, hi = (float)(T + 2 - ib) - 0.5f;
+                    v = fp2_band_ray<true>(rowbase, f0, Bu, lo, hi);
+                }
+                if (ray) acc[w] += v;
+            }
+        }
+        __syncthreads();
+        if (more) transform();
+        __syncthreads();
+    }
+    if (a >= 0) {
+        const float sc = 0.5f * g.ang[a].invc;        // (S + g D) = 2 lerp
+        for (int w = lane; w < Wwin; w += 32) {
+            const int d = d0 + w;
+            f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = (d >= 0 && d < g.nd) ? acc[w] * sc : 0.f;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Backprojection M_{L'} W^T (pixel driven, exact transpose of k_fp) with the
+// fused solver epilogues.  CTA = (tile r, 64x64 sub-tile); thread = 2 x 8
+// pixels (columns lane, lane + 32; 8 consecutive rows).  Per chunk of CA angles the CTA stages, for each angle, the
+// SW-bin sub-window of the source sinogram that its sub-tile can reach, as
+// tap pairs (v[m], v[m+1]) / c (one conflict-free LDS.64 per pixel-angle: a
+// warp's 32 pixels of one row reach at most 33 consecutive bins).  The window
+// is staged one warp per angle row (coalesced loads, pairs via shuffles).  The hat
+// weights (V2) become hat(u / c) = sat(1 - |u| / c), computed on the
+// fp32 pair datapath for two pixels at a time.
+// Anchors: tau at the sub-tile centre in fp64, fp32 positions relative to the
+// window centre (|.| <= 48 bins).
+// NS = 0: no gather (y = 0 at k = 1), NS = 1: one sinogram.
+// ---------------------------------------------------------------------------
+constexpr int BP_CA = 32;   // angles per staged chunk
+constexpr int BP_SUB = 64;  // sub-tile side (pixels)
+constexpr int BP_PR = 8;    // rows per thread (x 2 columns, 32 apart)
+constexpr int BP_SW = 96;   // bins per angle per sub-tile (>= 63*sqrt2 + 4), a multiple of 32
 
 enum BpMode {
     BP_PLAIN_TILE = 0,   // out plain [tile][T][T]  (stage-wise parity, lt_backproject)
@@ -328,7 +493,7 @@ enum BpMode {
 
 struct BpEpi {
     const int* blist;                                      // sub-tile list (nullable: all sub-tiles of the tile)
-    const float* xsg; int xsg_pitch;                       // global x_s^k = W^T b_k image (BOX/TV with NS <= 1)
+    const float* xsg; int xsg_pitch;                       // global x_s^k = W^T b_k image (BOX/TV)
     float* out; long long out_tstride; int out_pitch;     // plain outputs
     float* y; float* yT; long long y_tstride;              // padded tile images (state)
     float* v; float* xs; long long p_tstride;              // plain [T][T] (TV)
@@ -338,76 +503,152 @@ struct BpEpi {
 
 template <int NS, int MODE>
 __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoView s2, BpEpi e) {
-    __shared__ float2 sw[BP_CA][BP_SW];
-    __shared__ float4 sa[BP_CA];
+    static_assert(NS == 0 || NS == 1, "one gathered sinogram at most");
+    __shared__ float2 sw[BP_CA][BP_SW];          // (v[m], v[m+1]) / c_a, m relative to the window centre
+    __shared__ float4 sa[BP_CA];                 // (cos, sin, K' = 1 - 1/(2c), 1/c)
     __shared__ float sanch[BP_CA];
-    __shared__ int ssub0[BP_CA];
 
     const int r = blockIdx.y;
     const int T = t.T, na = g.na;
-    const int nsx = (T + 31) >> 5;
+    const int nsx = (T + BP_SUB - 1) / BP_SUB;
     const int sub = e.blist ? __ldg(e.blist + blockIdx.x) : (int)blockIdx.x;
     const int sty = sub / nsx, stx = sub - sty * nsx;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int pj = stx * 32 + tx;
-    const int pi0 = sty * 32 + ty * 4;
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int pj0 = stx * BP_SUB + lane;                  // columns pj0, pj0 + 32
+    const int pi0 = sty * BP_SUB + wq * BP_PR;            // rows pi0 .. pi0 + BP_PR - 1
     const double Lc = 0.5 * (T - 1);
-    const double dxc = stx * 32 + 15.5 - Lc, dyc = sty * 32 + 15.5 - Lc;
-    const float dx = (float)tx - 15.5f, dy0 = (float)(ty * 4) - 15.5f;
+    const double hs = 0.5 * (BP_SUB - 1);
+    const double dxc = stx * BP_SUB + hs - Lc, dyc = sty * BP_SUB + hs - Lc;
+    const float dx = (float)lane - (float)hs, dy0 = (float)(wq * BP_PR) - (float)hs;
 
-    float g1[4] = {0.f, 0.f, 0.f, 0.f}, g2[4] = {0.f, 0.f, 0.f, 0.f};
+    float2 acc[2][BP_PR];                         // (left-tap, right-tap) partial sums per pixel
+    #pragma unroll
+    for (int h = 0; h < 2; ++h)
+        #pragma unroll
+        for (int p = 0; p < BP_PR; ++p) acc[h][p] = make_float2(0.f, 0.f);
     for (int a0 = 0; a0 < (NS > 0 ? na : 0); a0 += BP_CA) {
         const int ca = min(BP_CA, na - a0);
         __syncthreads();
-        for (int q = threadIdx.x; q < ca; q += blockDim.x) {
+        // one warp per angle row: anchors, then the BP_SW + 1 bins of the window as pairs
+        for (int q = wq; q < ca; q += 8) {
             const int a = a0 + q;
             const double tc = t.tauc[r * na + a] + dxc * g.cs64[a] - dyc * g.sn64[a];
-            const int sub0 = (int)floor(tc) - BP_SW / 2;
-            sanch[q] = (float)(tc - (double)sub0) - 0.5f;
-            ssub0[q] = sub0;
+            const int sub0 = (int)floor(tc) - BP_SW / 2;          // window bins sub0 .. sub0 + BP_SW
             const AngF an = g.ang[a];
-            sa[q] = make_float4(an.cs, an.sn, an.K, an.ic2);
+            if (lane == 0) {
+                sanch[q] = (float)(tc - (double)(sub0 + BP_SW / 2)) - 0.5f;
+                sa[q] = make_float4(an.cs, an.sn, 1.f - 0.5f * an.invc, an.invc);
+            }
+            const int off = (s1.use_d0 ? __ldg(t.d0 + r * na + a) : 0) + sub0;
+            const float* rowp = s1.base + (long long)r * s1.tile_stride + (long long)a * s1.row_stride;
+            float v[BP_SW / 32 + 1];
+            #pragma unroll
+            for (int u = 0; u <= BP_SW / 32; ++u) {
+                const int idx = off + lane + 32 * u;
+                v[u] = (idx >= 0 && idx < s1.len && lane + 32 * u <= BP_SW) ? __ldg(rowp + idx) * an.invc : 0.f;
+            }
+            #pragma unroll
+            for (int u = 0; u < BP_SW / 32; ++u) {
+                float nx = __shfl_down_sync(0xffffffffu, v[u], 1);
+                const float nx0 = __shfl_sync(0xffffffffu, v[u + 1], 0);
+                if (lane == 31) nx = nx0;
+                sw[q][lane + 32 * u] = make_float2(v[u], nx);
+            }
         }
         __syncthreads();
-        for (int el = threadIdx.x; el < ca * BP_SW; el += blockDim.x) {
-            const int q = el / BP_SW, w = el - q * BP_SW;
-            const int a = a0 + q, wb = ssub0[q] + w;
-            const float v1 = sv_fetch(s1, t.d0, na, r, a, wb);
-            const float v2 = NS == 2 ? sv_fetch(s2, t.d0, na, r, a, wb) : 0.f;
-            sw[q][w] = make_float2(v1, v2);
-        }
-        __syncthreads();
-        const unsigned swbase = opaque_u32((unsigned)__cvta_generic_to_shared(&sw[0][0]) - 8u * (unsigned)MAGICI);
-        #pragma unroll 2
+        // entry of bin m (relative to the window centre) at swbase + 8 (m + MAGIC bits)
+        const unsigned swbase = opaque_u32((unsigned)__cvta_generic_to_shared(&sw[0][BP_SW / 2]) - 8u * (unsigned)MAGICI);
+        #pragma unroll 1
         for (int q = 0; q < ca; ++q) {
             const float4 A4 = sa[q];
-            const float t0 = fmaf(dx, A4.x, fmaf(-dy0, A4.y, sanch[q]));
+            const float t00 = fmaf(dx, A4.x, fmaf(-dy0, A4.y, sanch[q]));   // column pj0, row pi0
             const unsigned rowb = opaque_u32(swbase + (unsigned)(q * BP_SW * 8));
             #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float tt = fmaf(-(float)p, A4.y, t0);
-                const float rm = tt + MAGICF;
-                const float gg = tt - (rm - MAGICF);
-                unsigned addr;
-                asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(addr) : "r"(__float_as_int(rm)), "r"(rowb));
-                const float w0 = fmaxf(0.f, fmaf(-gg, A4.w, A4.z));
-                const float w1 = fmaxf(0.f, fmaf(gg, A4.w, A4.z));
-                float b0x, b0y, b1x, b1y;
-                asm volatile("ld.shared.v2.f32 {%0, %1}, [%4];\n\tld.shared.v2.f32 {%2, %3}, [%4+8];"
-                             : "=f"(b0x), "=f"(b0y), "=f"(b1x), "=f"(b1y) : "r"(addr));
-                g1[p] = fmaf(w0, b0x, fmaf(w1, b1x, g1[p]));
-                if (NS == 2) g2[p] = fmaf(w0, b0y, fmaf(w1, b1y, g2[p]));
+            for (int h = 0; h < 2; ++h) {
+                const float t0 = h ? fmaf(32.f, A4.x, t00) : t00;
+                #pragma unroll
+                for (int p = 0; p < BP_PR; p += 2) {
+                    // positions of pixels p, p+1 (one row apart): tt = t0 - p sin
+                    const float2 tt = __ffma2_rn(make_float2(-(float)p, -(float)(p + 1)), make_float2(A4.y, A4.y),
+                                                 make_float2(t0, t0));
+                    const float2 rm = __fadd2_rn(tt, make_float2(MAGICF, MAGICF));
+                    const float2 kk = __fadd2_rn(rm, make_float2(-MAGICF, -MAGICF));   // round(tt), exact
+                    const float2 gg = __fadd2_rn(tt, make_float2(-kk.x, -kk.y));
+                    unsigned ad0, ad1;
+                    asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ad0) : "r"(__float_as_int(rm.x)), "r"(rowb));
+                    asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ad1) : "r"(__float_as_int(rm.y)), "r"(rowb));
+                    float2 b0, b1;
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b0.x), "=f"(b0.y) : "r"(ad0));
+                    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b1.x), "=f"(b1.y) : "r"(ad1));
+                    // hat weights of the left / right bin: sat(K' -/+ gg / c)
+                    const float2 w0 = make_float2(__saturatef(fmaf(-gg.x, A4.w, A4.z)), __saturatef(fmaf(gg.x, A4.w, A4.z)));
+                    const float2 w1 = make_float2(__saturatef(fmaf(-gg.y, A4.w, A4.z)), __saturatef(fmaf(gg.y, A4.w, A4.z)));
+                    acc[h][p] = __ffma2_rn(w0, b0, acc[h][p]);
+                    acc[h][p + 1] = __ffma2_rn(w1, b1, acc[h][p + 1]);
+                }
             }
         }
     }
-
-    // ---- epilogue ------------------------------------------------------------
     const TileT ti = t.tile[r];
     const int n = g.n;
-    float discc = 0.f;
-    if ((MODE == BP_BOX || MODE == BP_TV) && e.use_disc) discc = *e.discc;
     #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int h = 0; h < 2; ++h) {
+    const int pj = pj0 + 32 * h;
+    float g1[BP_PR];
+    #pragma unroll
+    for (int p = 0; p < BP_PR; ++p) g1[p] = acc[h][p].x + acc[h][p].y;
+
+    // ---- epilogue ------------------------------------------------------------
+    if (MODE == BP_BOX || MODE == BP_TV) {
+        const float discc = e.use_disc ? *e.discc : 0.f;
+        // loads of all four pixels first, then the stores
+        float yv[BP_PR], xsv[BP_PR];
+        bool valid[BP_PR];
+        #pragma unroll
+        for (int p = 0; p < BP_PR; ++p) {
+            const int i = pi0 + p, j = pj;
+            valid[p] = i < T && j < T && i >= ti.vr0 && i < ti.vr1 && j >= ti.vc0 && j < ti.vc1;
+            yv[p] = 0.f; xsv[p] = 0.f;
+            if (valid[p]) {
+                float dval = 0.f;
+                if (e.use_disc) {
+                    const int gi = ti.row0 + i, gj = ti.col0 + j;
+                    const int u = 2 * gj - n + 1, v = 2 * gi - n + 1;   // 2x, 2y of the pixel centre
+                    dval = (u * u + v * v <= n * n) ? discc : 0.f;      // D: centred disc, diameter N
+                }
+                // x_s^k = M_{L'} W^T b_k + c D: the global backprojection, read at this pixel
+                xsv[p] = __ldg(e.xsg + (long long)(ti.row0 + i) * e.xsg_pitch + (ti.col0 + j)) + dval;
+                yv[p] = e.y[(long long)r * e.y_tstride + (long long)i * t.TP + PADL + j];
+            }
+        }
+        #pragma unroll
+        for (int p = 0; p < BP_PR; ++p) {
+            const int i = pi0 + p, j = pj;
+            if (i >= T || j >= T) continue;
+            float val = 0.f;
+            if (valid[p]) {
+                const float wts = NS >= 1 ? g1[p] : 0.f;                // (W_{L'}^T W_{L'} y)_j
+                const float S = xsv[p] + yv[p] - e.alpha * wts;         // S(x^{k-1}) split
+                if (MODE == BP_BOX) {
+                    const float x = fminf(fmaxf(S, e.lo), e.hi);         // eq. sirtbox
+                    val = e.last ? x : x - xsv[p];                       // y^k = clamp(S) - x_s^k
+                } else {
+                    val = S;
+                }
+            }
+            if (MODE == BP_BOX) {
+                e.y[(long long)r * e.y_tstride + (long long)i * t.TP + PADL + j] = val;
+                e.yT[(long long)r * e.y_tstride + (long long)j * t.TP + PADL + i] = val;
+            } else {
+                const long long pl = (long long)r * e.p_tstride + (long long)i * T + j;
+                e.v[pl] = val;
+                e.xs[pl] = xsv[p];
+            }
+        }
+        continue;
+    }
+    #pragma unroll
+    for (int p = 0; p < BP_PR; ++p) {
         const int i = pi0 + p, j = pj;
         if (i >= T || j >= T) continue;
         const bool valid = i >= ti.vr0 && i < ti.vr1 && j >= ti.vc0 && j < ti.vc1;
@@ -417,41 +658,6 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
             e.out[(long long)r * e.out_tstride + (long long)i * T + j] = valid ? g1[p] : 0.f;
         } else if (MODE == BP_PLAIN_GLOBAL) {
             if (valid) e.out[(long long)(ti.row0 + i) * e.out_pitch + (ti.col0 + j)] = g1[p];
-        } else if (MODE == BP_BOX || MODE == BP_TV) {
-            float xs = 0.f, yv = 0.f, val = 0.f;
-            if (valid) {
-                float dval = 0.f;
-                if (e.use_disc) {
-                    const int gi = ti.row0 + i, gj = ti.col0 + j;
-                    const int u = 2 * gj - n + 1, v = 2 * gi - n + 1;   // 2x, 2y of the pixel centre
-                    dval = (u * u + v * v <= n * n) ? discc : 0.f;      // D: centred disc, diameter N
-                }
-                float wts;                                               // (W_{L'}^T W_{L'} y)_j
-                if (e.xsg) {
-                    // x_s^k = M_{L'} W^T b_k: the global backprojection, read at this pixel
-                    xs = __ldg(e.xsg + (long long)(ti.row0 + i) * e.xsg_pitch + (ti.col0 + j)) + dval;
-                    wts = NS >= 1 ? g1[p] : 0.f;
-                } else {
-                    xs = g1[p] + dval;                                   // x_s^k = FBP_L(p_c, u_k) + c D
-                    wts = NS == 2 ? g2[p] : 0.f;
-                }
-                yv = e.y[pp];
-                const float S = xs + yv - e.alpha * wts;                 // S(x^{k-1}) split
-                if (MODE == BP_BOX) {
-                    const float x = fminf(fmaxf(S, e.lo), e.hi);         // eq. sirtbox
-                    val = e.last ? x : x - xs;                           // y^k = clamp(S) - x_s^k
-                } else {
-                    val = S;
-                }
-            }
-            if (MODE == BP_BOX) {
-                e.y[pp] = val;
-                e.yT[pt] = val;
-            } else {
-                const long long pl = (long long)r * e.p_tstride + (long long)i * T + j;
-                e.v[pl] = val;
-                e.xs[pl] = xs;
-            }
         } else if (MODE == BP_ALG1) {
             const float c = valid ? e.y[pp] - e.alpha * g1[p] : 0.f;
             e.y[pp] = c;
@@ -463,6 +669,7 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
         } else if (MODE == BP_GTV) {
             if (valid) e.out[(long long)i * T + j] = e.y[pp] + e.alpha * g1[p];
         }
+    }
     }
 }
 
@@ -1071,22 +1278,36 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fgp2(FgpArgs A) {
             xv[2 * c2 + 1] = b[k][c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
         }
         if (i < Hv) {
-            #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int j = x0 + c;
-                if (j >= Wv) continue;
-                const float x = xv[c];
-                if (MODE == 0) {
-                    A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + j] = x;
-                } else {
-                    const int ti_ = vr0 + i, tj = vc0 + j;
-                    const long long pl = (long long)tile * A.p_tstride + (long long)ti_ * A.T + tj;
-                    const float xp = A.xprev[pl];
-                    const float rr = x + A.beta_o * (x - xp);             // FISTA extrapolation (A12)
-                    const float yv = rr - A.xs[pl];                         // x_L^k = r - x_s^k
-                    A.xprev[pl] = x;
-                    A.y[(long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + tj] = yv;
-                    A.yT[(long long)tile * A.y_tstride + (long long)tj * A.TP + PADL + ti_] = yv;
+            if (MODE == 0) {
+                #pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (x0 + c < Wv) A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + x0 + c] = xv[c];
+            } else {
+                // all loads of the row first (the stores below touch other addresses
+                // of this thread only), so their latencies overlap
+                const int ti_ = vr0 + i;
+                const long long prow = (long long)tile * A.p_tstride + (long long)ti_ * A.T + vc0 + x0;
+                const float* __restrict__ xpp = A.xprev + prow;
+                const float* __restrict__ xsp = A.xs + prow;
+                float xpv[8], xsv[8];
+                #pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const bool ok = x0 + c < Wv;
+                    xpv[c] = ok ? xpp[c] : 0.f;
+                    xsv[c] = ok ? __ldg(xsp + c) : 0.f;
+                }
+                float* __restrict__ yrow = A.y + (long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + vc0 + x0;
+                float* __restrict__ ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + ti_;
+                float* __restrict__ xpw = A.xprev + prow;
+                #pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (x0 + c >= Wv) continue;
+                    const float x = xv[c];
+                    const float rr = x + A.beta_o * (x - xpv[c]);             // FISTA extrapolation (A12)
+                    const float yv = rr - xsv[c];                             // x_L^k = r - x_s^k
+                    xpw[c] = x;
+                    yrow[c] = yv;
+                    ycol[(long long)c * A.TP] = yv;
                 }
             }
         }

@@ -86,7 +86,7 @@ struct lt_plan {
     std::vector<int> d0, gd0;
     std::vector<double> tauc, gtauc;
     std::vector<int> fpgroups;    // [ngroups][FP_GA] angle indices of one orientation, -1 padded
-    // 32x32 image blocks that the global x_s^k backprojection must cover: list 0 for
+    // BP_SUB^2 image blocks that the global x_s^k backprojection must cover: list 0 for
     // all local ROIs, lists 1 and 2 for the two pipelined ROI groups (halves)
     std::vector<int> xsblk[3];
     int ngroups = 0;
@@ -166,9 +166,21 @@ int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, cons
 // direct-read kernel when the staged band would not fit)
 int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
                   float* out, long long out_ts, cudaStream_t st) {
-    const size_t smem = (size_t)2 * FP_BL * FP_P * sizeof(float);
+    static int fpv = -1;
+    if (fpv < 0) { const char* e = getenv("LT_FP_V"); fpv = (e && atoi(e) == 1) ? 1 : 2; }
     if (t.TP > FP_P || t.Wwin > 32 * FP_U)
         return launch_fp(p, 0, t, img, imgT, img_ts, out, out_ts, nullptr, nullptr, st);
+    if (fpv == 2 && t.TP <= FP2_P) {
+        const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)FP_GA * 32 * FP_U * sizeof(float);
+        LT_CUDA(cudaFuncSetAttribute(k_fp_roi2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
+        dim3 grid(p.ngroups, t.ntiles);
+        ScopedTimer tm(TC_FP, st);
+        k_fp_roi2<<<grid, 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
+        LT_LAUNCHED();
+        return LT_OK;
+    }
+    const size_t smem = (size_t)2 * FP_BL * FP_P * sizeof(float);
     LT_CUDA(cudaFuncSetAttribute(k_fp_roi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
     dim3 grid(p.ngroups, t.ntiles);
@@ -181,7 +193,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
 template <int NS, int MODE>
 int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const SinoView& s2, const BpEpi& e,
                 cudaStream_t st, int nblist = 0) {
-    const int nsx = (t.T + 31) / 32;
+    const int nsx = (t.T + BP_SUB - 1) / BP_SUB;
     if (e.blist && nblist == 0) return LT_OK;
     dim3 grid(e.blist ? nblist : nsx * nsx, t.ntiles);
     ScopedTimer tm(TC_BP, st);
@@ -674,7 +686,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     p->ngroups = (int)p->fpgroups.size() / FP_GA;
     // x_s block lists: blocks meeting any valid extended rect
     {
-        const int nbk = (n + 31) / 32;
+        const int nbk = (n + BP_SUB - 1) / BP_SUB;
         const int half = (p->R + 1) / 2;
         const int ranges[3][2] = {{0, p->R}, {0, half}, {half, p->R}};
         for (int l = 0; l < 3; ++l) {
@@ -682,8 +694,8 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
             for (int q = ranges[l][0]; q < ranges[l][1]; ++q) {
                 const TileT& t = p->tiles[q];
                 const int r0 = t.row0 + t.vr0, r1 = t.row0 + t.vr1, c0 = t.col0 + t.vc0, c1 = t.col0 + t.vc1;
-                for (int by = r0 / 32; by <= (r1 - 1) / 32; ++by)
-                    for (int bx = c0 / 32; bx <= (c1 - 1) / 32; ++bx) need[(size_t)by * nbk + bx] = 1;
+                for (int by = r0 / BP_SUB; by <= (r1 - 1) / BP_SUB; ++by)
+                    for (int bx = c0 / BP_SUB; bx <= (c1 - 1) / BP_SUB; ++bx) need[(size_t)by * nbk + bx] = 1;
             }
             for (int b = 0; b < nbk * nbk; ++b)
                 if (need[b]) p->xsblk[l].push_back(b);
