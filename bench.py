@@ -227,7 +227,7 @@ def run_ours(args, cfg):
         e2e_ms = float(t.item())
 
     # global counts
-    upd_local, fgp_local, _ = algorithmic_counts(cfg, rects, n_iter)
+    upd_local, fgp_local, Ptot_local = algorithmic_counts(cfg, rects, n_iter)
     if dist:
         t = torch.tensor([upd_local, fgp_local], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
@@ -249,21 +249,24 @@ def run_ours(args, cfg):
     dom_ms, dom_n = ktimes[dom]
     avg_ms = dom_ms / max(dom_n, 1)
     local_upd_per_step = upd_local
+    nA = cfg.n_angles * Ptot_local          # pixel-angle updates of one A or A^T over all local ROIs
     if dom == "fgp":
         work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / max(dom_n, 1)
-    elif dom in ("fp", "bp"):
-        # each FP launch is one A (N_theta * P updates); each two-sinogram BP counts 2
-        work = JOSEPH_FLOPS_PER_UPDATE * local_upd_per_step * args.steps / max(ktimes["fp"][1] + ktimes["bp"][1], 1)
+    elif dom == "fp":      # one W_{L'} y per iteration 2..n
+        work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / max(dom_n, 1)
+    elif dom == "bp":      # x_s^k = M_{L'} W^T b_k (n) and W_{L'}^T s (n - 1), counted per ROI as in the method
+        work = JOSEPH_FLOPS_PER_UPDATE * nA * (2 * n_iter - 1) * args.steps / max(dom_n, 1)
     else:
         work = 0.0
     achieved = work / (avg_ms / 1e3) / 1e12
-    kname = {"fgp": "k_fgp", "fp": "k_fp_roi", "bp": "k_bp", "conv": "k_conv"}[dom]
+    kname = {"fgp": "k_fgp2", "fp": "k_fp_roi2", "bp": "k_bp_roi", "conv": "k_conv"}[dom]
     traffic, traffic_src = None, None
     try:   # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
             tj = json.load(f)
         if kname in tj:
-            traffic = float(tj[kname]["dram_bytes_per_launch"])
+            # the capture's launches cover all R ROIs; scale to this run's launch size
+            traffic = float(tj[kname]["dram_bytes_per_launch"]) * (plan.R / float(tj[kname].get("rois_per_launch", plan.R)))
             traffic_src = tj[kname]["source"]
     except Exception:
         traffic = None

@@ -1056,11 +1056,16 @@ struct Fgp2Smem {
     static constexpr int hr = rx_z + 2 * FGP2_ROW;             // [2][NW][256] last r row of each warp
     static constexpr int hz = hr + 2 * NW * FGP2_ROW;          // [2][NW][256] first z row of each warp
     static constexpr int hp = hz + 2 * NW * FGP2_ROW;          // [NW][256] last p row (epilogue)
-    static constexpr int total = hp + NW * FGP2_ROW;
+    static constexpr int bsm = hp + NW * FGP2_ROW;             // [NW][FR][256] b (BSM variant)
+    static constexpr int total = bsm;
+    static constexpr int total_bsm = bsm + NW * FR * FGP2_ROW;
 };
 
-template <int MODE, int FR, int NW, int SYNC>
-__global__ void __launch_bounds__(NW * 32, 1) k_fgp2(FgpArgs A) {
+// BSM: b (read once per iteration) lives in shared memory instead of registers,
+// so the kernel fits 128 registers and two CTAs (two tiles) share an SM: one
+// tile's halo latency is hidden behind the other tile's arithmetic.
+template <int MODE, int FR, int NW, int SYNC, bool BSM>
+__global__ void __launch_bounds__(NW * 32, BSM ? 2 : 1) k_fgp2(FgpArgs A) {
     using SM = Fgp2Smem<FR, NW>;
     extern __shared__ __align__(16) float sm[];
     cg::cluster_group cl = cg::this_cluster();
@@ -1100,20 +1105,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fgp2(FgpArgs A) {
     auto wr = [&](int ww, int par) { return wbar0 + 8u * (4 * ww + par); };
     auto wz = [&](int ww, int par) { return wbar0 + 8u * (4 * ww + 2 + par); };
 
-    float2 b[FR][4], r[FR][4], s[FR][4], p[FR][4], q[FR][4], z[FR][4];
+    float2 breg[BSM ? 1 : FR][4], r[FR][4], s[FR][4], p[FR][4], q[FR][4], z[FR][4];
+    float* bs = sm + SM::bsm + (w * FR) * FGP2_ROW;          // this warp's b rows (BSM)
+    auto bget = [&](int k, float2 (&v)[4]) {
+        if constexpr (BSM) {
+            row_ld(bs + k * FGP2_ROW, lane, v);
+        } else {
+            #pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) v[c2] = breg[k][c2];
+        }
+    };
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)vr0 * A.b_pitch + vc0;
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
+        float2 bv[4];
         #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) {
             const int x = x0 + 2 * c2;
             const bool rv = i < Hv;
             const float bx = (rv && x < Wv) ? __ldg(bsrc + (long long)i * A.b_pitch + x) : 0.f;
             const float by = (rv && x + 1 < Wv) ? __ldg(bsrc + (long long)i * A.b_pitch + x + 1) : 0.f;
-            b[k][c2] = make_float2(bx, by);
+            if constexpr (!BSM) breg[k][c2] = make_float2(bx, by); else bv[c2] = make_float2(bx, by);
             r[k][c2] = f2s(0.5f); s[k][c2] = f2s(0.5f); p[k][c2] = f2s(0.5f); q[k][c2] = f2s(0.5f);
         }
+        if constexpr (BSM) row_st(bs + k * FGP2_ROW, lane, bv);
     }
     const float lam = A.lam;
     const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
@@ -1169,10 +1185,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fgp2(FgpArgs A) {
             float sl = __shfl_up_sync(0xffffffffu, s[k][3].y, 1);
             if (lane == 0) sl = 0.5f;
             // z = b - lam2 (r - rup) - lam2 s + lam2 s_left
-            float2 t[4];
+            float2 t[4], bk[4];
+            bget(k, bk);
             #pragma unroll
             for (int c2 = 0; c2 < 4; ++c2) {
-                t[c2] = f2fma(nl2, f2sub(r[k][c2], rup[c2]), b[k][c2]);
+                t[c2] = f2fma(nl2, f2sub(r[k][c2], rup[c2]), bk[c2]);
                 t[c2] = f2fma(nl2, s[k][c2], t[c2]);
             }
             z[k][0].x = fmaf(lam2, sl, t[0].x);
@@ -1270,12 +1287,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_fgp2(FgpArgs A) {
         float ql = __shfl_up_sync(0xffffffffu, q[k][3].y, 1);
         if (lane == 0) ql = 0.5f;
         float xv[8];
+        float2 bk[4];
+        bget(k, bk);
         #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) {
             const float2 pu = k > 0 ? p[k - 1][c2] : pup0[c2];
             const float qlx = c2 > 0 ? q[k][c2 - 1].y : ql;
-            xv[2 * c2] = b[k][c2].x - lam2 * (p[k][c2].x + q[k][c2].x - pu.x - qlx);
-            xv[2 * c2 + 1] = b[k][c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
+            xv[2 * c2] = bk[c2].x - lam2 * (p[k][c2].x + q[k][c2].x - pu.x - qlx);
+            xv[2 * c2 + 1] = bk[c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
         }
         if (i < Hv) {
             if (MODE == 0) {

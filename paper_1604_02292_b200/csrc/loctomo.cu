@@ -287,12 +287,12 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
 // k_fgp2 (paired-FP32 layout): NW warps of FR full rows per CTA, K CTAs per
 // cluster.  LT_FGP2_CFG = "4x8" (default), "2x8", "2x16" (FR x NW);
 // LT_FGP2_SYNC = 1 replaces the per-phase CTA barrier by warp-to-warp mbarriers.
-template <int MODE, int FR, int NW, int SYNC>
+template <int MODE, int FR, int NW, int SYNC, bool BSM = false>
 int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
-    const size_t smem = (size_t)Fgp2Smem<FR, NW>::total * sizeof(float);
-    auto kern = k_fgp2<MODE, FR, NW, SYNC>;
+    const size_t smem = (size_t)(BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) * sizeof(float);
+    auto kern = k_fgp2<MODE, FR, NW, SYNC, BSM>;
     LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg;
@@ -328,7 +328,7 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
         static int cfgv = -1;
         if (cfgv < 0) {
             const char* e = getenv("LT_FGP2_CFG");
-            cfgv = !e ? 1 : !strcmp(e, "2x8") ? 2 : !strcmp(e, "2x16") ? 0 : 1;
+            cfgv = !e ? 1 : !strcmp(e, "2x8") ? 2 : !strcmp(e, "2x16") ? 0 : !strcmp(e, "2x8b") ? 3 : !strcmp(e, "4x8b") ? 4 : 1;
         }
         static int syncv = -1;
         if (syncv < 0) { const char* e = getenv("LT_FGP2_SYNC"); syncv = (e && atoi(e) == 1) ? 1 : 0; }
@@ -339,6 +339,8 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
         }
         if (cfgv == 1) return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
         if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
+        if (cfgv == 3) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
+        if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8, 0, true>(A, rows, ntiles, st);
         return launch_fgp2_t<MODE, 2, 16, 0>(A, rows, ntiles, st);
     }
     FgpCfg c;
@@ -776,7 +778,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(cudaStreamSynchronize(st));
     if (!p->gst[0]) {
         const char* e = getenv("LT_SPLIT");
-        p->nsplit = (e && atoi(e) == 1) ? 1 : 2;
+        p->nsplit = (e && atoi(e) == 2) ? 2 : 1;     // default: one stream (kernels fill the SMs; overlap gains ~2%)
         int lo_prio = 0, hi_prio = 0;
         LT_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
         const char* pe = getenv("LT_PRIO");
