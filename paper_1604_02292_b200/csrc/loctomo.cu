@@ -285,8 +285,8 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
 }
 
 // k_fgp2 (paired-FP32 layout): NW warps of FR full rows per CTA, K CTAs per
-// cluster.  LT_FGP2_CFG = "4x8" (default), "2x8", "2x16" (FR x NW);
-// LT_FGP2_SYNC = 1 replaces the per-phase CTA barrier by warp-to-warp mbarriers.
+// cluster.  LT_FGP2_CFG = "4x8" (default, 8-CTA clusters for 256-row tiles),
+// "2x8" (16-CTA clusters), "2x8b" (b in shared memory, two CTAs per SM).
 template <int MODE, int FR, int NW, int SYNC, bool BSM = false>
 int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
@@ -328,20 +328,11 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
         static int cfgv = -1;
         if (cfgv < 0) {
             const char* e = getenv("LT_FGP2_CFG");
-            cfgv = !e ? 1 : !strcmp(e, "2x8") ? 2 : !strcmp(e, "2x16") ? 0 : !strcmp(e, "2x8b") ? 3 : !strcmp(e, "4x8b") ? 4 : 1;
+            cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : 0;
         }
-        static int syncv = -1;
-        if (syncv < 0) { const char* e = getenv("LT_FGP2_SYNC"); syncv = (e && atoi(e) == 1) ? 1 : 0; }
-        if (syncv == 1) {
-            if (cfgv == 1) return launch_fgp2_t<MODE, 4, 8, 1>(A, rows, ntiles, st);
-            if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 1>(A, rows, ntiles, st);
-            return launch_fgp2_t<MODE, 2, 16, 1>(A, rows, ntiles, st);
-        }
-        if (cfgv == 1) return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
-        if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
-        if (cfgv == 3) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
-        if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8, 0, true>(A, rows, ntiles, st);
-        return launch_fgp2_t<MODE, 2, 16, 0>(A, rows, ntiles, st);
+        if (cfgv == 1) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
+        if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
+        return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
     }
     FgpCfg c;
     if (int rc = fgp_config(rows, cols, A.nfgp, &c)) return rc;
