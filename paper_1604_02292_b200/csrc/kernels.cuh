@@ -1281,6 +1281,21 @@ __global__ void __launch_bounds__(NW * 32, BSM ? 2 : 1) k_fgp2(FgpArgs A) {
         #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) pup0[c2] = f2s(0.5f);
     }
+    // FISTA state of all rows first (independent loads in flight together)
+    float xpv[MODE == 1 ? FR : 1][8], xsv[MODE == 1 ? FR : 1][8];
+    if constexpr (MODE == 1) {
+        #pragma unroll
+        for (int k = 0; k < FR; ++k) {
+            const int i = i0 + k;
+            const long long prow = (long long)tile * A.p_tstride + (long long)(vr0 + i) * A.T + vc0 + x0;
+            #pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const bool ok = i < Hv && x0 + c < Wv;
+                xpv[k][c] = ok ? __ldcs(A.xprev + prow + c) : 0.f;
+                xsv[k][c] = ok ? __ldcs(A.xs + prow + c) : 0.f;
+            }
+        }
+    }
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
@@ -1297,34 +1312,22 @@ __global__ void __launch_bounds__(NW * 32, BSM ? 2 : 1) k_fgp2(FgpArgs A) {
             xv[2 * c2 + 1] = bk[c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
         }
         if (i < Hv) {
-            if (MODE == 0) {
+            if constexpr (MODE == 0) {
                 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (x0 + c < Wv) A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + x0 + c] = xv[c];
             } else {
-                // all loads of the row first (the stores below touch other addresses
-                // of this thread only), so their latencies overlap
                 const int ti_ = vr0 + i;
                 const long long prow = (long long)tile * A.p_tstride + (long long)ti_ * A.T + vc0 + x0;
-                const float* __restrict__ xpp = A.xprev + prow;
-                const float* __restrict__ xsp = A.xs + prow;
-                float xpv[8], xsv[8];
-                #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const bool ok = x0 + c < Wv;
-                    xpv[c] = ok ? xpp[c] : 0.f;
-                    xsv[c] = ok ? __ldg(xsp + c) : 0.f;
-                }
-                float* __restrict__ yrow = A.y + (long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + vc0 + x0;
-                float* __restrict__ ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + ti_;
-                float* __restrict__ xpw = A.xprev + prow;
+                float* yrow = A.y + (long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + vc0 + x0;
+                float* ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + ti_;
                 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     if (x0 + c >= Wv) continue;
                     const float x = xv[c];
-                    const float rr = x + A.beta_o * (x - xpv[c]);             // FISTA extrapolation (A12)
-                    const float yv = rr - xsv[c];                             // x_L^k = r - x_s^k
-                    xpw[c] = x;
+                    const float rr = x + A.beta_o * (x - xpv[k][c]);          // FISTA extrapolation (A12)
+                    const float yv = rr - xsv[k][c];                          // x_L^k = r - x_s^k
+                    A.xprev[prow + c] = x;
                     yrow[c] = yv;
                     ycol[(long long)c * A.TP] = yv;
                 }
