@@ -151,6 +151,17 @@ int lt_global_tv(lt_plan* plan, const float* d_sino, int32_t n_iter, float lambd
 int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda,
                  int32_t n_fgp, float* d_out, void* stream);
 
+/* Truncated projection data ("simply
+ * padding the acquired data", constant padding P:L1148): each of the
+ * n_angles rows of d_in (n_trunc measured central bins, row-major
+ * [n_angles][n_trunc]) is extended on both sides with its edge value to n_det
+ * bins, centred: d_out[a][d] = d_in[a][clamp(d - (n_det - n_trunc)/2, 0,
+ * n_trunc - 1)] ([n_angles][n_det]).  The result is an ordinary sinogram of the
+ * plan's geometry.  Errors (2): n_angles < 1, n_trunc < 1, n_det < n_trunc,
+ * n_det - n_trunc odd (no centred padding), null pointers. */
+int lt_pad_truncated(const float* d_in, int32_t n_angles, int32_t n_trunc, int32_t n_det, float* d_out,
+                     void* stream);
+
 /* Number of kernels this library has launched so far (process-wide). */
 int64_t lt_launch_count(void);
 

@@ -221,6 +221,24 @@ def stitch(n: int, centres, radius: int, cores: np.ndarray) -> np.ndarray:
     return img
 
 
+def pad_truncated(p_t: np.ndarray, n_det: int) -> np.ndarray:
+    """Truncated projection data:
+    each angle row of the n_trunc measured central bins is extended on both
+    sides with its edge value ("constant padding", L1148) to n_det bins, centred
+    so that bin j of the truncated row keeps its detector coordinate."""
+    p_t = _f64(p_t)
+    na, nt = p_t.shape
+    if nt < 1 or n_det < nt or (n_det - nt) % 2:
+        raise OracleError("pad_truncated: need 1 <= n_trunc <= n_det, n_det - n_trunc even")
+    lo = (n_det - nt) // 2
+    out = np.empty((na, n_det))
+    for a in range(na):
+        out[a, :lo] = p_t[a, 0]
+        out[a, lo:lo + nt] = p_t[a]
+        out[a, lo + nt:] = p_t[a, nt - 1]
+    return out
+
+
 def pipeline(p: np.ndarray, angles, n: int, centres, radius: int, margin: int, n_iter: int,
              mode: str = "box", lo: float = 0.0, hi: float = np.inf, lam: float = 0.0,
              n_fgp: int = 100, use_disc: bool = True, bank: Optional[np.ndarray] = None,

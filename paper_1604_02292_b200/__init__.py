@@ -57,6 +57,7 @@ _SIGS = {
     "lt_global_sirt": ([_P, _P, _I, _F, _F, _P, _P], _I),
     "lt_global_tv": ([_P, _P, _I, _F, _I, _P, _P], _I),
     "lt_fgp_batch": ([_I, _I, _I, _P, _F, _I, _P, _P], _I),
+    "lt_pad_truncated": ([_P, _I, _I, _I, _P, _P], _I),
     "lt_launch_count": ([], _i64),
     "lt_timing_enable": ([_I], None),
     "lt_timing_read": ([_P, _P], _I),
@@ -283,4 +284,19 @@ def fgp_batch(x: torch.Tensor, lam: float, n_fgp: int) -> torch.Tensor:
     cnt, h, w = x.shape
     out = torch.empty_like(x)
     _chk(_lib.lt_fgp_batch(h, w, cnt, x.data_ptr(), lam, n_fgp, out.data_ptr(), _stream(x.device)), "lt_fgp_batch")
+    return out
+
+
+def pad_truncated(sino_t: torch.Tensor, n_det: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Edge-constant, centred padding of truncated data ([N_theta, n_trunc] ->
+    [N_theta, n_det]), PAPER.md L1134-1170 (lt_pad_truncated)."""
+    sino_t = _cuda_f32(sino_t, "sino_t")
+    na, nt = sino_t.shape
+    if out is None:
+        out = torch.empty(na, n_det, dtype=torch.float32, device=sino_t.device)
+    out = _cuda_f32(out, "out")
+    if tuple(out.shape) != (na, n_det):
+        raise ValueError(f"out must be ({na}, {n_det})")
+    _chk(_lib.lt_pad_truncated(sino_t.data_ptr(), na, nt, n_det, out.data_ptr(), _stream(sino_t.device)),
+         "lt_pad_truncated")
     return out

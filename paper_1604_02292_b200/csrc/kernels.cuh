@@ -1495,6 +1495,14 @@ __global__ void k_extract(int n, int T, int TP, TileT ti, const float* __restric
     tT[(long long)j * TP + PADL + i] = v;
 }
 
+// truncated data, edge-constant centred padding: one thread per output bin
+__global__ void k_pad_truncated(int na, int nt, int nd, const float* __restrict__ in, float* __restrict__ out) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x, a = blockIdx.y;
+    if (d >= nd) return;
+    const int j = min(max(d - (nd - nt) / 2, 0), nt - 1);
+    out[(long long)a * nd + d] = __ldg(in + (long long)a * nt + j);
+}
+
 // window -> full sinogram (zero outside the window)
 __global__ void k_scatter_win(int na, int nd, int Wwin, const int* __restrict__ d0,
                               const float* __restrict__ win, float* __restrict__ sino) {

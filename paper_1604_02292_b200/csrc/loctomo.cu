@@ -1075,6 +1075,17 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
     return launch_fgp<0>(A, h, w, count, (cudaStream_t)stream);
 }
 
+int lt_pad_truncated(const float* d_in, int32_t n_angles, int32_t n_trunc, int32_t n_det, float* d_out,
+                     void* stream) {
+    if (n_angles < 1 || n_trunc < 1 || n_det < n_trunc || (n_det - n_trunc) % 2)
+        return fail(LT_ERR_INVALID, "pad_truncated: need n_angles >= 1, 1 <= n_trunc <= n_det, n_det - n_trunc even");
+    if (!d_in || !d_out) return fail(LT_ERR_INVALID, "null pointer");
+    dim3 grid((n_det + 255) / 256, n_angles);
+    k_pad_truncated<<<grid, 256, 0, (cudaStream_t)stream>>>(n_angles, n_trunc, n_det, d_in, d_out);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
 void lt_plan_destroy(lt_plan* p) {
     if (!p) return;
     for (int g = 0; g < 2; ++g) {

@@ -69,6 +69,7 @@ class Config:
     n_fgp: int
     n_ellipses: int
     n_rects: int
+    n_trunc: int = 0   # > 0: only the central n_trunc detector bins are measured
 
 
 # BASELINE.json "configs", in order (C1..C5).  lambda for C3/C4 is not given
@@ -84,6 +85,14 @@ CONFIGS = {
                  64, "tiling", 200, "tv", 0.05, 100, 32, 0),
     "C5": Config(5, "C5", 4096, 256, math.pi, 5793, "gauss", 0.01, 1024, 64,
                  64, "tiling", 500, "sirt", 0.0, 100, 64, 0),
+    # SURVEY §8(f) NEXT-3, the paper's truncated-data experiment (PAPER.md L1143-1148:
+    # 1024 detectors truncated to the central 256, 512 angles on [0, pi), Poisson
+    # noise, TV, central ROI): here N = 1024 with the full detector N_d = 1449
+    # truncated to the central 257 bins (odd, so it stays centred), I0 = 1e4 (the
+    # paper gives none for this figure), a central 192^2 core with margin 32
+    # (extended side 256, the kernels' maximum).
+    "T1": Config(6, "T1", 1024, 512, math.pi, 1449, "poisson", 1e4, 1, 96, 32,
+                 "centre", 200, "tv", 0.05, 100, 25, 0, 257),
 }
 
 
@@ -244,6 +253,7 @@ class Inputs:
     sino: np.ndarray            # fp32 [N_theta, N_d]  (noisy, the solver input)
     sino_clean: np.ndarray      # fp64 [N_theta, N_d]
     centres: np.ndarray         # int32 [R, 2]
+    sino_trunc: Optional[np.ndarray] = None   # fp32 [N_theta, n_trunc]: the measured central bins
 
 
 def make_inputs(name_or_cfg, n_angles: Optional[int] = None, n_det: Optional[int] = None,
@@ -257,4 +267,8 @@ def make_inputs(name_or_cfg, n_angles: Optional[int] = None, n_det: Optional[int
     shapes = random_shapes(cfg.n, cfg.n_ellipses, cfg.n_rects, seeded_rng(cfg.cfg_id, 0))
     clean = analytic_sinogram(shapes, ang, cfg.n_det)
     sino = add_noise(clean, cfg.noise, cfg.noise_level, seeded_rng(cfg.cfg_id, 1)) if noise else clean
-    return Inputs(cfg, ang, shapes, sino.astype(np.float32), clean, roi_centres(cfg))
+    trunc = None
+    if cfg.n_trunc:
+        lo = (cfg.n_det - cfg.n_trunc) // 2
+        trunc = np.ascontiguousarray(sino[:, lo:lo + cfg.n_trunc]).astype(np.float32)
+    return Inputs(cfg, ang, shapes, sino.astype(np.float32), clean, roi_centres(cfg), trunc)

@@ -314,3 +314,36 @@ def test_host_buffer_entry_matches_device_path(lt):
     img_host = plan.solve_host("sirt", torch.from_numpy(inp.sino).pin_memory(), 0.0, math.inf)
     torch.cuda.synchronize()
     assert np.array_equal(img_host.numpy().astype(np.float64), img_dev)
+
+
+# ------------------------------------------------------------------ NEXT-3: truncated data
+
+@pytest.mark.parametrize("na,nt,nd", [(512, 257, 1449), (7, 1, 91), (3, 91, 91), (40, 31, 91)])
+def test_pad_truncated_exact(lt, orc, na, nt, nd):
+    """lt_pad_truncated is a copy: bit-exact against the oracle (T1 size and edge cases)."""
+    p = np.random.default_rng(nt).random((na, nt)).astype(np.float32)
+    got = cpu(lt.pad_truncated(gpu(p), nd))
+    assert np.array_equal(got, orc.pad_truncated(p.astype(np.float64), nd))
+
+
+def test_pad_truncated_rejects(lt):
+    with pytest.raises(ValueError):
+        lt.pad_truncated(gpu(np.zeros((4, 9))), 10)      # odd difference
+    with pytest.raises(ValueError):
+        lt.pad_truncated(gpu(np.zeros((4, 9))), 7)       # target smaller than the data
+
+
+def test_truncated_tv_solve(lt, orc):
+    """T1 recipe at C1 size: central 31 of 91 bins measured, padded on the GPU,
+    then the local FISTA-TV path, against the oracle on the oracle's padding."""
+    cfg = synth.Config(21, "trunc-small", 64, 48, math.pi, 91, "poisson", 1e4, 1, 12, 8, "centre", 15, "tv",
+                       0.05, 40, 5, 0, 31)
+    inp = synth.make_inputs(cfg)
+    assert inp.sino_trunc.shape == (48, 31)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    padded = lt.pad_truncated(gpu(inp.sino_trunc), cfg.n_det)
+    cores = cpu(plan.tv_solve(padded, cfg.lam, cfg.n_fgp))
+    ref = orc.pipeline(orc.pad_truncated(inp.sino_trunc.astype(np.float64), cfg.n_det), inp.angles, cfg.n,
+                       inp.centres, cfg.radius, cfg.margin, cfg.n_iter, mode="tv", lam=cfg.lam, n_fgp=cfg.n_fgp)
+    assert relerr(cores[0], ref[0]) <= 1e-3

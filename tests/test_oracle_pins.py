@@ -398,3 +398,34 @@ def test_P14_stitch(orc):
     img2 = orc.stitch(n, cen2, r, cores[:2])
     assert img2[3, 3] == 0.5 * (cores[0][3, 3] + cores[1][1, 1])
     assert img2[0, 0] == cores[0][0, 0] and img2[15, 15] == 0.0
+
+
+# ------------------------------------------------------------------ NEXT-3: truncated data
+
+def test_pad_truncated_pins(orc):
+    """Truncated data (constant padding L1148): identity when
+    nothing is truncated, zeros stay zeros, the edge value extends each row."""
+    rng = np.random.default_rng(31)
+    p = rng.random((5, 9))
+    assert np.array_equal(orc.pad_truncated(p, 9), p)
+    assert np.array_equal(orc.pad_truncated(np.zeros((3, 5)), 11), np.zeros((3, 11)))
+    q = orc.pad_truncated(p, 15)
+    assert np.array_equal(q[:, 3:12], p)
+    assert np.array_equal(q[:, :3], np.repeat(p[:, :1], 3, axis=1))
+    assert np.array_equal(q[:, 12:], np.repeat(p[:, -1:], 3, axis=1))
+    with pytest.raises(orc.OracleError):
+        orc.pad_truncated(p, 10)          # odd difference: no centred padding
+    with pytest.raises(orc.OracleError):
+        orc.pad_truncated(p, 7)           # target smaller than the data
+
+
+def test_pad_truncated_keeps_detector_coordinates(orc):
+    """Centring pinned against the geometry (V1: t_d = d - (N_d - 1)/2): the
+    analytic sinogram measured on n_trunc central bins equals the central bins of
+    the full-detector sinogram, and padding puts them back at the same place."""
+    shapes = synth.random_shapes(64, 5, 0, synth.seeded_rng(31, 0))
+    ang = synth.angles_for(12)
+    full = synth.analytic_sinogram(shapes, ang, 91)
+    trunc = synth.analytic_sinogram(shapes, ang, 31)
+    assert np.allclose(trunc, full[:, 30:61], rtol=0, atol=1e-12)
+    assert np.array_equal(orc.pad_truncated(trunc, 91)[:, 30:61], trunc)
