@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--xs-exact", action="store_true",
+                    help="NEXT-4(i): x_s^k from the global SIRT iterate instead of the filtered backprojection")
     return ap.parse_args()
 
 
@@ -133,7 +135,8 @@ def run_ours(args, cfg):
     inp = synth.make_inputs(cfg)
     n_iter = cfg.n_iter
     mode = "tv" if "tv" in cfg.solver else "sirt"
-    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter, rank=rank, world=world)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter, rank=rank, world=world,
+                   xs_exact=args.xs_exact)
     rects, _, _ = plan.tables()
     # per-geometry precompute (outside the timed region)
     torch.cuda.synchronize()
@@ -296,7 +299,9 @@ def run_ours(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.n}, {cfg.n_angles} angles, {cfg.n_det} det, "
                                f"{cfg.n_roi} ROIs r={cfg.radius} m={cfg.margin}, {mode}, n={n_iter}"
-                               + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" else ""),
+                               + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" else "")
+                               + (f", truncated to {cfg.n_trunc} central bins" if cfg.n_trunc else "")
+                               + (", x_s = global SIRT iterate (exact)" if args.xs_exact else ""),
                    "global_batch_rois": cfg.n_roi, "parallelism": f"roi-shard x{world}",
                    "l2": "inputs larger than L2 (conv cache 417 MB + ROI state), no flush",
                    "bank": "warm (per-geometry precompute, excluded)"},

@@ -42,6 +42,11 @@ extern "C" {
 
 /* flags for lt_roi_setup */
 #define LT_DISC_ON 1   /* disc pre-correction, default on */
+#define LT_XS_EXACT 2  /* x_s^k = M_{L'} (global SIRT iterate k) instead of
+                        * FBP_L(p_c, u_k) + cD (removes approximation 1 of P:L625-630, so a
+                        * ROI covering the grid reproduces the global solve, pins P9/P10); the
+                        * SIRT iterate is advanced once per iteration on the full grid (shared by
+                        * all ROIs), no filter bank, conv cache or disc is used */
 
 typedef struct lt_plan lt_plan;
 

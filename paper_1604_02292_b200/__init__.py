@@ -28,6 +28,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 LT_OK, LT_ERR_RUNTIME, LT_ERR_INVALID = 0, 1, 2
 LT_DISC_ON = 1
+LT_XS_EXACT = 2
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int32
@@ -126,8 +127,10 @@ class Plan:
     """
 
     def __init__(self, n: int, angles, n_det: int, centres, radius: int, margin: int, n_iter: int,
-                 disc: bool = True, rank: int = 0, world: int = 1, device=None, bind: bool = True):
-        """bind=False plans on the host only (tables, partition); no device memory."""
+                 disc: bool = True, rank: int = 0, world: int = 1, device=None, bind: bool = True,
+                 xs_exact: bool = False):
+        """bind=False plans on the host only (tables, partition); no device memory.
+        xs_exact: x_s^k from the global SIRT iterate (LT_XS_EXACT, NEXT-4(i))."""
         if bind:
             self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         else:
@@ -142,7 +145,8 @@ class Plan:
         self._p = ctypes.c_void_p()
         _chk(_lib.lt_roi_setup(self.n, len(ang), self.n_det, ang.ctypes.data, len(cen), rows.ctypes.data,
                                cols.ctypes.data, self.radius, self.margin, self.n_iter,
-                               LT_DISC_ON if disc else 0, rank, world, ctypes.byref(self._p)), "lt_roi_setup")
+                               (LT_DISC_ON if disc else 0) | (LT_XS_EXACT if xs_exact else 0), rank, world,
+                               ctypes.byref(self._p)), "lt_roi_setup")
         self.workspace_bytes = nbytes = int(_lib.lt_plan_workspace_bytes(self._p))
         if bind:
             with torch.cuda.device(self.device):

@@ -385,7 +385,8 @@ int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
 // the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
 // one ROI group (tiles [t0, t0 + cnt)) through all n iterations on stream st
 int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp,
-                     cudaStream_t st, cudaStream_t fst = nullptr, cudaEvent_t pev = nullptr, cudaEvent_t fev = nullptr) {
+                     const float* d_sino, cudaStream_t st, cudaStream_t fst = nullptr, cudaEvent_t pev = nullptr,
+                     cudaEvent_t fev = nullptr) {
     Tiles t = p.roi_tiles();
     t.tile += t0; t.d0 += (size_t)t0 * p.na; t.tauc += (size_t)t0 * p.na; t.ntiles = cnt;
     const long long yts = p.ytile();
@@ -396,17 +397,30 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
     float* xs = p.P<float>(p.off.xs) + t0 * p.ptile();
     float* xprev = p.P<float>(p.off.xprev) + t0 * p.ptile();
     const long long ns = (long long)p.na * p.nd;
-    const bool disc = (p.flags & LT_DISC_ON) != 0;
+    const bool exact = (p.flags & LT_XS_EXACT) != 0;
+    const bool disc = (p.flags & LT_DISC_ON) != 0 && !exact;
     // x_s^k = M_{L'} W^T b_k for every ROI of the group comes from one global
     // backprojection over the image blocks the group's extended ROIs cover
     // (the extended ROIs overlap, so this is ~4x less work than per ROI)
     float* xsg = p.P<float>(p.off.xsg[gl == 2 ? 1 : 0]);
+    int xsg_pitch = p.n;
     const int* blist = p.P<int>(p.off.xsblk[gl]);
     const int nbl = (int)p.xsblk[gl].size();
+    if (exact) { xsg = p.P<float>(p.off.gimg) + PADL; xsg_pitch = p.GTP; }   // the global SIRT iterate
     double tk = 1.0;
     for (int k = 0; k < p.n_iter; ++k) {
         const float* bk = p.P<float>(p.off.conv) + (long long)k * ns;
-        {   // (independent of y: overlaps the previous FGP of this group)
+        if (exact) {   // x^k = x^{k-1} + alpha W^T (p - W x^{k-1}) on the full grid, x^0 = 0 (eq. sirtit)
+            const Tiles gt = p.glob_tiles();
+            float* gx = p.P<float>(p.off.gimg);
+            float* gxT = p.P<float>(p.off.gimgT);
+            float* r = p.P<float>(p.off.gsino);
+            if (int rc = launch_fp(p, 2, gt, gx, gxT, 0, r, 0, d_sino, nullptr, st)) return rc;
+            BpEpi eg = epi0();
+            eg.y = gx; eg.yT = gxT; eg.alpha = (float)p.alpha;
+            const SinoView sv = view_full(r, p.nd);
+            if (int rc = launch_bp_t<1, BP_GSIRT>(p, gt, sv, sv, eg, st)) return rc;
+        } else {   // (independent of y: overlaps the previous FGP of this group)
             BpEpi ex = epi0();
             ex.blist = blist; ex.out = xsg; ex.out_pitch = p.n;
             const SinoView vb = view_full(bk, p.nd);
@@ -414,7 +428,7 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
         }
         if (fst && k > 0) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));    // previous FGP of this group
         BpEpi e = epi0();
-        e.xsg = xsg; e.xsg_pitch = p.n;
+        e.xsg = xsg; e.xsg_pitch = xsg_pitch;
         e.y = y; e.yT = yT; e.y_tstride = yts;
         e.v = v; e.xs = xs; e.p_tstride = p.ptile();
         e.discc = p.P<float>(p.off.discc32); e.use_disc = disc;
@@ -457,14 +471,21 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
 }
 
 // the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
-int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, cudaStream_t st) {
+int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, const float* d_sino,
+                     cudaStream_t st) {
     const long long yts = p.ytile();
+    const bool exact = (p.flags & LT_XS_EXACT) != 0;
+    if (exact) {
+        const size_t gbytes = (size_t)p.GT * p.GTP * sizeof(float);
+        LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.gimg), 0, gbytes, st));
+        LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.gimgT), 0, gbytes, st));
+    }
     LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.y), 0, (size_t)p.R * yts * sizeof(float), st));
     LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.yT), 0, (size_t)p.R * yts * sizeof(float), st));
     if (mode == 1) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
-    const int ng = (p.nsplit > 1 && p.R >= 2 && p.gst[0]) ? 2 : 1;
+    const int ng = (p.nsplit > 1 && p.R >= 2 && p.gst[0] && !exact) ? 2 : 1;
     if (ng == 1) {
-        if (int rc = group_iterations(p, 0, 0, p.R, mode, lo, hi, lam, nfgp, st)) return rc;
+        if (int rc = group_iterations(p, 0, 0, p.R, mode, lo, hi, lam, nfgp, d_sino, st)) return rc;
     } else {
         // fork: both group streams wait for the work already queued on st
         LT_CUDA(cudaEventRecord(p.gev[2], st));
@@ -474,8 +495,8 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
             const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
             const bool prio = p.fst[g] && mode == 1;
             if (prio) LT_CUDA(cudaStreamWaitEvent(p.fst[g], p.gev[2], 0));
-            if (int rc = group_iterations(p, 1 + g, t0, cnt, mode, lo, hi, lam, nfgp, p.gst[g], prio ? p.fst[g] : nullptr,
-                                          p.pev[g], p.fev[g])) return rc;
+            if (int rc = group_iterations(p, 1 + g, t0, cnt, mode, lo, hi, lam, nfgp, d_sino, p.gst[g],
+                                          prio ? p.fst[g] : nullptr, p.pev[g], p.fev[g])) return rc;
             LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
         }
         // join
@@ -499,14 +520,18 @@ int crop_cores(lt_plan& p, float* d_cores, cudaStream_t st) {
 
 int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfgp, float* d_cores, cudaStream_t st) {
     float* pc = p.P<float>(p.off.pc);
-    if (p.flags & LT_DISC_ON) {
+    if (p.flags & LT_XS_EXACT) {
+        LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.discc32), 0, sizeof(float), st));
+    } else if (p.flags & LT_DISC_ON) {
         if (int rc = disc_correct(p, d_sino, pc, nullptr, st)) return rc;
     } else {
         LT_CUDA(cudaMemcpyAsync(pc, d_sino, (size_t)p.na * p.nd * sizeof(float), cudaMemcpyDeviceToDevice, st));
         LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.discc32), 0, sizeof(float), st));
     }
-    if (int rc = conv_cache(p, pc, st)) return rc;
-    if (int rc = local_iterations(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode == 1 ? a0 : 0.f, nfgp, st))
+    if (!(p.flags & LT_XS_EXACT))
+        if (int rc = conv_cache(p, pc, st)) return rc;
+    if (int rc = local_iterations(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode == 1 ? a0 : 0.f, nfgp,
+                                  d_sino, st))
         return rc;
     return crop_cores(p, d_cores, st);
 }

@@ -347,3 +347,51 @@ def test_truncated_tv_solve(lt, orc):
     ref = orc.pipeline(orc.pad_truncated(inp.sino_trunc.astype(np.float64), cfg.n_det), inp.angles, cfg.n,
                        inp.centres, cfg.radius, cfg.margin, cfg.n_iter, mode="tv", lam=cfg.lam, n_fgp=cfg.n_fgp)
     assert relerr(cores[0], ref[0]) <= 1e-3
+
+
+# ------------------------------------------------------------------ NEXT-4(i): exact x_s
+
+def test_exact_xs_full_grid_is_global_box_sirt(lt, orc):
+    """P9 on the GPU: with x_s^k = the global SIRT iterate (LT_XS_EXACT) a ROI
+    covering the whole grid reproduces global box-SIRT (split exactness,
+    eq. sirtitprior): GPU local vs GPU global and vs the oracle."""
+    n, na, nit = 48, 30, 25
+    inp = synth.make_inputs("C1", n=n, n_angles=na, n_det=nd_for(n))
+    plan = lt.Plan(n, inp.angles, nd_for(n), [[n // 2, n // 2]], n // 2, 0, nit, xs_exact=True)
+    core = cpu(plan.sirt_solve(gpu(inp.sino), 0.0, math.inf))[0]
+    glob = cpu(plan.global_sirt(gpu(inp.sino), nit, 0.0, math.inf))
+    ref = orc.global_box(inp.sino.astype(np.float64), inp.angles, n, nit, lo=0.0, hi=np.inf)
+    assert relerr(core, ref) <= 1e-4
+    assert relerr(core, glob) <= 1e-4
+
+
+def test_exact_xs_full_grid_is_global_fista_tv(lt, orc):
+    """P10 on the GPU: the same for FISTA-TV (Alg. 3 corrected, A12)."""
+    n, na, nit, lam, nf = 32, 24, 10, 0.05, 40
+    inp = synth.make_inputs("C1", n=n, n_angles=na, n_det=nd_for(n))
+    plan = lt.Plan(n, inp.angles, nd_for(n), [[n // 2, n // 2]], n // 2, 0, nit, xs_exact=True)
+    core = cpu(plan.tv_solve(gpu(inp.sino), lam, nf))[0]
+    ref = orc.global_tv(inp.sino.astype(np.float64), inp.angles, n, nit, lam, nf)
+    assert relerr(core, ref) <= 1e-3
+
+
+@pytest.mark.parametrize("mode", ["box", "tv"])
+def test_exact_xs_local_parity(lt, orc, mode):
+    """Exact-x_s local solves on clipped and interior ROIs against the oracle
+    fed the oracle's own unconstrained SIRT iterates (xs_exact)."""
+    n, na, nit = 64, 32, 12
+    inp = synth.make_inputs("C1", n=n, n_angles=na)
+    cen = np.array([[32, 32], [12, 50], [52, 14]], dtype=np.int32)
+    r, m = 10, 6
+    plan = lt.Plan(n, inp.angles, 91, cen, r, m, nit, xs_exact=True)
+    p64 = inp.sino.astype(np.float64)
+    _, xs = orc.global_box(p64, inp.angles, n, nit, lo=-np.inf, hi=np.inf, iterates=True)
+    if mode == "box":
+        got = cpu(plan.sirt_solve(gpu(inp.sino), 0.0, math.inf))
+        ref = orc.local_solve(n, inp.angles, 91, np.zeros((nit, na, 91)), cen, r, m, mode="box", xs_exact=xs)
+    else:
+        got = cpu(plan.tv_solve(gpu(inp.sino), 0.05, 30))
+        ref = orc.local_solve(n, inp.angles, 91, np.zeros((nit, na, 91)), cen, r, m, mode="tv", lam=0.05,
+                              n_fgp=30, xs_exact=xs)
+    for q in range(3):
+        assert relerr(got[q], ref[q]) <= 1e-3, q
