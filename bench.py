@@ -161,14 +161,29 @@ def run_ours(args, cfg):
     image = torch.empty(cfg.n, cfg.n, device="cuda")
     gathered = torch.empty(world * spr, side, side, device="cuda") if world > 1 else None
 
+    # lambda-sweep workloads (L1, NEXT-1): every ROI carries its own lambda; the
+    # step scores each core against the ground truth (MSE, SSIM) instead of combining
+    sweep = cfg.layout == "sweep"
+    lam_arg = cfg.lam
+    scores = {}
+    if sweep:
+        lam_arg = synth.sweep_lambdas(cfg)[plan.local_rois]
+        truth = synth.raster(inp.shapes, cfg.n)
+        r_ = cfg.radius
+        tc = np.stack([truth[c[0] - r_:c[0] + r_, c[1] - r_:c[1] + r_] for c in inp.centres[plan.local_rois]])
+        truth_cores = torch.from_numpy(tc.astype(np.float32)).cuda()
+
     def step():
         out = cores[:plan.R]
         if trunc:
             lt.pad_truncated(sino_in, cfg.n_det, out=sino)
         if mode == "tv":
-            plan.tv_solve(sino, cfg.lam, cfg.n_fgp, out=out)
+            plan.tv_solve(sino, lam_arg, cfg.n_fgp, out=out)
         else:
             plan.sirt_solve(sino, 0.0, math.inf, out=out)
+        if sweep:
+            scores["mse"], scores["ssim"] = lt.metrics(out, truth_cores)
+            return
         if world > 1:
             ltd.gather_cores(cores, out=gathered)          # NCCL all-gather over NVLink
             plan.combine(gathered, slot_roi, out=image)
@@ -210,7 +225,16 @@ def run_ours(args, cfg):
 
     # e2e: same step through the host-buffer C-ABI entry (pinned H2D + solve + combine + D2H)
     image_host = torch.empty(cfg.n, cfg.n, dtype=torch.float32).pin_memory()
-    if world == 1 and not trunc:
+    if sweep:
+        score_host = torch.empty(2, plan.R, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            sino_in.copy_(sino_host, non_blocking=True)
+            step()
+            score_host[0].copy_(scores["mse"], non_blocking=True)
+            score_host[1].copy_(scores["ssim"], non_blocking=True)
+            torch.cuda.synchronize()
+    elif world == 1 and not trunc:
         def e2e_step():
             plan.solve_host(mode, sino_host, cfg.lam if mode == "tv" else 0.0,
                             0.0 if mode == "tv" else math.inf, cfg.n_fgp, image_host)
@@ -299,9 +323,12 @@ def run_ours(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.n}, {cfg.n_angles} angles, {cfg.n_det} det, "
                                f"{cfg.n_roi} ROIs r={cfg.radius} m={cfg.margin}, {mode}, n={n_iter}"
-                               + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" else "")
+                               + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" and not sweep
+                                  else f", n_fgp={cfg.n_fgp}" if mode == "tv" else "")
                                + (f", truncated to {cfg.n_trunc} central bins" if cfg.n_trunc else "")
-                               + (", x_s = global SIRT iterate (exact)" if args.xs_exact else ""),
+                               + (", x_s = global SIRT iterate (exact)" if args.xs_exact else "")
+                               + (f", lambda sweep: {synth.SWEEP_ROIS} ROIs x {synth.SWEEP_LAMBDAS} lambdas in "
+                                  "[1e-3, 1], MSE+SSIM vs ground truth" if sweep else ""),
                    "global_batch_rois": cfg.n_roi, "parallelism": f"roi-shard x{world}",
                    "l2": "inputs larger than L2 (conv cache 417 MB + ROI state), no flush",
                    "bank": "warm (per-geometry precompute, excluded)"},
@@ -312,7 +339,8 @@ def run_ours(args, cfg):
         "gpu_launches": int(n_launch),
         "e2e": {"value": round(cfg.n_roi / (e2e_ms / 1e3), 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(sino_host.numel() * 4),
-                "d2h_bytes_per_step": int(cfg.n * cfg.n * 4), "ms_per_step": round(e2e_ms, 3)},
+                "d2h_bytes_per_step": int(2 * plan.R * 8 if sweep else cfg.n * cfg.n * 4),
+                "ms_per_step": round(e2e_ms, 3)},
         "roofline": roofline,
         "hbm_peak_gbs": pk.get("hbm_gbs"),
         "clocks": clk,

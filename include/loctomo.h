@@ -156,6 +156,37 @@ int lt_global_tv(lt_plan* plan, const float* d_sino, int32_t n_iter, float lambd
 int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda,
                  int32_t n_fgp, float* d_out, void* stream);
 
+/* Lambda sweep (P:L789-795 tune lambda per reconstruction,
+ * P:L1116-1120 "the same ... for many different parameter values"): the local
+ * FISTA-TV solve of lt_tv_solve with lambda = h_lambdas[q] (host array, one
+ * value >= 0 per LOCAL ROI q, in lt_plan_local_rois order) — every ROI of the
+ * plan may be the same region repeated with another lambda; the ROIs share the
+ * filter bank, the conv cache and the global x_s backprojection.  Errors as
+ * lt_tv_solve, plus 2 for a negative or NaN lambda. */
+int lt_tv_solve_lambdas(lt_plan* plan, const float* d_sino, const float* h_lambdas, int32_t n_fgp,
+                        float* d_cores, void* stream);
+
+/* Quality inside the ROI: for each of `count`
+ * image pairs (d_x[i], d_ref[i], each h x w row-major, device) d_mse[i] =
+ * mean (x - ref)^2 and d_ssim[i] = mean SSIM (Wang et al. 2004: 11 x 11
+ * Gaussian window with sigma 1.5, weights normalised, K1 = 0.01, K2 = 0.03,
+ * population moments, mean over the window positions inside the image — 0
+ * when h or w < 11) with dynamic range L = data_range if > 0, else
+ * max(ref_i) - min(ref_i).  d_mse, d_ssim: device double[count].  Errors (2):
+ * count < 0, h or w < 1, null pointers. */
+int lt_metrics(const float* d_x, const float* d_ref, int32_t count, int32_t h, int32_t w, float data_range,
+               double* d_mse, double* d_ssim, void* stream);
+
+/* One-dimensional Nelder-Mead ("using the Nelder-Mead method")
+ * minimising f(t, ctx) over t in [t_lo, t_hi] (the caller's t, e.g. log10 of
+ * lambda): initial simplex {mid, mid + 0.5}, reflection 1, expansion 2,
+ * contraction 1/2, shrink 1/2, every trial point clamped into the bounds, at
+ * most `budget` evaluations (the 2 initial ones included).  Host-only and
+ * deterministic; writes the best evaluated point and value and the number of
+ * evaluations.  Errors (2): null f/outputs, t_lo >= t_hi, budget < 3. */
+int lt_nelder_mead_1d(double (*f)(double, void*), void* ctx, double t_lo, double t_hi, int32_t budget,
+                      double* t_best, double* f_best, int32_t* n_eval);
+
 /* Truncated projection data ("simply
  * padding the acquired data", constant padding P:L1148): each of the
  * n_angles rows of d_in (n_trunc measured central bins, row-major

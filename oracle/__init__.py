@@ -18,6 +18,7 @@ DESIGN.md).
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from typing import Optional, Tuple
@@ -256,3 +257,104 @@ def pipeline(p: np.ndarray, angles, n: int, centres, radius: int, margin: int, n
     b = conv_cache(bank[:n_iter], pc)
     return local_solve(n, angles, n_det, b, centres, radius, margin, mode=mode, lo=lo, hi=hi,
                        lam=lam, n_fgp=n_fgp, disc_c=c, use_disc=use_disc, want_ext=want_ext)
+
+
+# --------------------------------------------------------------------------- NEXT-1: metrics, Nelder-Mead
+
+def mse(x: np.ndarray, ref: np.ndarray) -> float:
+    """Mean squared error inside the region."""
+    x = _f64(x); ref = _f64(ref)
+    if x.shape != ref.shape:
+        raise OracleError("size mismatch")
+    return float(np.mean((x - ref) ** 2))
+
+
+def ssim_window() -> np.ndarray:
+    """11 x 11 Gaussian window, sigma 1.5, normalised (Wang et al. 2004)."""
+    a = np.arange(11) - 5.0
+    w = np.exp(-(a[:, None] ** 2 + a[None, :] ** 2) / (2.0 * 1.5 ** 2))
+    return w / w.sum()
+
+
+def ssim(x: np.ndarray, ref: np.ndarray, data_range: Optional[float] = None) -> float:
+    """Mean SSIM (Wang et al. 2004): at every position where the
+    11 x 11 window lies inside the image, with population moments under the
+    window weights, C1 = (0.01 L)^2, C2 = (0.03 L)^2, L = max ref - min ref."""
+    x = _f64(x); g = _f64(ref)
+    if x.shape != g.shape:
+        raise OracleError("size mismatch")
+    L = float(data_range) if data_range else float(g.max() - g.min())
+    C1, C2 = (0.01 * L) ** 2, (0.03 * L) ** 2
+    w = ssim_window()
+    h, wd = x.shape
+    vals = []
+    for i in range(h - 10):
+        for j in range(wd - 10):
+            xa = x[i:i + 11, j:j + 11]; ga = g[i:i + 11, j:j + 11]
+            mx, mg = np.sum(w * xa), np.sum(w * ga)
+            vx = np.sum(w * xa * xa) - mx * mx
+            vg = np.sum(w * ga * ga) - mg * mg
+            cxg = np.sum(w * xa * ga) - mx * mg
+            vals.append((2 * mx * mg + C1) * (2 * cxg + C2) / ((mx * mx + mg * mg + C1) * (vx + vg + C2)))
+    return float(np.mean(vals)) if vals else 0.0
+
+
+def nelder_mead_1d(f, t_lo: float, t_hi: float, budget: int):
+    """Nelder & Mead (1965) in one dimension: initial simplex
+    {mid, mid + 0.5}, reflection 1, expansion 2, contraction 1/2, shrink 1/2,
+    trial points clamped into [t_lo, t_hi], at most `budget` evaluations.
+    Returns (t_best, f_best, evaluations)."""
+    if not t_lo < t_hi or budget < 3:
+        raise OracleError("need t_lo < t_hi and budget >= 3")
+    state = {"n": 0, "bx": None, "bf": math.inf}
+
+    def clamp(t):
+        return min(max(t, t_lo), t_hi)
+
+    def F(t):
+        t = clamp(t)
+        v = f(t)
+        state["n"] += 1
+        if state["n"] == 1 or v < state["bf"]:
+            state["bf"], state["bx"] = v, t
+        return v
+
+    mid = 0.5 * (t_lo + t_hi)
+    x0, x1 = mid, clamp(mid + 0.5)
+    if x1 == x0:
+        x1 = clamp(mid - 0.5)
+    f0, f1 = F(x0), F(x1)
+    while state["n"] < budget:
+        if f1 < f0:
+            x0, x1, f0, f1 = x1, x0, f1, f0
+        if abs(x1 - x0) < 1e-9:
+            break
+        xr = clamp(x0 + (x0 - x1))
+        fr = F(xr)
+        if fr < f0:
+            if state["n"] < budget:
+                xe = clamp(x0 + 2.0 * (xr - x0))
+                fe = F(xe)
+                x1, f1 = (xe, fe) if fe < fr else (xr, fr)
+            else:
+                x1, f1 = xr, fr
+            continue
+        if state["n"] >= budget:
+            break
+        if fr < f1:
+            xc = clamp(x0 + 0.5 * (xr - x0))
+            fc = F(xc)
+            if fc <= fr:
+                x1, f1 = xc, fc
+                continue
+        else:
+            xc = clamp(x0 + 0.5 * (x1 - x0))
+            fc = F(xc)
+            if fc < f1:
+                x1, f1 = xc, fc
+                continue
+        if state["n"] >= budget:
+            break
+        x1 = x0 + 0.5 * (x1 - x0)
+        f1 = F(x1)
+    return state["bx"], state["bf"], state["n"]

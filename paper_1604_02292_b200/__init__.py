@@ -59,6 +59,9 @@ _SIGS = {
     "lt_global_tv": ([_P, _P, _I, _F, _I, _P, _P], _I),
     "lt_fgp_batch": ([_I, _I, _I, _P, _F, _I, _P, _P], _I),
     "lt_pad_truncated": ([_P, _I, _I, _I, _P, _P], _I),
+    "lt_tv_solve_lambdas": ([_P, _P, _P, _I, _P, _P], _I),
+    "lt_metrics": ([_P, _P, _I, _I, _I, _F, _P, _P, _P], _I),
+    "lt_nelder_mead_1d": ([_P, _P, ctypes.c_double, ctypes.c_double, _I, _P, _P, _P], _I),
     "lt_launch_count": ([], _i64),
     "lt_timing_enable": ([_I], None),
     "lt_timing_read": ([_P, _P], _I),
@@ -233,14 +236,39 @@ class Plan:
              "lt_sirt_solve")
         return out
 
-    def tv_solve(self, sino: torch.Tensor, lam: float, n_fgp: int = 100,
+    def tv_solve(self, sino: torch.Tensor, lam, n_fgp: int = 100,
                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """lam: one value, or one per local ROI (lambda sweep, lt_tv_solve_lambdas)."""
         sino = _cuda_f32(sino, "sino")
         side = 2 * self.radius
         out = self._empty(self.R, side, side) if out is None else out
-        _chk(_lib.lt_tv_solve(self._p, sino.data_ptr(), lam, n_fgp, out.data_ptr(), _stream(self.device)),
-             "lt_tv_solve")
+        if np.ndim(lam) == 0:
+            _chk(_lib.lt_tv_solve(self._p, sino.data_ptr(), float(lam), n_fgp, out.data_ptr(), _stream(self.device)),
+                 "lt_tv_solve")
+        else:
+            lams = np.ascontiguousarray(np.asarray(lam, dtype=np.float32).reshape(-1))
+            if lams.size != self.R:
+                raise ValueError(f"{lams.size} lambdas for {self.R} local ROIs")
+            _chk(_lib.lt_tv_solve_lambdas(self._p, sino.data_ptr(), lams.ctypes.data, n_fgp, out.data_ptr(),
+                                          _stream(self.device)), "lt_tv_solve_lambdas")
         return out
+
+    def optimize_lambda(self, sino: torch.Tensor, ref_cores: torch.Tensor, target: str = "mse",
+                        log10_bounds=(-3.0, 0.0), budget: int = 20, n_fgp: int = 100):
+        """lambda minimising the mean MSE (or maximising the mean SSIM) of this
+        plan's ROI cores against ref_cores by Nelder-Mead in log10(lambda)
+        (PAPER.md L789-795): returns (lambda, value, evaluations)."""
+        ref = _cuda_f32(ref_cores, "ref_cores")
+        side = 2 * self.radius
+        cores = self._empty(self.R, side, side)
+
+        def objective(t):
+            self.tv_solve(sino, 10.0 ** t, n_fgp, out=cores)
+            mse, ssim = metrics(cores, ref)
+            return float(mse.mean()) if target == "mse" else -float(ssim.mean())
+
+        t, v, n = nelder_mead_1d(objective, log10_bounds[0], log10_bounds[1], budget)
+        return 10.0 ** t, (v if target == "mse" else -v), n
 
     def get_ext(self) -> torch.Tensor:
         E = 2 * self.h
@@ -304,3 +332,43 @@ def pad_truncated(sino_t: torch.Tensor, n_det: int, out: Optional[torch.Tensor] 
     _chk(_lib.lt_pad_truncated(sino_t.data_ptr(), na, nt, n_det, out.data_ptr(), _stream(sino_t.device)),
          "lt_pad_truncated")
     return out
+
+
+def metrics(x: torch.Tensor, ref: torch.Tensor, data_range: Optional[float] = None):
+    """(MSE, SSIM) per image of x vs ref ((count, h, w) or (h, w)), as float64
+    CUDA tensors (lt_metrics)."""
+    x = _cuda_f32(x, "x")
+    ref = _cuda_f32(ref, "ref")
+    if x.shape != ref.shape:
+        raise ValueError("x and ref must have the same shape")
+    x3 = x.reshape(-1, x.shape[-2], x.shape[-1])
+    cnt, h, w = x3.shape
+    mse = torch.empty(cnt, dtype=torch.float64, device=x.device)
+    ssim = torch.empty(cnt, dtype=torch.float64, device=x.device)
+    _chk(_lib.lt_metrics(x3.data_ptr(), ref.data_ptr(), cnt, h, w, float(data_range or 0.0), mse.data_ptr(),
+                         ssim.data_ptr(), _stream(x.device)), "lt_metrics")
+    return mse, ssim
+
+
+_NM_CB = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+
+
+def nelder_mead_1d(f, t_lo: float, t_hi: float, budget: int):
+    """Minimise f(t) over [t_lo, t_hi] with the library's 1-D Nelder-Mead
+    (lt_nelder_mead_1d): returns (t_best, f_best, evaluations)."""
+    err = []
+
+    def cb(t, _ctx):
+        try:
+            return float(f(t))
+        except Exception as e:   # noqa: BLE001 - re-raised after the C call returns
+            err.append(e)
+            return math.inf
+
+    c = _NM_CB(cb)
+    tb, fb, ne = ctypes.c_double(0.0), ctypes.c_double(0.0), ctypes.c_int32(0)
+    _chk(_lib.lt_nelder_mead_1d(ctypes.cast(c, ctypes.c_void_p), None, t_lo, t_hi, budget, ctypes.byref(tb),
+                                ctypes.byref(fb), ctypes.byref(ne)), "lt_nelder_mead_1d")
+    if err:
+        raise err[0]
+    return tb.value, fb.value, ne.value

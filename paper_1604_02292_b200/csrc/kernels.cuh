@@ -695,6 +695,7 @@ struct FgpArgs {
     int H, W;                                           // when tiles == nullptr
     int G, NTW;                                         // strips per CTA, threads per strip row (32 | NTW)
     float lam; int nfgp;
+    const float* lams;                                  // nullable: per-tile lambda (lambda sweep, NEXT-1)
     float* out; int out_pitch; long long out_tstride;   // MODE 0
     // FISTA epilogue (MODE 1)
     const float* xs; float* xprev; long long p_tstride; int T;
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
     // step sizes with the boundary masks folded in: gamma = 0 where the dual
     // component does not exist (p: rows >= Hv-1 or invalid column; q: column
     // >= Wv-1 or invalid row); a dual that starts at 0 with step 0 stays 0.
-    const float lam = A.lam;
+    const float lam = A.lams ? __ldg(A.lams + tile) : A.lam;
     const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
     const float gam = lam > 0.f ? 1.f / (16.f * lam) : 0.f;   // step 1/(8 lam) on p = 2p' - 1
     const float gq_col = (j < Wv - 1) ? gam : 0.f;
@@ -1131,7 +1132,7 @@ __global__ void __launch_bounds__(NW * 32, BSM ? 2 : 1) k_fgp2(FgpArgs A) {
         }
         if constexpr (BSM) row_st(bs + k * FGP2_ROW, lane, bv);
     }
-    const float lam = A.lam;
+    const float lam = A.lams ? __ldg(A.lams + tile) : A.lam;
     const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
     const float gam = lam > 0.f ? 1.f / (16.f * lam) : 0.f;
     // q step per column (0 where q does not exist: j >= W_v - 1)
@@ -1493,6 +1494,71 @@ __global__ void k_extract(int n, int T, int TP, TileT ti, const float* __restric
     const float v = valid ? img[(long long)(ti.row0 + i) * n + ti.col0 + j] : 0.f;
     t[(long long)i * TP + PADL + j] = v;
     tT[(long long)j * TP + PADL + i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Quality metrics inside the ROI (DESIGN.md
+// §11 reading M1): per image pair (x, g) of h x w,
+//   MSE  = mean (x - g)^2,
+//   SSIM = mean over the valid positions (window inside the image) of
+//          (2 mu_x mu_g + C1)(2 s_xg + C2) / ((mu_x^2 + mu_g^2 + C1)(s_x^2 + s_g^2 + C2))
+//   (Wang et al. 2004: 11 x 11 Gaussian window, sigma 1.5, normalised weights;
+//   C1 = (0.01 L)^2, C2 = (0.03 L)^2, L = max g - min g unless given).
+// One CTA per image; fp64 accumulation of the means.
+// ---------------------------------------------------------------------------
+__constant__ float c_ssim_w[121];
+
+__global__ void __launch_bounds__(256) k_metrics(int h, int w, const float* __restrict__ x, const float* __restrict__ g,
+                                                 float range, double* __restrict__ mse, double* __restrict__ ssim) {
+    __shared__ double red[256];
+    __shared__ float smin[256], smax[256];
+    const int img = blockIdx.x;
+    const float* xi = x + (long long)img * h * w;
+    const float* gi = g + (long long)img * h * w;
+    const int n = h * w;
+    double se = 0.0;
+    float lo = INFINITY, hi = -INFINITY;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const double d = (double)xi[e] - (double)gi[e];
+        se += d * d;
+        lo = fminf(lo, gi[e]); hi = fmaxf(hi, gi[e]);
+    }
+    red[threadIdx.x] = se; smin[threadIdx.x] = lo; smax[threadIdx.x] = hi;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            red[threadIdx.x] += red[threadIdx.x + s];
+            smin[threadIdx.x] = fminf(smin[threadIdx.x], smin[threadIdx.x + s]);
+            smax[threadIdx.x] = fmaxf(smax[threadIdx.x], smax[threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    const double L = range > 0.f ? (double)range : (double)smax[0] - (double)smin[0];
+    const double C1 = (0.01 * L) * (0.01 * L), C2 = (0.03 * L) * (0.03 * L);
+    if (threadIdx.x == 0) mse[img] = red[0] / n;
+    __syncthreads();
+    const int vh = h - 10, vw = w - 10;
+    double acc = 0.0;
+    for (int e = threadIdx.x; e < vh * vw; e += blockDim.x) {
+        const int i = e / vw, j = e - i * vw;
+        double mx = 0.0, mg = 0.0, xx = 0.0, gg = 0.0, xg = 0.0;
+        for (int a = 0; a < 11; ++a)
+            for (int b = 0; b < 11; ++b) {
+                const double wt = c_ssim_w[a * 11 + b];
+                const double xv = xi[(i + a) * w + j + b], gv = gi[(i + a) * w + j + b];
+                mx += wt * xv; mg += wt * gv;
+                xx += wt * xv * xv; gg += wt * gv * gv; xg += wt * xv * gv;
+            }
+        const double vx = xx - mx * mx, vg = gg - mg * mg, cxg = xg - mx * mg;
+        acc += (2.0 * mx * mg + C1) * (2.0 * cxg + C2) / ((mx * mx + mg * mg + C1) * (vx + vg + C2));
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ssim[img] = vh > 0 && vw > 0 ? red[0] / ((double)vh * vw) : 0.0;
 }
 
 // truncated data, edge-constant centred padding: one thread per output bin

@@ -95,6 +95,7 @@ struct lt_plan {
     int64_t ws_bytes = 0;
     bool bound = false, bank_ready = false, wd_ready = false;
     int last_mode = -1;
+    bool lam_array = false;       // tv solve with per-ROI lambda (lt_tv_solve_lambdas)
     int stitch_cap = 0;           // max list entries
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
@@ -108,7 +109,7 @@ struct lt_plan {
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
-        size_t xsblk[3], xsg[2];
+        size_t xsblk[3], xsg[2], lams;
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -453,6 +454,7 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
             A.b = v; A.b_pitch = p.T; A.b_tstride = p.ptile();
             A.tiles = p.P<TileT>(p.off.tiles) + t0;
             A.lam = lam; A.nfgp = nfgp;
+            A.lams = p.lam_array ? p.P<float>(p.off.lams) + t0 : nullptr;
             A.xs = xs; A.xprev = xprev; A.p_tstride = p.ptile(); A.T = p.T;
             A.y = y; A.yT = yT; A.y_tstride = yts; A.TP = p.TP;
             A.beta_o = (float)beta;
@@ -753,6 +755,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.v = take(R * ptile * fs); f.xs = take(R * ptile * fs); f.xprev = take(R * ptile * fs);
     for (int l = 0; l < 3; ++l) f.xsblk[l] = take(std::max<size_t>(p->xsblk[l].size(), 1) * 4);
     for (int l = 0; l < 2; ++l) f.xsg[l] = take((size_t)n * n * fs);
+    f.lams = take(R * fs);
     f.tt = take(ytile * fs); f.ttT = take(ytile * fs); f.tw = take((size_t)n_angles * p->Wwin * fs);
     f.st_off = take(((size_t)nb * nb + 1) * 4); f.st_lst = take((size_t)p->stitch_cap * 4);
     f.st_r0 = take((size_t)n_roi * std::max(1, world) * 4 + 4); f.st_c0 = take((size_t)n_roi * std::max(1, world) * 4 + 4);
@@ -1098,6 +1101,97 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
     A.lam = lambda; A.nfgp = n_fgp;
     A.out = d_out; A.out_pitch = w; A.out_tstride = (long long)h * w;
     return launch_fgp<0>(A, h, w, count, (cudaStream_t)stream);
+}
+
+int lt_tv_solve_lambdas(lt_plan* p, const float* d_sino, const float* h_lambdas, int32_t n_fgp, float* d_cores,
+                        void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || (p->R > 0 && (!d_cores || !h_lambdas))) return fail(LT_ERR_INVALID, "null pointer");
+    if (n_fgp < 1 || n_fgp > 4096) return fail(LT_ERR_INVALID, "1 <= n_fgp <= 4096 required");
+    for (int q = 0; q < p->R; ++q)
+        if (!(h_lambdas[q] >= 0.f)) return fail(LT_ERR_INVALID, "lambda[%d] must be >= 0", q);
+    FgpCfg fc;
+    if (int rc = fgp_config(p->T, p->T, n_fgp, &fc)) return rc;
+    if (p->R == 0) return LT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    LT_CUDA(cudaMemcpyAsync(p->P<float>(p->off.lams), h_lambdas, (size_t)p->R * sizeof(float), cudaMemcpyHostToDevice, st));
+    p->lam_array = true;
+    const int rc = solve(*p, 1, d_sino, 0.f, 0.f, n_fgp, d_cores, st);
+    p->lam_array = false;
+    return rc;
+}
+
+int lt_metrics(const float* d_x, const float* d_ref, int32_t count, int32_t h, int32_t w, float data_range,
+               double* d_mse, double* d_ssim, void* stream) {
+    if (count < 0 || h < 1 || w < 1) return fail(LT_ERR_INVALID, "count >= 0, h, w >= 1 required");
+    if (count == 0) return LT_OK;
+    if (!d_x || !d_ref || !d_mse || !d_ssim) return fail(LT_ERR_INVALID, "null pointer");
+    static bool have_w = false;
+    if (!have_w) {   // 11 x 11 Gaussian, sigma 1.5, normalised (fp64 on the host)
+        double wt[121], s = 0.0;
+        for (int a = 0; a < 11; ++a)
+            for (int b = 0; b < 11; ++b) { wt[a * 11 + b] = std::exp(-((a - 5) * (a - 5) + (b - 5) * (b - 5)) / (2.0 * 1.5 * 1.5)); s += wt[a * 11 + b]; }
+        float wf[121];
+        for (int e = 0; e < 121; ++e) wf[e] = (float)(wt[e] / s);
+        LT_CUDA(cudaMemcpyToSymbol(c_ssim_w, wf, sizeof wf));
+        have_w = true;
+    }
+    k_metrics<<<count, 256, 0, (cudaStream_t)stream>>>(h, w, d_x, d_ref, data_range, d_mse, d_ssim);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int lt_nelder_mead_1d(double (*f)(double, void*), void* ctx, double t_lo, double t_hi, int32_t budget,
+                      double* t_best, double* f_best, int32_t* n_eval) {
+    if (!f || !t_best || !f_best) return fail(LT_ERR_INVALID, "null pointer");
+    if (!(t_lo < t_hi) || budget < 3) return fail(LT_ERR_INVALID, "need t_lo < t_hi and budget >= 3");
+    // Nelder & Mead (1965) in one dimension, coefficients 1, 2, 1/2, 1/2; initial
+    // simplex {mid, mid + 0.5} (SPEC S:L499 reading); every point
+    // is clamped into [t_lo, t_hi]; the best evaluated point is returned.
+    int ne = 0;
+    double bx = 0.0, bf = INFINITY;
+    auto F = [&](double t) {
+        t = std::min(std::max(t, t_lo), t_hi);
+        const double v = f(t, ctx);
+        ++ne;
+        if (v < bf || ne == 1) { bf = v; bx = t; }
+        return v;
+    };
+    auto clampt = [&](double t) { return std::min(std::max(t, t_lo), t_hi); };
+    const double mid = 0.5 * (t_lo + t_hi);
+    double x0 = mid, x1 = clampt(mid + 0.5);
+    if (x1 == x0) x1 = clampt(mid - 0.5);
+    double f0 = F(x0), f1 = F(x1);
+    while (ne < budget) {
+        if (f1 < f0) { std::swap(x0, x1); std::swap(f0, f1); }      // x0 best, x1 worst
+        if (std::fabs(x1 - x0) < 1e-9) break;
+        const double xr = clampt(x0 + (x0 - x1));
+        const double fr = F(xr);
+        if (fr < f0) {
+            if (ne < budget) {
+                const double xe = clampt(x0 + 2.0 * (xr - x0));
+                const double fe = F(xe);
+                if (fe < fr) { x1 = xe; f1 = fe; } else { x1 = xr; f1 = fr; }
+            } else { x1 = xr; f1 = fr; }
+            continue;
+        }
+        if (ne >= budget) break;
+        if (fr < f1) {                                             // outside contraction
+            const double xc = clampt(x0 + 0.5 * (xr - x0));
+            const double fc = F(xc);
+            if (fc <= fr) { x1 = xc; f1 = fc; continue; }
+        } else {                                                   // inside contraction
+            const double xc = clampt(x0 + 0.5 * (x1 - x0));
+            const double fc = F(xc);
+            if (fc < f1) { x1 = xc; f1 = fc; continue; }
+        }
+        if (ne >= budget) break;
+        x1 = x0 + 0.5 * (x1 - x0);                                 // shrink towards the best point
+        f1 = F(x1);
+    }
+    *t_best = bx; *f_best = bf;
+    if (n_eval) *n_eval = ne;
+    return LT_OK;
 }
 
 int lt_pad_truncated(const float* d_in, int32_t n_angles, int32_t n_trunc, int32_t n_det, float* d_out,

@@ -30,7 +30,7 @@ import numpy as np
 __all__ = [
     "Shape", "Config", "CONFIGS", "config", "angles_for", "random_shapes",
     "analytic_sinogram", "raster", "add_noise", "roi_centres", "make_inputs",
-    "seeded_rng",
+    "seeded_rng", "sweep_lambdas",
 ]
 
 
@@ -93,7 +93,21 @@ CONFIGS = {
     # (extended side 256, the kernels' maximum).
     "T1": Config(6, "T1", 1024, 512, math.pi, 1449, "poisson", 1e4, 1, 96, 32,
                  "centre", 200, "tv", 0.05, 100, 25, 0, 257),
+    # SURVEY §8(f) NEXT-1, the lambda-sweep / parameter-estimation workload
+    # (PAPER.md L789-795, L1116-1120): C2's geometry and noise, 4 seeded ROIs
+    # each solved for 16 lambdas log-spaced in [1e-3, 1] in one batch (64
+    # ROI-lambda solves), scored by MSE and SSIM against the ground truth.
+    "L1": Config(7, "L1", 512, 64, math.pi, 725, "poisson", 1e4, 64, 32, 32,
+                 "sweep", 200, "tv", 0.05, 100, 16, 0),
 }
+
+SWEEP_ROIS, SWEEP_LAMBDAS = 4, 16
+
+
+def sweep_lambdas(cfg: "Config") -> np.ndarray:
+    """Per-ROI lambda of a "sweep" layout: 16 values log-spaced in [1e-3, 1],
+    repeated for each of the 4 ROI positions (ROI-major)."""
+    return np.tile(np.logspace(-3.0, 0.0, SWEEP_LAMBDAS), cfg.n_roi // SWEEP_LAMBDAS)
 
 
 def config(name: str) -> Config:
@@ -235,6 +249,10 @@ def roi_centres(cfg: Config) -> np.ndarray:
     if cfg.layout == "seeded":
         rng = seeded_rng(cfg.cfg_id, 2)
         return rng.integers(r, n - r + 1, size=(cfg.n_roi, 2)).astype(np.int32)
+    if cfg.layout == "sweep":
+        rng = seeded_rng(cfg.cfg_id, 2)
+        base = rng.integers(r + cfg.margin, n - r - cfg.margin + 1, size=(cfg.n_roi // SWEEP_LAMBDAS, 2))
+        return np.repeat(base, SWEEP_LAMBDAS, axis=0).astype(np.int32)
     if cfg.layout == "tiling":
         k = n // (2 * r)
         g = r + 2 * r * np.arange(k)

@@ -395,3 +395,64 @@ def test_exact_xs_local_parity(lt, orc, mode):
                               n_fgp=30, xs_exact=xs)
     for q in range(3):
         assert relerr(got[q], ref[q]) <= 1e-3, q
+
+
+# ------------------------------------------------------------------ NEXT-1: lambda sweep, metrics, Nelder-Mead
+
+@pytest.mark.parametrize("cnt,h,w,rng_L", [(5, 24, 24, None), (3, 64, 48, None), (2, 11, 11, 2.0), (2, 9, 30, None)])
+def test_metrics_parity(lt, orc, cnt, h, w, rng_L):
+    """lt_metrics (MSE, SSIM) against the oracle's explicit definitions, 1e-6 absolute."""
+    g = np.random.default_rng(h * w).random((cnt, h, w)).astype(np.float32)
+    x = (g + 0.08 * np.random.default_rng(cnt).standard_normal(g.shape)).astype(np.float32)
+    mse, ssim = lt.metrics(gpu(x), gpu(g), rng_L)
+    mse, ssim = cpu(mse), cpu(ssim)
+    for i in range(cnt):
+        assert abs(mse[i] - orc.mse(x[i], g[i])) <= 1e-6 * max(1.0, orc.mse(x[i], g[i]))
+        assert abs(ssim[i] - orc.ssim(x[i], g[i], rng_L)) <= 1e-6, (i, ssim[i])
+    same = cpu(lt.metrics(gpu(g), gpu(g))[1])
+    assert np.all(np.abs(same - (1.0 if h >= 11 and w >= 11 else 0.0)) < 1e-9)
+
+
+def test_lambda_sweep_matches_per_lambda_solves(lt, orc):
+    """One plan holding the same ROI with several lambdas (lt_tv_solve_lambdas)
+    equals the oracle's separate solves, and lambda = 0 gives the unregularized path."""
+    cfg = synth.Config(22, "sweep", 96, 24, math.pi, 137, "poisson", 1e4, 4, 14, 10, "centre", 8, "tv",
+                       0.05, 30, 6, 0)
+    inp = synth.make_inputs(cfg)
+    lams = [0.0, 0.01, 0.05, 0.3]
+    cen = np.repeat(np.array([[48, 40]], dtype=np.int32), len(lams), axis=0)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    got = cpu(plan.tv_solve(gpu(inp.sino), lams, cfg.n_fgp))
+    for q, lam in enumerate(lams):
+        ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen[:1], cfg.radius, cfg.margin,
+                           cfg.n_iter, mode="tv", lam=lam, n_fgp=cfg.n_fgp)
+        assert relerr(got[q], ref[0]) <= 1e-3, lam
+    single = cpu(plan.tv_solve(gpu(inp.sino), 0.05, cfg.n_fgp))
+    assert relerr(got[2], single[2]) <= 1e-6
+
+
+def test_optimize_lambda(lt, orc):
+    """Nelder-Mead over log10(lambda) driving GPU solves + metrics:
+    same trajectory as the oracle's Nelder-Mead on the same GPU objective, result
+    inside the bounds and no worse than the initial simplex."""
+    cfg = synth.Config(23, "tune", 64, 32, math.pi, 91, "poisson", 3e3, 1, 12, 8, "centre", 10, "tv",
+                       0.05, 30, 5, 0)
+    inp = synth.make_inputs(cfg)
+    truth = synth.raster(inp.shapes, cfg.n)
+    r0, c0 = 32 - 12, 32 - 12
+    ref_core = gpu(truth[r0:r0 + 24, c0:c0 + 24][None])
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    sino = gpu(inp.sino)
+    lam, val, n = plan.optimize_lambda(sino, ref_core, "mse", (-3.0, 0.0), budget=12, n_fgp=cfg.n_fgp)
+    assert 1e-3 <= lam <= 1.0 and n <= 12
+
+    def obj(t):
+        c = plan.tv_solve(sino, 10.0 ** t, cfg.n_fgp)
+        return float(lt.metrics(c, ref_core)[0].mean())
+    t_ref, v_ref, n_ref = orc.nelder_mead_1d(obj, -3.0, 0.0, 12)
+    assert abs(math.log10(lam) - t_ref) < 1e-12 and n == n_ref and abs(val - v_ref) <= 1e-9 * max(v_ref, 1e-30)
+    assert val <= min(obj(-1.5), obj(-1.0)) + 1e-12
+    lam_s, val_s, _ = plan.optimize_lambda(sino, ref_core, "ssim", (-3.0, 0.0), budget=8, n_fgp=cfg.n_fgp)
+    assert 1e-3 <= lam_s <= 1.0 and 0.0 < val_s <= 1.0

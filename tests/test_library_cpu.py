@@ -142,3 +142,25 @@ def test_workspace_size_reasonable(lt):
                    c.n_iter, bind=False)
     gb = plan.workspace_bytes / 2**30
     assert 5.0 < gb < 40.0, gb          # bank + conv cache (2 x 2.97 GB) + ROI state fit 180 GB
+
+
+@pytest.mark.parametrize("fn,lo,hi,budget", [
+    (lambda t: (t - 2.0) ** 2, -3.0, 4.0, 50),
+    (lambda t: (t - 2.0) ** 2, -3.0, 4.0, 3),
+    (lambda t: t, -3.0, 4.0, 40),
+    (lambda t: abs(math.sin(3.0 * t)) + 0.1 * t * t, -2.0, 1.0, 25),
+])
+def test_nelder_mead_matches_oracle(lt, orc, fn, lo, hi, budget):
+    """lt_nelder_mead_1d (host code of the library, NEXT-1) follows the same
+    deterministic trajectory as the oracle's independent implementation."""
+    a, b = [], []
+    got = lt.nelder_mead_1d(lambda t: a.append(t) or fn(t), lo, hi, budget)
+    ref = orc.nelder_mead_1d(lambda t: b.append(t) or fn(t), lo, hi, budget)
+    assert got == ref and a == b
+
+
+def test_nelder_mead_validation(lt):
+    with pytest.raises(ValueError):
+        lt.nelder_mead_1d(lambda t: t, 1.0, 1.0, 10)
+    with pytest.raises(ValueError):
+        lt.nelder_mead_1d(lambda t: t, 0.0, 1.0, 2)

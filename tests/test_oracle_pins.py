@@ -429,3 +429,60 @@ def test_pad_truncated_keeps_detector_coordinates(orc):
     trunc = synth.analytic_sinogram(shapes, ang, 31)
     assert np.allclose(trunc, full[:, 30:61], rtol=0, atol=1e-12)
     assert np.array_equal(orc.pad_truncated(trunc, 91)[:, 30:61], trunc)
+
+
+# ------------------------------------------------------------------ NEXT-1: metrics, Nelder-Mead
+
+def test_mse_pins(orc):
+    """MSE: a == b -> 0; [0,1] vs [1,1] -> 0.5; offset c -> c^2."""
+    a = np.random.default_rng(5).random((7, 9))
+    assert orc.mse(a, a) == 0.0
+    assert orc.mse(np.array([[0.0, 1.0]]), np.array([[1.0, 1.0]])) == 0.5
+    assert abs(orc.mse(a + 0.25, a) - 0.0625) < 1e-15
+
+
+def test_ssim_pins(orc):
+    """SSIM (Wang 2004, P:L786-788): ssim(a, a) = 1; symmetric for a fixed L;
+    constant images c1, c2 -> (2 c1 c2 + C1) / (c1^2 + c2^2 + C1)."""
+    rng = np.random.default_rng(6)
+    a = rng.random((24, 30)); b = a + 0.1 * rng.standard_normal(a.shape)
+    assert abs(orc.ssim(a, a) - 1.0) < 1e-12
+    assert abs(orc.ssim(a, b, data_range=1.0) - orc.ssim(b, a, data_range=1.0)) < 1e-12
+    c1, c2, L = 0.3, 0.7, 1.0
+    C1 = (0.01 * L) ** 2
+    got = orc.ssim(np.full((15, 15), c1), np.full((15, 15), c2), data_range=L)
+    assert abs(got - (2 * c1 * c2 + C1) / (c1 ** 2 + c2 ** 2 + C1)) < 1e-12
+    assert 0.0 < orc.ssim(b, a) < 1.0
+
+
+def test_ssim_matches_scipy_filtering(orc):
+    """Independent route: the same Wang-2004 statistics by scipy.ndimage Gaussian
+    correlation (library filtering, 'valid' positions) agree with the oracle's
+    explicit window sums."""
+    from scipy import ndimage
+    rng = np.random.default_rng(7)
+    g = np.clip(rng.random((26, 21)), 0, 1)
+    x = g + 0.05 * rng.standard_normal(g.shape)
+    w = orc.ssim_window()
+    def filt(im):
+        return ndimage.correlate(im, w, mode="constant")[5:-5, 5:-5]
+    mx, mg = filt(x), filt(g)
+    vx, vg, cxg = filt(x * x) - mx ** 2, filt(g * g) - mg ** 2, filt(x * g) - mx * mg
+    L = g.max() - g.min()
+    C1, C2 = (0.01 * L) ** 2, (0.03 * L) ** 2
+    ref = np.mean((2 * mx * mg + C1) * (2 * cxg + C2) / ((mx ** 2 + mg ** 2 + C1) * (vx + vg + C2)))
+    assert abs(orc.ssim(x, g) - ref) < 1e-12
+
+
+def test_nelder_mead_pins(orc):
+    """Nelder-Mead in one dimension: finds the minimum of
+    (t - 2)^2 within 50 evaluations, honours the budget exactly, never leaves the
+    bounds, and a monotone objective ends at the boundary."""
+    t, v, n = orc.nelder_mead_1d(lambda t: (t - 2.0) ** 2, -3.0, 4.0, 50)
+    assert abs(t - 2.0) < 1e-2 and n <= 50
+    calls = []
+    t, v, n = orc.nelder_mead_1d(lambda t: calls.append(t) or (t - 2.0) ** 2, -3.0, 4.0, 3)
+    assert n == 3 and len(calls) == 3
+    seen = []
+    t, v, n = orc.nelder_mead_1d(lambda t: seen.append(t) or t, -3.0, 4.0, 40)
+    assert all(-3.0 <= s <= 4.0 for s in seen) and t == -3.0
