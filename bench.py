@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prior", default="config", choices=["config", "haar"],
+                    help="haar: NEXT-2 Haar-wavelet l1 prior (FISTA, 4 levels, lambda 0.02) instead of the config's")
     ap.add_argument("--xs-exact", action="store_true",
                     help="NEXT-4(i): x_s^k from the global SIRT iterate instead of the filtered backprojection")
     return ap.parse_args()
@@ -135,6 +137,9 @@ def run_ours(args, cfg):
     inp = synth.make_inputs(cfg)
     n_iter = cfg.n_iter
     mode = "tv" if "tv" in cfg.solver else "sirt"
+    if args.prior == "haar":
+        mode = "haar"
+    HAAR_LAM, HAAR_LEVELS = 0.02, 4
     plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter, rank=rank, world=world,
                    xs_exact=args.xs_exact)
     rects, _, _ = plan.tables()
@@ -179,6 +184,8 @@ def run_ours(args, cfg):
             lt.pad_truncated(sino_in, cfg.n_det, out=sino)
         if mode == "tv":
             plan.tv_solve(sino, lam_arg, cfg.n_fgp, out=out)
+        elif mode == "haar":
+            plan.haar_solve(sino, HAAR_LAM, HAAR_LEVELS, out=out)
         else:
             plan.sirt_solve(sino, 0.0, math.inf, out=out)
         if sweep:
@@ -234,7 +241,7 @@ def run_ours(args, cfg):
             score_host[0].copy_(scores["mse"], non_blocking=True)
             score_host[1].copy_(scores["ssim"], non_blocking=True)
             torch.cuda.synchronize()
-    elif world == 1 and not trunc:
+    elif world == 1 and not trunc and mode != "haar":
         def e2e_step():
             plan.solve_host(mode, sino_host, cfg.lam if mode == "tv" else 0.0,
                             0.0 if mode == "tv" else math.inf, cfg.n_fgp, image_host)
@@ -283,7 +290,9 @@ def run_ours(args, cfg):
     avg_ms = dom_ms / max(dom_n, 1)
     local_upd_per_step = upd_local
     nA = cfg.n_angles * Ptot_local          # pixel-angle updates of one A or A^T over all local ROIs
-    if dom == "fgp":
+    if dom == "fgp" and mode == "haar":
+        work = 0.0         # the Haar prox is a few flops per pixel: not a roofline kernel
+    elif dom == "fgp":
         work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / max(dom_n, 1)
     elif dom == "fp":      # one W_{L'} y per iteration 2..n
         work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / max(dom_n, 1)
@@ -325,6 +334,7 @@ def run_ours(args, cfg):
                                f"{cfg.n_roi} ROIs r={cfg.radius} m={cfg.margin}, {mode}, n={n_iter}"
                                + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" and not sweep
                                   else f", n_fgp={cfg.n_fgp}" if mode == "tv" else "")
+                               + (f", Haar l1 lambda={HAAR_LAM}, levels={HAAR_LEVELS}, FISTA" if mode == "haar" else "")
                                + (f", truncated to {cfg.n_trunc} central bins" if cfg.n_trunc else "")
                                + (", x_s = global SIRT iterate (exact)" if args.xs_exact else "")
                                + (f", lambda sweep: {synth.SWEEP_ROIS} ROIs x {synth.SWEEP_LAMBDAS} lambdas in "

@@ -156,6 +156,17 @@ int lt_global_tv(lt_plan* plan, const float* d_sino, int32_t n_iter, float lambd
 int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda,
                  int32_t n_fgp, float* d_out, void* stream);
 
+/* Local reconstruction with the Haar-wavelet l1 prior (
+ * g(x) = ||Bx||_1 in a Haar basis; eq. sirtista, solved
+ * with FISTA as in the paper, or ISTA when momentum = 0): Alg. 3
+ * with the FGP replaced by x = B^{-1} P_lambda(B v), B the orthonormal 2D Haar
+ * transform with `levels` levels and P_lambda the symmetric soft threshold of
+ * every coefficient.  0 <= levels <= 5; every local ROI's
+ * extended rectangle (after clipping) must have both sides divisible by
+ * 2^levels, else error 2.  d_cores as lt_tv_solve. */
+int lt_haar_solve(lt_plan* plan, const float* d_sino, float lambda, int32_t levels, int32_t momentum,
+                  float* d_cores, void* stream);
+
 /* Lambda sweep (P:L789-795 tune lambda per reconstruction,
  * P:L1116-1120 "the same ... for many different parameter values"): the local
  * FISTA-TV solve of lt_tv_solve with lambda = h_lambdas[q] (host array, one

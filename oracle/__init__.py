@@ -154,6 +154,22 @@ def fgp(b: np.ndarray, lam: float, n_iter: int, return_duals: bool = False):
     return (x, P, Q) if return_duals else x
 
 
+def haar(x: np.ndarray, levels: int, inverse: bool = False) -> np.ndarray:
+    """Orthonormal 2D Haar, in-place layout (NEXT-2; "wavelet decomposition
+    operator B", Haar basis L764)."""
+    y = np.ascontiguousarray(_f64(x)).copy()
+    _chk(_L().or_haar(y.shape[0], y.shape[1], levels, int(inverse), _d(y)), "or_haar")
+    return y
+
+
+def haar_prox(v: np.ndarray, lam: float, levels: int) -> np.ndarray:
+    """B^{-1} P_lambda(B v) with the symmetric soft threshold (eq. sirtista, A15)."""
+    v = np.ascontiguousarray(_f64(v))
+    x = np.zeros_like(v)
+    _chk(_L().or_haar_prox(v.shape[0], v.shape[1], levels, _d(v), ctypes.c_double(lam), _d(x)), "or_haar_prox")
+    return x
+
+
 def roi_rects(n: int, centres, radius: int, margin: int) -> np.ndarray:
     """[R, 8] = core (r0, r1, c0, c1), extended (r0, r1, c0, c1)."""
     c = _i32(centres).reshape(-1, 2)
@@ -166,9 +182,10 @@ def local_solve(n: int, angles, n_det: int, bconv: np.ndarray, centres, radius: 
                 mode: str = "box", lo: float = 0.0, hi: float = np.inf, lam: float = 0.0,
                 n_fgp: int = 100, momentum: bool = True, disc_c: float = 0.0, use_disc: bool = False,
                 alpha: Optional[float] = None, xs_exact: Optional[np.ndarray] = None,
-                want_ext: bool = False):
-    """Alg. 2 (box) / Alg. 3 (TV) for every ROI.  Returns cores [R, 2r, 2r]
-    (and ext [R, 2h, 2h] when want_ext).  PAPER.md L613-620, L637-688."""
+                want_ext: bool = False, levels: int = 4):
+    """Alg. 2 (box) / Alg. 3 (TV; "haar": the Haar l1 prior, NEXT-2, `levels`
+    levels) for every ROI.  Returns cores [R, 2r, 2r] (and ext [R, 2h, 2h]
+    when want_ext).  PAPER.md L613-620, L637-688."""
     ang = _f64(angles)
     bconv = _f64(bconv)
     nk = bconv.shape[0]
@@ -181,8 +198,8 @@ def local_solve(n: int, angles, n_det: int, bconv: np.ndarray, centres, radius: 
     xe = _f64(xs_exact) if xs_exact is not None else None
     rc = _L().or_local_solve(n, len(ang), n_det, _d(ang), nk, ctypes.c_double(a), _d(bconv),
                              ctypes.c_double(disc_c), int(use_disc), R, _i(c), radius, margin,
-                             0 if mode == "box" else 1, ctypes.c_double(lo), ctypes.c_double(hi),
-                             ctypes.c_double(lam), n_fgp, int(momentum),
+                             {"box": 0, "tv": 1, "haar": 2}[mode], ctypes.c_double(lo), ctypes.c_double(hi),
+                             ctypes.c_double(lam), levels if mode == "haar" else n_fgp, int(momentum),
                              _d(xe) if xe is not None else None, _d(cores),
                              _d(ext) if ext is not None else None)
     _chk(rc, "or_local_solve")
@@ -243,7 +260,7 @@ def pad_truncated(p_t: np.ndarray, n_det: int) -> np.ndarray:
 def pipeline(p: np.ndarray, angles, n: int, centres, radius: int, margin: int, n_iter: int,
              mode: str = "box", lo: float = 0.0, hi: float = np.inf, lam: float = 0.0,
              n_fgp: int = 100, use_disc: bool = True, bank: Optional[np.ndarray] = None,
-             want_ext: bool = False):
+             want_ext: bool = False, levels: int = 4):
     """The whole local path for a set of ROIs: disc (a2) -> bank (a3) ->
     conv cache (a4) -> local iterations (a5-a8) -> cores (a9 crop)."""
     p = _f64(p)
@@ -256,7 +273,7 @@ def pipeline(p: np.ndarray, angles, n: int, centres, radius: int, margin: int, n
         bank = filter_bank(n, angles, n_det, n_iter)
     b = conv_cache(bank[:n_iter], pc)
     return local_solve(n, angles, n_det, b, centres, radius, margin, mode=mode, lo=lo, hi=hi,
-                       lam=lam, n_fgp=n_fgp, disc_c=c, use_disc=use_disc, want_ext=want_ext)
+                       lam=lam, n_fgp=n_fgp, disc_c=c, use_disc=use_disc, want_ext=want_ext, levels=levels)
 
 
 # --------------------------------------------------------------------------- NEXT-1: metrics, Nelder-Mead

@@ -340,6 +340,71 @@ int or_roi_rects(int n, int nroi, const int* centres, int radius, int margin, in
 }
 
 /* ---------------------------------------------------------------------------
+ * Haar wavelet prior.  B = the orthonormal 2D Haar
+ * decomposition with `levels` levels (the paper's "wavelet decomposition
+ * operator B", in a Haar basis), on an h x w image with
+ * 2^levels dividing h and w, stored in place: level l (stride
+ * s = 2^l) maps every 2x2 group of approximation samples (a b; c d) at
+ * (i, j), (i, j+s), (i+s, j), (i+s, j+s), i, j multiples of 2s, to
+ * ((a+b+c+d)/2, (a-b+c-d)/2, (a+b-c-d)/2, (a-b-c+d)/2).  Its inverse applies
+ * the same (self-inverse) 2x2 map from the coarsest level down.
+ * P_lambda: symmetric soft threshold of EVERY coefficient (g(x) = ||Bx||_1,
+ * P:L764; symmetric per reading A15 of the one-sided P:L409).
+ * ------------------------------------------------------------------------- */
+static void haar_level(int w, int s, int gi, int gj, double* x) {
+    double* a = x + (size_t)gi * w + gj;
+    double* b = a + s;
+    double* c = a + (size_t)s * w;
+    double* d = c + s;
+    const double A = *a, B = *b, C = *c, D = *d;
+    *a = 0.5 * (A + B + C + D);
+    *b = 0.5 * (A - B + C - D);
+    *c = 0.5 * (A + B - C - D);
+    *d = 0.5 * (A - B - C + D);
+}
+
+static void haar_fwd(int h, int w, int levels, double* x) {
+    for (int l = 0; l < levels; ++l) {
+        const int s = 1 << l;
+        for (int i = 0; i < h; i += 2 * s)
+            for (int j = 0; j < w; j += 2 * s) haar_level(w, s, i, j, x);
+    }
+}
+
+static void haar_inv(int h, int w, int levels, double* x) {
+    for (int l = levels - 1; l >= 0; --l) {
+        const int s = 1 << l;
+        for (int i = 0; i < h; i += 2 * s)
+            for (int j = 0; j < w; j += 2 * s) haar_level(w, s, i, j, x);
+    }
+}
+
+/* x = B^{-1} P_lambda(B v)  (eq. sirtista P:L400-401 applied to v = S(.)) */
+static void haar_prox(int h, int w, int levels, const double* v, double lam, double* x) {
+    const size_t P = (size_t)h * w;
+    memcpy(x, v, sizeof(double) * P);
+    haar_fwd(h, w, levels, x);
+    for (size_t e = 0; e < P; ++e) {
+        const double a = fabs(x[e]) - lam;
+        x[e] = a > 0.0 ? (x[e] > 0.0 ? a : -a) : 0.0;
+    }
+    haar_inv(h, w, levels, x);
+}
+
+int or_haar(int h, int w, int levels, int inverse, double* x) {
+    if (h < 1 || w < 1 || levels < 0 || (h % (1 << levels)) || (w % (1 << levels))) return OR_ERR_INVALID;
+    if (inverse) haar_inv(h, w, levels, x); else haar_fwd(h, w, levels, x);
+    return OR_OK;
+}
+
+int or_haar_prox(int h, int w, int levels, const double* v, double lam, double* x) {
+    if (h < 1 || w < 1 || levels < 0 || (h % (1 << levels)) || (w % (1 << levels)) || !(lam >= 0.0))
+        return OR_ERR_INVALID;
+    haar_prox(h, w, levels, v, lam, x);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * Local method for one ROI (eq. localmethod; Alg. 2 P:L637-652 with
  * the box correction d of P:L538-546; Alg. 3 P:L665-688 with the FISTA garbles
  * corrected per reading A12).  The prior acts only on the extended ROI L'
@@ -349,6 +414,8 @@ int or_roi_rects(int n, int nroi, const int* centres, int radius, int margin, in
  *   mode 1 (TV):   v = x_s + y - alpha M W^T W M y;  x = FGP(v);  t' = ...;
  *                  r = x + (t-1)/t' (x - x_prev);  y = r - x_s;  x_prev = x
  *                  (momentum = 0 -> r = x)
+ *   mode 2 (Haar): as mode 1 with x = B^{-1} P_lam(B v) (NEXT-2; the paper's
+ *                  FISTA for the l1 penalties); nfgp = levels
  * Output: x^n on the extended rect (ext_out, h_e x w_e, nullable) and cropped
  * to the core (core_out, 2r x 2r).
  * xs_exact (nullable): nk images N x N replacing x_s^k (pins P9/P10: exact
@@ -397,7 +464,8 @@ static void local_one(int n, int na, int nd, const double* ang, int nk, double a
                 y[e] = x[e] - xs[e];
             }
         } else {
-            fgp(H, Wd, v, lam, nfgp, x, NULL, NULL);                 /* Alg. 3 line 6 */
+            if (mode == 2) haar_prox(H, Wd, nfgp, v, lam, x);      /* Haar prior: nfgp = levels (NEXT-2) */
+            else fgp(H, Wd, v, lam, nfgp, x, NULL, NULL);          /* Alg. 3 line 6 */
             const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t)); /* A12 */
             const double beta = momentum ? (t - 1.0) / tn : 0.0;
             for (size_t e = 0; e < P; ++e) {
@@ -429,9 +497,15 @@ int or_local_solve(int n, int na, int nd, const double* ang, int nk, double alph
     if (check_geom(n, na, nd, ang) || nk < 1 || !(alpha > 0.0)) return OR_ERR_INVALID;
     if (mode == 0 && lo > hi) return OR_ERR_INVALID;
     if (mode == 1 && (lam < 0.0 || nfgp < 1)) return OR_ERR_INVALID;
+    if (mode == 2 && (lam < 0.0 || nfgp < 0)) return OR_ERR_INVALID;
     int* rects = (int*)malloc(sizeof(int) * 8 * (nroi > 0 ? nroi : 1));
     if (or_roi_rects(n, nroi, centres, radius, margin, rects)) { free(rects); return OR_ERR_INVALID; }
     const int side = 2 * radius, eside = 2 * (radius + margin);
+    if (mode == 2)
+        for (int r = 0; r < nroi; ++r) {
+            const int* rc = rects + 8 * r;
+            if ((rc[5] - rc[4]) % (1 << nfgp) || (rc[7] - rc[6]) % (1 << nfgp)) { free(rects); return OR_ERR_INVALID; }
+        }
     for (int r = 0; r < nroi; ++r) {
         const int* rc = rects + 8 * r;
         const int H = rc[5] - rc[4], Wd = rc[7] - rc[6];

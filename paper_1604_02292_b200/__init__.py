@@ -60,6 +60,7 @@ _SIGS = {
     "lt_fgp_batch": ([_I, _I, _I, _P, _F, _I, _P, _P], _I),
     "lt_pad_truncated": ([_P, _I, _I, _I, _P, _P], _I),
     "lt_tv_solve_lambdas": ([_P, _P, _P, _I, _P, _P], _I),
+    "lt_haar_solve": ([_P, _P, _F, _I, _I, _P, _P], _I),
     "lt_metrics": ([_P, _P, _I, _I, _I, _F, _P, _P, _P], _I),
     "lt_nelder_mead_1d": ([_P, _P, ctypes.c_double, ctypes.c_double, _I, _P, _P, _P], _I),
     "lt_launch_count": ([], _i64),
@@ -251,6 +252,16 @@ class Plan:
                 raise ValueError(f"{lams.size} lambdas for {self.R} local ROIs")
             _chk(_lib.lt_tv_solve_lambdas(self._p, sino.data_ptr(), lams.ctypes.data, n_fgp, out.data_ptr(),
                                           _stream(self.device)), "lt_tv_solve_lambdas")
+        return out
+
+    def haar_solve(self, sino: torch.Tensor, lam: float, levels: int = 4, momentum: bool = True,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Local reconstruction with the Haar-wavelet l1 prior (lt_haar_solve)."""
+        sino = _cuda_f32(sino, "sino")
+        side = 2 * self.radius
+        out = self._empty(self.R, side, side) if out is None else out
+        _chk(_lib.lt_haar_solve(self._p, sino.data_ptr(), float(lam), int(levels), int(bool(momentum)),
+                                out.data_ptr(), _stream(self.device)), "lt_haar_solve")
         return out
 
     def optimize_lambda(self, sino: torch.Tensor, ref_cores: torch.Tensor, target: str = "mse",

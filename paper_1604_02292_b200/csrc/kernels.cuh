@@ -1561,6 +1561,94 @@ __global__ void __launch_bounds__(256) k_metrics(int h, int w, const float* __re
     if (threadIdx.x == 0) ssim[img] = vh > 0 && vw > 0 ? red[0] / ((double)vh * vw) : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Haar-wavelet l1 prox + FISTA update (eq. sirtista
+// P:L397-409 with the paper's FISTA for the l1 penalties):
+//   x = B^{-1} P_lam(B v) on each tile's valid rectangle, then
+//   r = x + beta_o (x - x_prev), y = r - x_s, x_prev = x   (Alg. 3, A12).
+// B: orthonormal 2D Haar with `levels` <= 5 levels (2^levels divides the
+// valid sizes), in place: level l (stride s = 2^l) maps each 2x2 group of
+// approximation samples (a b; c d) to ((a+b+c+d), (a-b+c-d), (a+b-c-d),
+// (a-b-c+d)) / 2.  The transform is block-local (2^levels-pixel blocks), so a
+// CTA owns a 32 x 32 region in shared memory; every coefficient is soft
+// thresholded (symmetric, A15).  HBM-bound: reads v, x_s, x_prev, writes
+// x_prev, y, y^T once.
+// ---------------------------------------------------------------------------
+struct HaarArgs {
+    const float* v; const float* xs; float* xprev; long long p_tstride; int T;
+    float* y; float* yT; long long y_tstride; int TP;
+    const TileT* tiles;
+    float lam; int levels; float beta_o;
+};
+
+__global__ void __launch_bounds__(256) k_haar(HaarArgs A) {
+    __shared__ float sx[32][33];
+    const int tile = blockIdx.y;
+    const TileT ti = A.tiles[tile];
+    const int Hv = ti.vr1 - ti.vr0, Wv = ti.vc1 - ti.vc0;
+    const int nbx = (A.T + 31) / 32;
+    const int by = blockIdx.x / nbx, bx = blockIdx.x - by * nbx;
+    const int i0 = by * 32, j0 = bx * 32;              // region origin in valid-rect coordinates
+    if (i0 >= Hv || j0 >= Wv) return;
+    const long long pbase = (long long)tile * A.p_tstride;
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int e = threadIdx.x + 256 * u, i = e >> 5, j = e & 31;
+        const bool ok = i0 + i < Hv && j0 + j < Wv;
+        sx[i][j] = ok ? __ldcs(A.v + pbase + (long long)(ti.vr0 + i0 + i) * A.T + ti.vc0 + j0 + j) : 0.f;
+    }
+    __syncthreads();
+    auto level = [&](int s) {
+        const int ng = 32 / (2 * s);                        // groups per row of the region
+        for (int e = threadIdx.x; e < ng * ng; e += 256) {
+            const int gi = (e / ng) * 2 * s, gj = (e % ng) * 2 * s;
+            const float a = sx[gi][gj], b = sx[gi][gj + s], c = sx[gi + s][gj], d = sx[gi + s][gj + s];
+            sx[gi][gj] = 0.5f * (a + b + c + d);
+            sx[gi][gj + s] = 0.5f * (a - b + c - d);
+            sx[gi + s][gj] = 0.5f * (a + b - c - d);
+            sx[gi + s][gj + s] = 0.5f * (a - b - c + d);
+        }
+        __syncthreads();
+    };
+    for (int l = 0; l < A.levels; ++l) level(1 << l);
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+        const int i = e >> 5, j = e & 31;
+        const float c = sx[i][j], m = fabsf(c) - A.lam;
+        sx[i][j] = m > 0.f ? copysignf(m, c) : 0.f;
+    }
+    __syncthreads();
+    for (int l = A.levels - 1; l >= 0; --l) level(1 << l);
+    float xpv[4], xsv[4];                                             // all loads in flight first
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int e = threadIdx.x + 256 * u, i = e >> 5, j = e & 31;
+        const bool ok = i0 + i < Hv && j0 + j < Wv;
+        const long long pl = pbase + (long long)(ti.vr0 + i0 + i) * A.T + ti.vc0 + j0 + j;
+        xpv[u] = ok ? __ldcs(A.xprev + pl) : 0.f;
+        xsv[u] = ok ? __ldcs(A.xs + pl) : 0.f;
+    }
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int e = threadIdx.x + 256 * u, i = e >> 5, j = e & 31;
+        if (i0 + i >= Hv || j0 + j >= Wv) continue;
+        const int ti_ = ti.vr0 + i0 + i, tj = ti.vc0 + j0 + j;
+        const long long pl = pbase + (long long)ti_ * A.T + tj;
+        const float x = sx[i][j];
+        const float rr = x + A.beta_o * (x - xpv[u]);                 // FISTA extrapolation (A12)
+        const float yv = rr - xsv[u];                                 // x_L^k = r - x_s^k
+        A.xprev[pl] = x;
+        A.y[(long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + tj] = yv;
+        sx[i][j] = yv;                                                // own element: no race
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += 256) {                  // y^T through shared memory (coalesced)
+        const int j = e >> 5, i = e & 31;
+        if (i0 + i >= Hv || j0 + j >= Wv) continue;
+        const int ti_ = ti.vr0 + i0 + i, tj = ti.vc0 + j0 + j;
+        A.yT[(long long)tile * A.y_tstride + (long long)tj * A.TP + PADL + ti_] = sx[i][j];
+    }
+}
+
 // truncated data, edge-constant centred padding: one thread per output bin
 __global__ void k_pad_truncated(int na, int nt, int nd, const float* __restrict__ in, float* __restrict__ out) {
     const int d = blockIdx.x * blockDim.x + threadIdx.x, a = blockIdx.y;

@@ -96,6 +96,7 @@ struct lt_plan {
     bool bound = false, bank_ready = false, wd_ready = false;
     int last_mode = -1;
     bool lam_array = false;       // tv solve with per-ROI lambda (lt_tv_solve_lambdas)
+    bool haar_momentum = true;    // Haar solve: FISTA (true) or ISTA (false) update
     int stitch_cap = 0;           // max list entries
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
@@ -466,6 +467,16 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
             } else {
                 if (int rc = launch_fgp<1>(A, p.T, p.T, cnt, st)) return rc;
             }
+        } else if (mode == 2) {     // Haar l1 prox (NEXT-2), nfgp = levels
+            const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
+            const double beta = p.haar_momentum ? (tk - 1.0) / tn : 0.0;
+            tk = tn;
+            HaarArgs Hh{v, xs, xprev, p.ptile(), p.T, y, yT, yts, p.TP, p.P<TileT>(p.off.tiles) + t0,
+                        lam, nfgp, (float)beta};
+            const int nb = (p.T + 31) / 32;
+            ScopedTimer tm(TC_FGP, st);
+            k_haar<<<dim3(nb * nb, cnt), 256, 0, st>>>(Hh);
+            LT_LAUNCHED();
         }
     }
     if (fst && mode == 1) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));      // the group's stream ends after its last FGP
@@ -484,7 +495,7 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
     }
     LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.y), 0, (size_t)p.R * yts * sizeof(float), st));
     LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.yT), 0, (size_t)p.R * yts * sizeof(float), st));
-    if (mode == 1) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
+    if (mode != 0) LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.xprev), 0, (size_t)p.R * p.ptile() * sizeof(float), st));
     const int ng = (p.nsplit > 1 && p.R >= 2 && p.gst[0] && !exact) ? 2 : 1;
     if (ng == 1) {
         if (int rc = group_iterations(p, 0, 0, p.R, mode, lo, hi, lam, nfgp, d_sino, st)) return rc;
@@ -532,7 +543,7 @@ int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfg
     }
     if (!(p.flags & LT_XS_EXACT))
         if (int rc = conv_cache(p, pc, st)) return rc;
-    if (int rc = local_iterations(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode == 1 ? a0 : 0.f, nfgp,
+    if (int rc = local_iterations(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode != 0 ? a0 : 0.f, nfgp,
                                   d_sino, st))
         return rc;
     return crop_cores(p, d_cores, st);
@@ -1101,6 +1112,22 @@ int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float l
     A.lam = lambda; A.nfgp = n_fgp;
     A.out = d_out; A.out_pitch = w; A.out_tstride = (long long)h * w;
     return launch_fgp<0>(A, h, w, count, (cudaStream_t)stream);
+}
+
+int lt_haar_solve(lt_plan* p, const float* d_sino, float lambda, int32_t levels, int32_t momentum, float* d_cores,
+                  void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
+    if (!(lambda >= 0.f) || levels < 0 || levels > 5) return fail(LT_ERR_INVALID, "lambda >= 0 and 0 <= levels <= 5 required");
+    for (int q = 0; q < p->R; ++q) {
+        const TileT& t = p->tiles[q];
+        if ((t.vr1 - t.vr0) % (1 << levels) || (t.vc1 - t.vc0) % (1 << levels))
+            return fail(LT_ERR_INVALID, "ROI %d: extended rect %dx%d not divisible by 2^%d", p->local[q],
+                        t.vr1 - t.vr0, t.vc1 - t.vc0, levels);
+    }
+    if (p->R == 0) return LT_OK;
+    p->haar_momentum = momentum != 0;
+    return solve(*p, 2, d_sino, lambda, 0.f, levels, d_cores, (cudaStream_t)stream);
 }
 
 int lt_tv_solve_lambdas(lt_plan* p, const float* d_sino, const float* h_lambdas, int32_t n_fgp, float* d_cores,

@@ -456,3 +456,37 @@ def test_optimize_lambda(lt, orc):
     assert val <= min(obj(-1.5), obj(-1.0)) + 1e-12
     lam_s, val_s, _ = plan.optimize_lambda(sino, ref_core, "ssim", (-3.0, 0.0), budget=8, n_fgp=cfg.n_fgp)
     assert 1e-3 <= lam_s <= 1.0 and 0.0 < val_s <= 1.0
+
+
+# ------------------------------------------------------------------ NEXT-2: Haar l1 prior
+
+@pytest.mark.parametrize("momentum,levels", [(True, 4), (False, 3), (True, 0)])
+def test_haar_solve_parity(lt, orc, momentum, levels):
+    """Local Haar-l1 reconstruction (FISTA / ISTA) against the oracle, clipped and
+    interior ROIs whose extended sides are divisible by 2^levels."""
+    cfg = synth.Config(24, "haar", 96, 30, math.pi, 137, "poisson", 1e4, 3, 16, 16, "seeded", 10, "tv",
+                       0.05, 30, 6, 0)
+    inp = synth.make_inputs(cfg)
+    cen = np.array([[48, 48], [16, 64], [80, 32]], dtype=np.int32)   # extended sides 64, 48x64, 48x64
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    lam = 0.02
+    got = cpu(plan.haar_solve(gpu(inp.sino), lam, levels, momentum))
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, cfg.n_iter,
+                       mode="haar", lam=lam, levels=levels) if momentum else None
+    if not momentum:
+        pc, c, _, _ = orc.disc(inp.sino.astype(np.float64), inp.angles, cfg.n)
+        b = orc.conv_cache(orc.filter_bank(cfg.n, inp.angles, cfg.n_det, cfg.n_iter), pc)
+        ref = orc.local_solve(cfg.n, inp.angles, cfg.n_det, b, cen, cfg.radius, cfg.margin, mode="haar", lam=lam,
+                              levels=levels, momentum=False, disc_c=c, use_disc=True)
+    for q in range(3):
+        assert relerr(got[q], ref[q]) <= 1e-3, q
+
+
+def test_haar_solve_rejects_indivisible(lt):
+    inp = synth.make_inputs("C1")
+    plan = lt.Plan(64, inp.angles, 91, [[30, 30]], 12, 8, 5)      # extended side 40: not divisible by 16
+    plan.filter_bank()
+    with pytest.raises(ValueError):
+        plan.haar_solve(gpu(inp.sino), 0.01, 4)
+    plan.haar_solve(gpu(inp.sino), 0.01, 3)                      # 40 = 5 * 8

@@ -486,3 +486,58 @@ def test_nelder_mead_pins(orc):
     seen = []
     t, v, n = orc.nelder_mead_1d(lambda t: seen.append(t) or t, -3.0, 4.0, 40)
     assert all(-3.0 <= s <= 4.0 for s in seen) and t == -3.0
+
+
+# ------------------------------------------------------------------ NEXT-2: Haar l1 prior
+
+def test_haar_pins(orc):
+    """Orthonormal 2D Haar: inverse o forward = identity, Parseval,
+    a constant image has the single coefficient c 2^levels, one level on a 2x2
+    block is the closed-form orthonormal map, sizes must be divisible."""
+    rng = np.random.default_rng(41)
+    x = rng.standard_normal((32, 48))
+    for L in (1, 3, 4):
+        c = orc.haar(x, L)
+        assert np.allclose(orc.haar(c, L, inverse=True), x, rtol=0, atol=1e-12)
+        assert abs(np.linalg.norm(c) - np.linalg.norm(x)) < 1e-12
+    c = orc.haar(np.full((16, 16), 0.7), 4)
+    assert abs(c[0, 0] - 0.7 * 16) < 1e-12 and np.count_nonzero(np.abs(c) > 1e-12) == 1
+    a, b, cc, d = 1.0, 2.0, 3.0, 5.0
+    got = orc.haar(np.array([[a, b], [cc, d]]), 1)
+    assert np.allclose(got, 0.5 * np.array([[a + b + cc + d, a - b + cc - d], [a + b - cc - d, a - b - cc + d]]),
+                       rtol=0, atol=1e-15)
+    with pytest.raises(orc.OracleError):
+        orc.haar(np.zeros((12, 16)), 3)
+
+
+def test_haar_prox_pins(orc):
+    """P_lambda (symmetric reading A15): lambda = 0 is the
+    identity; the prox equals the closed-form minimiser of 1/2||x - v||^2 +
+    lambda ||Bx||_1 (componentwise in the orthonormal basis): checked by
+    optimality - no single-coefficient perturbation lowers the objective."""
+    rng = np.random.default_rng(42)
+    v = rng.standard_normal((16, 16))
+    assert np.allclose(orc.haar_prox(v, 0.0, 4), v, rtol=0, atol=1e-12)
+    lam = 0.3
+    x = orc.haar_prox(v, lam, 2)
+    def obj(z):
+        return 0.5 * np.sum((z - v) ** 2) + lam * np.sum(np.abs(orc.haar(z, 2)))
+    f0 = obj(x)
+    cx = orc.haar(x, 2)
+    for (i, j) in [(0, 0), (1, 3), (5, 7), (15, 15)]:
+        for eps in (1e-4, -1e-4):
+            c2 = cx.copy(); c2[i, j] += eps
+            assert obj(orc.haar(c2, 2, inverse=True)) >= f0 - 1e-12
+    assert np.all(np.abs(orc.haar(orc.haar_prox(v, 10.0, 2), 2)) == 0.0)   # lambda above every |coefficient|
+
+
+def test_local_haar_lambda0_equals_unregularized(orc):
+    """Haar prior with lambda = 0 is the identity prox: the local Haar-FISTA path
+    equals the local TV path with lambda = 0 (both plain FISTA on S)."""
+    n, nd, ang, p = _small_problem(n=24)
+    bank = orc.filter_bank(n, ang, nd, 6)
+    b = orc.conv_cache(bank, p)
+    cen = [[12, 12]]
+    a = orc.local_solve(n, ang, nd, b, cen, 4, 4, mode="haar", lam=0.0, levels=3)
+    t = orc.local_solve(n, ang, nd, b, cen, 4, 4, mode="tv", lam=0.0, n_fgp=10)
+    assert relerr(a, t) < 1e-13
