@@ -335,9 +335,9 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
         const float2 rm = __fadd2_rn(tt, make_float2(MAGICF, MAGICF));           // round(tt) in the low bits
         const float2 k2 = __ffma2_rn(rm, make_float2(-2.f, -2.f), make_float2(2.f * MAGICF, 2.f * MAGICF));   // -2 round(tt)
         const float2 g = __ffma2_rn(tt, make_float2(2.f, 2.f), k2);             // 2 (tt - round(tt)) in [-1, 1]
-        unsigned a0, a1;
-        asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(a0) : "r"(__float_as_int(rm.x)), "r"(rowbase));
-        asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(a1) : "r"(__float_as_int(rm.y)), "r"(rowbase));
+        // (shift + add: LEA on the ALU pipe, not IMAD on the FMA pipe)
+        const unsigned a0 = rowbase + ((unsigned)__float_as_int(rm.x) << 3);
+        const unsigned a1 = rowbase + ((unsigned)__float_as_int(rm.y) << 3);
         float s0, d0, s1, d1;
         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s0), "=f"(d0) : "r"(a0 + (unsigned)(i * FP2_P * 8)));
         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s1), "=f"(d1) : "r"(a1 + (unsigned)((i + 1) * FP2_P * 8)));
@@ -580,7 +580,8 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
                     float2 b0, b1;
                     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b0.x), "=f"(b0.y) : "r"(ad0));
                     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b1.x), "=f"(b1.y) : "r"(ad1));
-                    // hat weights of the left / right bin: sat(K' -/+ gg / c)
+                    // hat weights of the left / right bin: sat(K' -/+ gg / c) (FFMA.SAT, full-rate scalar FP32;
+                    // an FFMA2 + FMNMX form measured slower: FMNMX runs at half rate on the ALU pipe)
                     const float2 w0 = make_float2(__saturatef(fmaf(-gg.x, A4.w, A4.z)), __saturatef(fmaf(gg.x, A4.w, A4.z)));
                     const float2 w1 = make_float2(__saturatef(fmaf(-gg.y, A4.w, A4.z)), __saturatef(fmaf(gg.y, A4.w, A4.z)));
                     acc[h][p] = __ffma2_rn(w0, b0, acc[h][p]);
