@@ -1067,7 +1067,7 @@ struct Fgp2Smem {
 // so the kernel fits 128 registers and two CTAs (two tiles) share an SM: one
 // tile's halo latency is hidden behind the other tile's arithmetic.
 template <int MODE, int FR, int NW, int SYNC, bool BSM>
-__global__ void __launch_bounds__(NW * 32, BSM ? 2 : 1) k_fgp2(FgpArgs A) {
+__global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpArgs A) {
     using SM = Fgp2Smem<FR, NW>;
     extern __shared__ __align__(16) float sm[];
     cg::cluster_group cl = cg::this_cluster();

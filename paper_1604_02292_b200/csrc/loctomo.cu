@@ -330,10 +330,11 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
         static int cfgv = -1;
         if (cfgv < 0) {
             const char* e = getenv("LT_FGP2_CFG");
-            cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : 0;
+            cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : !strcmp(e, "2x16b") ? 3 : 0;
         }
         if (cfgv == 1) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
         if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
+        if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, 0, true>(A, rows, ntiles, st);
         return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
     }
     FgpCfg c;
