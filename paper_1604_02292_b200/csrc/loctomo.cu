@@ -663,25 +663,35 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         f.K = (float)(1.0 / c - 0.5 / (c * c)); f.A = (float)A; f.B = (float)B; f.col = col ? 1 : 0;
         p->angf[a] = f;
     }
-    // partition: longest-processing-time over valid extended pixel counts, ties by index
+    // partition: ROIs in raster order of their centres, cut into
+    // `world` contiguous runs of balanced cost, so each rank's ROIs are spatially
+    // compact (its global x_s backprojection covers only their neighbourhood).
+    // Cost model: the FGP cluster works on the full (2h)^2 tile, the projectors on
+    // the valid pixels: cost = 2 (2h)^2 + 3 * valid (measured ~40/60 split).
     std::vector<long long> cost(n_roi);
     for (int r = 0; r < n_roi; ++r) {
         const int cr = p->cen[2 * r], cc = p->cen[2 * r + 1], h = p->h;
         const long long hv = std::min(n, cr + h) - std::max(0, cr - h);
         const long long wv = std::min(n, cc + h) - std::max(0, cc - h);
-        cost[r] = hv * wv;
+        cost[r] = 2LL * (2 * h) * (2 * h) + 3LL * hv * wv;
     }
     std::vector<int> order(n_roi);
     for (int r = 0; r < n_roi; ++r) order[r] = r;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-    std::vector<long long> load(world, 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return p->cen[2 * a] != p->cen[2 * b] ? p->cen[2 * a] < p->cen[2 * b] : p->cen[2 * a + 1] < p->cen[2 * b + 1];
+    });
+    long long total = 0;
+    for (int r = 0; r < n_roi; ++r) total += cost[r];
     std::vector<int> owner(n_roi, 0);
-    for (int r : order) {
-        int best = 0;
-        for (int g = 1; g < world; ++g)
-            if (load[g] < load[best]) best = g;
-        owner[r] = best;
-        load[best] += cost[r];
+    {
+        long long cum = 0;
+        for (int r : order) {
+            // rank of the cost midpoint of this ROI: floor(world * (cum + cost/2) / total)
+            const long long mid2 = 2 * cum + cost[r];
+            int g = total > 0 ? (int)((long long)world * mid2 / (2 * total)) : 0;
+            owner[r] = std::min(std::max(g, 0), world - 1);
+            cum += cost[r];
+        }
     }
     for (int r = 0; r < n_roi; ++r)
         if (owner[r] == rank) p->local.push_back(r);

@@ -1,7 +1,7 @@
 """Multi-GPU combine plumbing: ROIs are partitioned by
 ``lt_roi_setup(rank, world)``; each rank solves its ROIs, the cores are
-all-gathered into fixed slots (``max_local`` per rank, ROI-index ordered
-within a rank) and every rank stitches the same image with ``lt_combine_rois``
+all-gathered into fixed slots (the largest local count of any rank, ROI-index
+ordered within a rank) and every rank stitches the same image with ``lt_combine_rois``
 (ascending global ROI order => bitwise identical for every world size).
 
 torch.distributed provides the collective (NCCL on GPUs; gloo works for the
@@ -15,9 +15,10 @@ import numpy as np
 import torch
 
 
-def max_local(n_roi: int, world: int) -> int:
-    """Slots per rank: the LPT partition gives every rank at most ceil(R / world) + 1 ROIs."""
-    return -(-n_roi // world) + (1 if world > 1 else 0)
+def slots_per_rank(local_lists: Sequence[Sequence[int]]) -> int:
+    """Slots per rank of the all-gather: the largest local ROI count (the
+    cost-balanced partition gives cheap clipped ROIs to some ranks, so counts differ)."""
+    return max(1, max(len(lst) for lst in local_lists))
 
 
 def slot_table(local_lists: Sequence[Sequence[int]], slots_per_rank: int) -> np.ndarray:
@@ -59,6 +60,6 @@ def setup_combine(plan, group=None) -> Tuple[int, np.ndarray]:
     """(slots_per_rank, slot -> global ROI table) for a plan of this rank."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    spr = max_local(len(plan.centres), world)
     lists = exchange_local_lists(plan.local_rois, group) if world > 1 else [list(plan.local_rois)]
+    spr = slots_per_rank(lists)
     return spr, slot_table(lists, spr)

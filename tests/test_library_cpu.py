@@ -121,19 +121,31 @@ def test_window_width_bruteforce():
             assert lo >= d0 and hi < d0 + W, (h, th, tau)
 
 
-def test_partition_covers_every_roi_once(lt):
-    c = synth.config("C4")
+@pytest.mark.parametrize("cfg_name", ["C2", "C4", "C5"])
+def test_partition_covers_every_roi_once(lt, cfg_name):
+    """Contiguous raster-order partition: every ROI on exactly one rank, local
+    lists ascending, cost balanced within one ROI's cost, ranks spatially compact
+    (for the C4/C5 tilings each rank's cores span at most ceil(rows/world) + 1 tile rows)."""
+    c = synth.config(cfg_name)
     cen = synth.roi_centres(c)
     ang = synth.angles_for(8)
+    h = c.radius + c.margin
+    def cost(r):
+        hv = min(c.n, cen[r, 0] + h) - max(0, cen[r, 0] - h)
+        wv = min(c.n, cen[r, 1] + h) - max(0, cen[r, 1] - h)
+        return 2 * (2 * h) ** 2 + 3 * hv * wv
     for world in (1, 2, 3, 4, 8):
-        seen = []
-        counts = []
+        seen, loads = [], []
         for rank in range(world):
             plan = lt.Plan(c.n, ang, c.n_det, cen, c.radius, c.margin, 1, rank=rank, world=world, bind=False)
             assert np.all(np.diff(plan.local_rois) > 0)
-            seen.extend(plan.local_rois.tolist()); counts.append(plan.R)
+            seen.extend(plan.local_rois.tolist())
+            loads.append(sum(cost(r) for r in plan.local_rois))
+            if c.layout == "tiling" and plan.R:
+                rows = np.unique(cen[plan.local_rois, 0])
+                assert len(rows) <= -(-(c.n // (2 * c.radius)) // world) + 1
         assert sorted(seen) == list(range(len(cen)))
-        assert max(counts) - min(counts) <= 2
+        assert max(loads) - sum(loads) / world <= max(cost(r) for r in range(len(cen)))
 
 
 def test_workspace_size_reasonable(lt):

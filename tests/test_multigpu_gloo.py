@@ -95,7 +95,7 @@ def test_slot_table_and_partition_balance():
             plan = lt.Plan(cfg.n, synth.angles_for(4), cfg.n_det, cen, cfg.radius, cfg.margin, 1,
                            rank=r, world=world, bind=False)
             lists.append(list(plan.local_rois))
-        spr = ltd.max_local(len(cen), world)
+        spr = ltd.slots_per_rank(lists)
         t = ltd.slot_table(lists, spr)
         assert sorted(t[t >= 0].tolist()) == list(range(len(cen)))
         assert max(len(l) for l in lists) <= spr
