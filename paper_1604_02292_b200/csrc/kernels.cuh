@@ -1403,6 +1403,41 @@ __global__ void __launch_bounds__(256) k_conv(int na, int nd, int nk, const floa
 }
 
 // ---------------------------------------------------------------------------
+// Convolution cache by FFT (same b_k as k_conv; the linear convolution of
+// rows zero-padded to L >= 2 N_d - 1 is the circular one of length L):
+//   k_padrows:  dst[r][0..L) = (src[r][0..nd), 0, ...)
+//   k_specmul:  S[kk][a][f] = U[k0+kk][a][f] * P[a][f]  (U already scaled by 1/L)
+//   k_croprows: b[k0+kk][a][d] = c[kk][a][d + d_c], d < N_d
+// ---------------------------------------------------------------------------
+__global__ void k_scale(long long n, float s, float* __restrict__ x) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) x[e] *= s;
+}
+
+__global__ void k_padrows(int nrows, int nd, int L, const float* __restrict__ src, float* __restrict__ dst) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (c >= L || r >= nrows) return;
+    dst[(long long)r * L + c] = c < nd ? src[(long long)r * nd + c] : 0.f;
+}
+
+__global__ void k_specmul(long long nk_rows_f, int na, int F, const float2* __restrict__ U, const float2* __restrict__ P,
+                          float2* __restrict__ S) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nk_rows_f) return;
+    const long long row = e / F;
+    const int f = (int)(e - row * F);
+    const int a = (int)(row % na);
+    const float2 u = U[e], q = P[(long long)a * F + f];
+    S[e] = make_float2(fmaf(u.x, q.x, -u.y * q.y), fmaf(u.x, q.y, u.y * q.x));
+}
+
+__global__ void k_croprows(int nrows, int nd, int L, int dc, const float* __restrict__ c, float* __restrict__ b) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (d >= nd || r >= nrows) return;
+    b[(long long)r * nd + d] = c[(long long)r * L + d + dc];
+}
+
+// ---------------------------------------------------------------------------
 // Small kernels: disc raster, zero-frequency sums, disc gray value, p_c,
 // image (un)packing, crop, extended-ROI export, stitch.
 // ---------------------------------------------------------------------------

@@ -4,6 +4,8 @@
 #include "loctomo.h"
 #include "kernels.cuh"
 
+#include <cufft.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -97,6 +99,12 @@ struct lt_plan {
     int last_mode = -1;
     bool lam_array = false;       // tv solve with per-ROI lambda (lt_tv_solve_lambdas)
     bool haar_momentum = true;    // Haar solve: FISTA (true) or ISTA (false) update
+    // convolution cache by FFT (cuFFT, library): length L >= 2 N_d - 1, k chunk,
+    // plans with their work area in the workspace, bank spectra U_k / L
+    int fftL = 0, fftF = 0, fft_kc = 0;
+    size_t fwork_bytes = 0;
+    cufftHandle plan_r2c_p = 0, plan_r2c_k = 0, plan_c2r_k = 0;
+    bool spec_ready = false;
     int stitch_cap = 0;           // max list entries
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
@@ -111,6 +119,7 @@ struct lt_plan {
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
         size_t xsblk[3], xsg[2], lams;
+        size_t uhat, phat, fspec, freal, fwork;
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -376,8 +385,102 @@ int disc_correct(lt_plan& p, const float* d_sino, float* d_pc, float* d_cuser, c
     return LT_OK;
 }
 
+#define LT_CUFFT(call)                                                                    \
+    do {                                                                                  \
+        cufftResult r_ = (call);                                                          \
+        if (r_ != CUFFT_SUCCESS) return fail(LT_ERR_RUNTIME, "%s: cufft error %d", #call, (int)r_); \
+    } while (0)
+
+// cuFFT plans (created on first use, work area inside the workspace)
+int fft_plans(lt_plan& p, cudaStream_t st) {
+    const int L = p.fftL, F = p.fftF;
+    int nL[1] = {L};
+    void* work = p.ws + p.off.fwork;
+    auto mk = [&](cufftHandle* h, cufftType type, int batch) -> int {
+        if (*h) return LT_OK;
+        size_t ws = 0;
+        LT_CUFFT(cufftCreate(h));
+        LT_CUFFT(cufftSetAutoAllocation(*h, 0));
+        if (type == CUFFT_R2C) LT_CUFFT(cufftMakePlanMany(*h, 1, nL, nullptr, 1, L, nullptr, 1, F, type, batch, &ws));
+        else LT_CUFFT(cufftMakePlanMany(*h, 1, nL, nullptr, 1, F, nullptr, 1, L, type, batch, &ws));
+        if (ws > p.fwork_bytes) return fail(LT_ERR_RUNTIME, "cufft needs %zu work bytes > %zu planned", ws, p.fwork_bytes);
+        return LT_OK;
+    };
+    if (int rc = mk(&p.plan_r2c_p, CUFFT_R2C, p.na)) return rc;
+    if (int rc = mk(&p.plan_r2c_k, CUFFT_R2C, p.fft_kc * p.na)) return rc;
+    if (int rc = mk(&p.plan_c2r_k, CUFFT_C2R, p.fft_kc * p.na)) return rc;
+    LT_CUFFT(cufftSetWorkArea(p.plan_r2c_p, work));    // (re-set every call: the workspace may be rebound)
+    LT_CUFFT(cufftSetWorkArea(p.plan_r2c_k, work));
+    LT_CUFFT(cufftSetWorkArea(p.plan_c2r_k, work));
+    LT_CUFFT(cufftSetStream(p.plan_r2c_p, st));
+    LT_CUFFT(cufftSetStream(p.plan_r2c_k, st));
+    LT_CUFFT(cufftSetStream(p.plan_c2r_k, st));
+    return LT_OK;
+}
+
+// bank spectra U_k / L (once per bank)
+int bank_spectra(lt_plan& p, cudaStream_t st) {
+    if (int rc = fft_plans(p, st)) return rc;
+    const int L = p.fftL, F = p.fftF, na = p.na, nd = p.nd;
+    const long long ns = (long long)na * nd;
+    float* real = p.P<float>(p.off.freal);
+    for (int k0 = 0; k0 < p.n_iter; k0 += p.fft_kc) {
+        const int kc = std::min(p.fft_kc, p.n_iter - k0);
+        k_padrows<<<dim3((L + 255) / 256, kc * na), 256, 0, st>>>(kc * na, nd, L, p.P<float>(p.off.bank) + k0 * ns, real);
+        LT_LAUNCHED();
+        if (kc < p.fft_kc)   // tail chunk: the plan's batch covers fft_kc rows-groups; clear the rest
+            LT_CUDA(cudaMemsetAsync(real + (size_t)kc * na * L, 0, (size_t)(p.fft_kc - kc) * na * L * sizeof(float), st));
+        float2* dst = p.P<float2>(p.off.uhat) + (size_t)k0 * na * F;
+        if (kc == p.fft_kc) {
+            LT_CUFFT(cufftExecR2C(p.plan_r2c_k, real, (cufftComplex*)dst));
+        } else {
+            float2* tmp = p.P<float2>(p.off.fspec);
+            LT_CUFFT(cufftExecR2C(p.plan_r2c_k, real, (cufftComplex*)tmp));
+            LT_CUDA(cudaMemcpyAsync(dst, tmp, (size_t)kc * na * F * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    // 1/L of the inverse transform folded into the spectra
+    const long long tot = (long long)p.n_iter * na * F * 2;
+    k_scale<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tot, 1.f / (float)L, p.P<float>(p.off.uhat));
+    LT_LAUNCHED();
+    p.spec_ready = true;
+    return LT_OK;
+}
+
+int conv_cache_direct(lt_plan& p, const float* d_pc, cudaStream_t st);
+
 int conv_cache(lt_plan& p, const float* d_pc, cudaStream_t st) {
     if (!p.bank_ready) return fail(LT_ERR_INVALID, "filter bank not computed (lt_filter_bank / lt_set_bank)");
+    static int direct = -1;
+    if (direct < 0) { const char* e = getenv("LT_CONV"); direct = (e && !strcmp(e, "direct")) ? 1 : 0; }
+    if (direct) return conv_cache_direct(p, d_pc, st);
+    ScopedTimer tm(TC_CONV, st);
+    if (!p.spec_ready)
+        if (int rc = bank_spectra(p, st)) return rc;
+    if (int rc = fft_plans(p, st)) return rc;
+    const int L = p.fftL, F = p.fftF, na = p.na, nd = p.nd;
+    float* real = p.P<float>(p.off.freal);
+    float2* spec = p.P<float2>(p.off.fspec);
+    float2* phat = p.P<float2>(p.off.phat);
+    k_padrows<<<dim3((L + 255) / 256, na), 256, 0, st>>>(na, nd, L, d_pc, real);
+    LT_LAUNCHED();
+    LT_CUFFT(cufftExecR2C(p.plan_r2c_p, real, (cufftComplex*)phat));
+    const long long ns = (long long)na * nd;
+    for (int k0 = 0; k0 < p.n_iter; k0 += p.fft_kc) {
+        const int kc = std::min(p.fft_kc, p.n_iter - k0);
+        const long long ne = (long long)kc * na * F;
+        k_specmul<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(ne, na, F, p.P<float2>(p.off.uhat) + (size_t)k0 * na * F,
+                                                               phat, spec);
+        LT_LAUNCHED();
+        LT_CUFFT(cufftExecC2R(p.plan_c2r_k, (cufftComplex*)spec, real));
+        k_croprows<<<dim3((nd + 255) / 256, kc * na), 256, 0, st>>>(kc * na, nd, L, (nd - 1) / 2, real,
+                                                                   p.P<float>(p.off.conv) + k0 * ns);
+        LT_LAUNCHED();
+    }
+    return LT_OK;
+}
+
+int conv_cache_direct(lt_plan& p, const float* d_pc, cudaStream_t st) {
     dim3 grid((p.nd + CV_DB - 1) / CV_DB, p.na, (p.n_iter + CV_KB - 1) / CV_KB);
     ScopedTimer tm(TC_CONV, st);
     k_conv<<<grid, 256, 0, st>>>(p.na, p.nd, p.n_iter, p.P<float>(p.off.bank), d_pc, p.P<float>(p.off.conv));
@@ -778,6 +881,25 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     for (int l = 0; l < 3; ++l) f.xsblk[l] = take(std::max<size_t>(p->xsblk[l].size(), 1) * 4);
     for (int l = 0; l < 2; ++l) f.xsg[l] = take((size_t)n * n * fs);
     f.lams = take(R * fs);
+    {   // FFT convolution cache: L = smallest power of two >= 2 N_d - 1
+        int L = 1;
+        while (L < 2 * n_det - 1) L <<= 1;
+        p->fftL = L; p->fftF = L / 2 + 1;
+        p->fft_kc = std::max(1, std::min(n_iter, (int)((size_t)(256u << 20) / ((size_t)n_angles * L * 4))));
+        const size_t F = p->fftF;
+        f.uhat = take((size_t)n_iter * n_angles * F * 8);
+        f.phat = take((size_t)n_angles * F * 8);
+        f.fspec = take((size_t)p->fft_kc * n_angles * F * 8);
+        f.freal = take((size_t)p->fft_kc * n_angles * L * fs);
+        // cuFFT work area: host-side estimate (no device work at setup)
+        size_t w1 = 0, w2 = 0, w3 = 0;
+        int nL[1] = {L};
+        cufftEstimateMany(1, nL, nullptr, 1, L, nullptr, 1, (int)F, CUFFT_R2C, n_angles, &w1);
+        cufftEstimateMany(1, nL, nullptr, 1, L, nullptr, 1, (int)F, CUFFT_R2C, p->fft_kc * n_angles, &w2);
+        cufftEstimateMany(1, nL, nullptr, 1, (int)F, nullptr, 1, L, CUFFT_C2R, p->fft_kc * n_angles, &w3);
+        p->fwork_bytes = std::max(std::max(w1, w2), w3) + (1u << 20);
+        f.fwork = take(p->fwork_bytes);
+    }
     f.tt = take(ytile * fs); f.ttT = take(ytile * fs); f.tw = take((size_t)n_angles * p->Wwin * fs);
     f.st_off = take(((size_t)nb * nb + 1) * 4); f.st_lst = take((size_t)p->stitch_cap * 4);
     f.st_r0 = take((size_t)n_roi * std::max(1, world) * 4 + 4); f.st_c0 = take((size_t)n_roi * std::max(1, world) * 4 + 4);
@@ -833,7 +955,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
         for (int g = 0; g < 3; ++g) LT_CUDA(cudaEventCreateWithFlags(&p->gev[g], cudaEventDisableTiming));
     }
     p->bound = true;
-    p->bank_ready = p->wd_ready = false;
+    p->bank_ready = p->wd_ready = p->spec_ready = false;
     return LT_OK;
 }
 
@@ -887,6 +1009,7 @@ int lt_filter_bank(lt_plan* p, void* stream) {
         }
     }
     p->bank_ready = true;
+    p->spec_ready = false;
     return LT_OK;
 }
 
@@ -896,6 +1019,7 @@ int lt_set_bank(lt_plan* p, const float* d_bank, void* stream) {
     LT_CUDA(cudaMemcpyAsync(p->ws + p->off.bank, d_bank, (size_t)p->n_iter * p->na * p->nd * sizeof(float),
                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     p->bank_ready = true;
+    p->spec_ready = false;
     return LT_OK;
 }
 
@@ -1253,6 +1377,9 @@ void lt_plan_destroy(lt_plan* p) {
     }
     for (int g = 0; g < 3; ++g)
         if (p->gev[g]) cudaEventDestroy(p->gev[g]);
+    if (p->plan_r2c_p) cufftDestroy(p->plan_r2c_p);
+    if (p->plan_r2c_k) cufftDestroy(p->plan_r2c_k);
+    if (p->plan_c2r_k) cufftDestroy(p->plan_c2r_k);
     delete p;
 }
 
