@@ -526,36 +526,57 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     for (int h = 0; h < 2; ++h)
         #pragma unroll
         for (int p = 0; p < BP_PR; ++p) acc[h][p] = make_float2(0.f, 0.f);
+    // Staging, software-pipelined: the next chunk's window bins are loaded into
+    // registers (warp = angle row, BP_CA / 8 rows per warp) while the current
+    // chunk is gathered, then written as pairs between two barriers.
+    constexpr int RPW = BP_CA / 8, NV = BP_SW / 32 + 1;
+    float pv[RPW][NV];
+    auto window_start = [&](int a, double& tc) {
+        tc = t.tauc[r * na + a] + dxc * g.cs64[a] - dyc * g.sn64[a];
+        return (int)floor(tc) - BP_SW / 2;                       // window bins sub0 .. sub0 + BP_SW
+    };
+    auto prefetch = [&](int a0n) {
+        const int can = min(BP_CA, na - a0n);
+        #pragma unroll
+        for (int qq = 0; qq < RPW; ++qq) {
+            const int q = wq + 8 * qq, a = a0n + q;
+            double tc;
+            const int sub0 = q < can ? window_start(a, tc) : 0;
+            const int off = q < can ? (s1.use_d0 ? __ldg(t.d0 + r * na + a) : 0) + sub0 : 0;
+            const float* rowp = s1.base + (long long)r * s1.tile_stride + (long long)(q < can ? a : 0) * s1.row_stride;
+            #pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int idx = off + lane + 32 * u;
+                pv[qq][u] = (q < can && idx >= 0 && idx < s1.len && lane + 32 * u <= BP_SW) ? __ldg(rowp + idx) : 0.f;
+            }
+        }
+    };
+    if (NS > 0) prefetch(0);
     for (int a0 = 0; a0 < (NS > 0 ? na : 0); a0 += BP_CA) {
         const int ca = min(BP_CA, na - a0);
         __syncthreads();
-        // one warp per angle row: anchors, then the BP_SW + 1 bins of the window as pairs
-        for (int q = wq; q < ca; q += 8) {
+        #pragma unroll
+        for (int qq = 0; qq < RPW; ++qq) {
+            const int q = wq + 8 * qq;
+            if (q >= ca) continue;
             const int a = a0 + q;
-            const double tc = t.tauc[r * na + a] + dxc * g.cs64[a] - dyc * g.sn64[a];
-            const int sub0 = (int)floor(tc) - BP_SW / 2;          // window bins sub0 .. sub0 + BP_SW
+            double tc;
+            const int sub0 = window_start(a, tc);
             const AngF an = g.ang[a];
             if (lane == 0) {
                 sanch[q] = (float)(tc - (double)(sub0 + BP_SW / 2)) - 0.5f;
                 sa[q] = make_float4(an.cs, an.sn, 1.f - 0.5f * an.invc, an.invc);
             }
-            const int off = (s1.use_d0 ? __ldg(t.d0 + r * na + a) : 0) + sub0;
-            const float* rowp = s1.base + (long long)r * s1.tile_stride + (long long)a * s1.row_stride;
-            float v[BP_SW / 32 + 1];
-            #pragma unroll
-            for (int u = 0; u <= BP_SW / 32; ++u) {
-                const int idx = off + lane + 32 * u;
-                v[u] = (idx >= 0 && idx < s1.len && lane + 32 * u <= BP_SW) ? __ldg(rowp + idx) * an.invc : 0.f;
-            }
             #pragma unroll
             for (int u = 0; u < BP_SW / 32; ++u) {
-                float nx = __shfl_down_sync(0xffffffffu, v[u], 1);
-                const float nx0 = __shfl_sync(0xffffffffu, v[u + 1], 0);
+                float nx = __shfl_down_sync(0xffffffffu, pv[qq][u], 1);
+                const float nx0 = __shfl_sync(0xffffffffu, pv[qq][u + 1], 0);
                 if (lane == 31) nx = nx0;
-                sw[q][lane + 32 * u] = make_float2(v[u], nx);
+                sw[q][lane + 32 * u] = make_float2(pv[qq][u] * an.invc, nx * an.invc);
             }
         }
         __syncthreads();
+        if (a0 + BP_CA < na) prefetch(a0 + BP_CA);
         // entry of bin m (relative to the window centre) at swbase + 8 (m + MAGIC bits)
         const unsigned swbase = opaque_u32((unsigned)__cvta_generic_to_shared(&sw[0][BP_SW / 2]) - 8u * (unsigned)MAGICI);
         #pragma unroll 1
