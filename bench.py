@@ -120,6 +120,33 @@ FGP_FLOPS_PER_PX_IT = 21.0      # z (5) + two dual steps with clip (10) + moment
 JOSEPH_FLOPS_PER_UPDATE = 8.0   # hat weight (2 FMA-equivalents) + 2 taps x FMA, per pixel-angle
 
 
+HAAR_LAM, HAAR_LEVELS = 0.02, 4
+
+
+def solve_mode(cfg, args) -> str:
+    if args.prior == "haar":
+        return "haar"
+    return "tv" if "tv" in cfg.solver else "sirt"
+
+
+def config_dict(cfg, args, world: int) -> dict:
+    """The workload description both arms print (same metric, unit, config)."""
+    mode = solve_mode(cfg, args)
+    sweep = cfg.layout == "sweep"
+    return {"workload": f"{cfg.name}: {cfg.n}x{cfg.n}, {cfg.n_angles} angles, {cfg.n_det} det, "
+                        f"{cfg.n_roi} ROIs r={cfg.radius} m={cfg.margin}, {mode}, n={cfg.n_iter}"
+                        + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" and not sweep
+                           else f", n_fgp={cfg.n_fgp}" if mode == "tv" else "")
+                        + (f", Haar l1 lambda={HAAR_LAM}, levels={HAAR_LEVELS}, FISTA" if mode == "haar" else "")
+                        + (f", truncated to {cfg.n_trunc} central bins" if cfg.n_trunc else "")
+                        + (", x_s = global SIRT iterate (exact)" if args.xs_exact else "")
+                        + (f", lambda sweep: {synth.SWEEP_ROIS} ROIs x {synth.SWEEP_LAMBDAS} lambdas in "
+                           "[1e-3, 1], MSE+SSIM vs ground truth" if sweep else ""),
+            "global_batch_rois": cfg.n_roi, "parallelism": f"roi-shard x{world}",
+            "l2": "inputs larger than L2 (conv cache 417 MB + ROI state), no flush",
+            "bank": "warm (per-geometry precompute, excluded)"}
+
+
 def run_ours(args, cfg):
     import torch
     import paper_1604_02292_b200 as lt
@@ -136,10 +163,7 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     inp = synth.make_inputs(cfg)
     n_iter = cfg.n_iter
-    mode = "tv" if "tv" in cfg.solver else "sirt"
-    if args.prior == "haar":
-        mode = "haar"
-    HAAR_LAM, HAAR_LEVELS = 0.02, 4
+    mode = solve_mode(cfg, args)
     plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter, rank=rank, world=world,
                    xs_exact=args.xs_exact)
     rects, _, _ = plan.tables()
@@ -325,23 +349,12 @@ def run_ours(args, cfg):
               for k, v in ktimes.items()}
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, budget_s=20.0)
+        cpu = cpu_baseline(cfg, budget_s=20.0, mode=mode)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.n}, {cfg.n_angles} angles, {cfg.n_det} det, "
-                               f"{cfg.n_roi} ROIs r={cfg.radius} m={cfg.margin}, {mode}, n={n_iter}"
-                               + (f", lambda={cfg.lam}, n_fgp={cfg.n_fgp}" if mode == "tv" and not sweep
-                                  else f", n_fgp={cfg.n_fgp}" if mode == "tv" else "")
-                               + (f", Haar l1 lambda={HAAR_LAM}, levels={HAAR_LEVELS}, FISTA" if mode == "haar" else "")
-                               + (f", truncated to {cfg.n_trunc} central bins" if cfg.n_trunc else "")
-                               + (", x_s = global SIRT iterate (exact)" if args.xs_exact else "")
-                               + (f", lambda sweep: {synth.SWEEP_ROIS} ROIs x {synth.SWEEP_LAMBDAS} lambdas in "
-                                  "[1e-3, 1], MSE+SSIM vs ground truth" if sweep else ""),
-                   "global_batch_rois": cfg.n_roi, "parallelism": f"roi-shard x{world}",
-                   "l2": "inputs larger than L2 (conv cache 417 MB + ROI state), no flush",
-                   "bank": "warm (per-geometry precompute, excluded)"},
+        "config": config_dict(cfg, args, world),
         "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
         "fgp_gpix_it_s": round(fgp_pi / (ms_per_step / 1e3) / 1e9, 2),
         "bank_ms": round(bank_ms, 2),
@@ -363,7 +376,7 @@ def run_ours(args, cfg):
 
 
 # --------------------------------------------------------------------------- oracle (CPU)
-def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None):
+def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None, mode=None):
     """Time the fp64 oracle on a bounded sample of the same workload and
     extrapolate to the full step: disc (whole) + conv cache (n_conv_k of n
     filters, scaled) + one ROI for n_iter_sample of n iterations (scaled, x R)."""
@@ -381,10 +394,11 @@ def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None):
     t_conv = (time.perf_counter() - t0) * cfg.n_iter / n_conv_k
     g = cfg.n_roi // 2 + cfg.n_roi // 32 if roi_index is None else roi_index
     bconv = rng.standard_normal((n_iter_sample, cfg.n_angles, cfg.n_det)) * 1e-3
-    mode = "tv" if "tv" in cfg.solver else "box"
+    mode = {"sirt": "box", "tv": "tv", "haar": "haar", None: "tv" if "tv" in cfg.solver else "box"}[mode]
     t0 = time.perf_counter()
     oracle.local_solve(n, inp.angles, cfg.n_det, bconv, inp.centres[g:g + 1], cfg.radius, cfg.margin, mode=mode,
-                       lam=cfg.lam, n_fgp=cfg.n_fgp, disc_c=c, use_disc=True)
+                       lam=HAAR_LAM if mode == "haar" else cfg.lam, n_fgp=cfg.n_fgp, disc_c=c, use_disc=True,
+                       levels=HAAR_LEVELS)
     t_roi = (time.perf_counter() - t0) * cfg.n_iter / n_iter_sample
     total = t_disc + t_conv + t_roi * cfg.n_roi
     sample = (f"disc (full) + conv cache {n_conv_k}/{cfg.n_iter} filters (x{cfg.n_iter / n_conv_k:g}) + ROI #{g} "
@@ -393,9 +407,9 @@ def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None):
     return cfg.n_roi / total, sample, oracle.get_threads()
 
 
-def cpu_baseline(cfg, budget_s=20.0):
+def cpu_baseline(cfg, budget_s=20.0, mode=None):
     try:
-        v, sample, cores = oracle_sample(cfg)
+        v, sample, cores = oracle_sample(cfg, mode=mode)
         return {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
     except Exception as e:  # report, never fake
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
@@ -407,19 +421,20 @@ def run_reference(args, cfg):
         return None
     import oracle
     for _ in range(args.warmup):
-        oracle_sample(cfg, n_iter_sample=2, n_conv_k=1)
+        oracle_sample(cfg, n_iter_sample=2, n_conv_k=1, mode=solve_mode(cfg, args))
     vals = []
     t0 = time.perf_counter()
     sample = ""
     for _ in range(args.steps):
-        v, sample, cores = oracle_sample(cfg, n_iter_sample=2, n_conv_k=1)
+        v, sample, cores = oracle_sample(cfg, n_iter_sample=2, n_conv_k=1, mode=solve_mode(cfg, args))
         vals.append(v)
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
     line = {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(cfg.n_roi / value * 1e3, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{cfg.name} (fp64 CPU oracle, extrapolated from a bounded sample)"},
+            "config": dict(config_dict(cfg, args, 1),
+                           reference="fp64 CPU oracle (the paper has no code), extrapolated from a bounded sample"),
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
