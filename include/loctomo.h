@@ -150,6 +150,16 @@ int lt_global_sirt(lt_plan* plan, const float* d_sino, int32_t n_iter, float lo,
 int lt_global_tv(lt_plan* plan, const float* d_sino, int32_t n_iter, float lambda, int32_t n_fgp,
                  float* d_img, void* stream);
 
+/* Chambolle-Pock primal-dual TV solver with diagonal (row / column sum)
+ * preconditioning on the full grid (the north
+ * star's literal "TV-regularized primal-dual solver"; P:L351-353 names
+ * primal-dual methods; global only, since it is not a "SIRT step +
+ * correction" method): minimises 1/2 ||W x - p||^2 +
+ * mu ||grad x||_1 (anisotropic, Neumann; mu = lambda / alpha gives the
+ * objective of lt_global_tv, reading A14), from x = 0, n_iter iterations.
+ * d_img: N x N.  Errors (2): n_iter < 1, mu < 0 or NaN, null pointers. */
+int lt_global_cp(lt_plan* plan, const float* d_sino, int32_t n_iter, float mu, float* d_img, void* stream);
+
 /* FGP TV prox (Beck & Teboulle) on `count` independent h x w
  * images (d_in/d_out: count x h x w), same kernel the TV solve uses
  * (h, w <= 256). */

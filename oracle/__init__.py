@@ -230,6 +230,16 @@ def global_tv(p: np.ndarray, angles, n: int, n_iter: int, lam: float, n_fgp: int
     return x
 
 
+def global_cp(p: np.ndarray, angles, n: int, n_iter: int, mu: float) -> np.ndarray:
+    """Chambolle-Pock TV with diagonal (row / column sum) preconditioning on the
+    full grid, minimising 1/2||Wx - p||^2 + mu ||grad x||_1 (NEXT-4(iii))."""
+    p = _f64(p); ang = _f64(angles)
+    x = np.zeros((n, n))
+    _chk(_L().or_global_cp(n, len(ang), p.shape[1], _d(ang), _d(p), n_iter, ctypes.c_double(mu), _d(x)),
+         "or_global_cp")
+    return x
+
+
 def stitch(n: int, centres, radius: int, cores: np.ndarray) -> np.ndarray:
     """Mean over covering cores, ascending ROI order (A19)."""
     c = _i32(centres).reshape(-1, 2)

@@ -584,6 +584,74 @@ int or_global_tv(int n, int na, int nd, const double* ang, const double* p, int 
 }
 
 /* ---------------------------------------------------------------------------
+ * Chambolle-Pock primal-dual TV solver with diagonal preconditioning (SURVEY
+ * §8(f) NEXT-4(iii): the north star's literal "TV-regularized primal-dual
+ * solver ... row and column normalisation"; Chambolle & Pock 2011 and Pock &
+ * Chambolle 2011, alpha = 1; the paper names primal-dual methods at P:L351-353
+ * and sets them aside because they are not "SIRT step + correction" methods,
+ * P:L371-381, so this is a GLOBAL solver only).  It minimises the same
+ * objective as the FISTA-TV reading A14:
+ *     F(x) = 1/2 ||W x - p||^2 + mu ||grad x||_1,   mu = lam / alpha,
+ * anisotropic forward differences with Neumann boundary (A13), no constraint.
+ * K = [W; grad]; Sigma = 1 / row sums of |K| (rays: sum_j W_ij = W 1; TV
+ * duals: 1/2), T = 1 / column sums (W^T 1 + number of difference terms that
+ * touch the pixel).  From x = xbar = 0, yd = 0, (yp, yq) = 0:
+ *     yd <- (yd + sd (W xbar - p)) / (1 + sd)           prox of (1/2||.-p||^2)*
+ *     (yp, yq) <- clip_[-mu, mu]((yp, yq) + 1/2 grad xbar)
+ *     x' <- x - T (W^T yd + grad^T (yp, yq));  xbar <- 2 x' - x;  x <- x'
+ * grad^T (p, q)_ij = p_ij + q_ij - p_{i-1,j} - q_{i,j-1} (the L of the FGP).
+ * ------------------------------------------------------------------------- */
+int or_global_cp(int n, int na, int nd, const double* ang, const double* p, int nk, double mu, double* x) {
+    if (check_geom(n, na, nd, ang) || nk < 1 || !(mu >= 0.0)) return OR_ERR_INVALID;
+    const size_t ns = (size_t)na * nd, ni = (size_t)n * n;
+    double* ones = (double*)malloc(sizeof(double) * ni);
+    double* sd = (double*)malloc(sizeof(double) * ns);
+    double* tau = (double*)malloc(sizeof(double) * ni);
+    double* yd = (double*)calloc(ns, sizeof(double));
+    double* yp = (double*)calloc(ni, sizeof(double));
+    double* yq = (double*)calloc(ni, sizeof(double));
+    double* xb = (double*)calloc(ni, sizeof(double));
+    double* sino = (double*)malloc(sizeof(double) * ns);
+    double* g = (double*)malloc(sizeof(double) * ni);
+    for (size_t e = 0; e < ni; ++e) ones[e] = 1.0;
+    fp_rect(n, na, nd, ang, ones, n, 0, 0, n, n, sino);                 /* row sums W 1 */
+    for (size_t e = 0; e < ns; ++e) sd[e] = sino[e] > 0.0 ? 1.0 / sino[e] : 0.0;
+    for (size_t e = 0; e < ns; ++e) sino[e] = 1.0;
+    bp_rect(n, na, nd, ang, sino, tau, n, 0, 0, n, n);                  /* column sums W^T 1 */
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int terms = (i < n - 1) + (i > 0) + (j < n - 1) + (j > 0);
+            tau[(size_t)i * n + j] = 1.0 / (tau[(size_t)i * n + j] + terms);
+        }
+    memset(x, 0, sizeof(double) * ni);
+    for (int k = 0; k < nk; ++k) {
+        fp_rect(n, na, nd, ang, xb, n, 0, 0, n, n, sino);
+        for (size_t e = 0; e < ns; ++e) yd[e] = (yd[e] + sd[e] * (sino[e] - p[e])) / (1.0 + sd[e]);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                const size_t o = (size_t)i * n + j;
+                const double dx = i < n - 1 ? xb[o + n] - xb[o] : 0.0;   /* p: vertical forward difference */
+                const double dy = j < n - 1 ? xb[o + 1] - xb[o] : 0.0;   /* q: horizontal */
+                double a = yp[o] + 0.5 * dx, b = yq[o] + 0.5 * dy;
+                yp[o] = i < n - 1 ? (a > mu ? mu : (a < -mu ? -mu : a)) : 0.0;
+                yq[o] = j < n - 1 ? (b > mu ? mu : (b < -mu ? -mu : b)) : 0.0;
+            }
+        bp_rect(n, na, nd, ang, yd, g, n, 0, 0, n, n);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                const size_t o = (size_t)i * n + j;
+                /* grad^T: the forward-difference transpose (-div) */
+                const double gt = -(yp[o] + yq[o]) + (i > 0 ? yp[o - n] : 0.0) + (j > 0 ? yq[o - 1] : 0.0);
+                const double xn = x[o] - tau[o] * (g[o] + gt);
+                xb[o] = 2.0 * xn - x[o];
+                x[o] = xn;
+            }
+    }
+    free(ones); free(sd); free(tau); free(yd); free(yp); free(yq); free(xb); free(sino); free(g);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * Combine (P:L1122-1127 tiling by placement; reading A19 for overlaps):
  * img(i,j) = mean over the ROIs whose core contains (i,j), summed in
  * ascending ROI index; pixels covered by no core are 0.

@@ -61,6 +61,7 @@ _SIGS = {
     "lt_pad_truncated": ([_P, _I, _I, _I, _P, _P], _I),
     "lt_tv_solve_lambdas": ([_P, _P, _P, _I, _P, _P], _I),
     "lt_haar_solve": ([_P, _P, _F, _I, _I, _P, _P], _I),
+    "lt_global_cp": ([_P, _P, _I, _F, _P, _P], _I),
     "lt_metrics": ([_P, _P, _I, _I, _I, _F, _P, _P, _P], _I),
     "lt_nelder_mead_1d": ([_P, _P, ctypes.c_double, ctypes.c_double, _I, _P, _P, _P], _I),
     "lt_launch_count": ([], _i64),
@@ -311,6 +312,14 @@ class Plan:
         out = self._empty(self.n, self.n)
         _chk(_lib.lt_global_sirt(self._p, sino.data_ptr(), n_iter, lo, hi, out.data_ptr(), _stream(self.device)),
              "lt_global_sirt")
+        return out
+
+    def global_cp(self, sino: torch.Tensor, n_iter: int, mu: float) -> torch.Tensor:
+        """Chambolle-Pock TV (diagonal preconditioning) on the full grid (lt_global_cp)."""
+        sino = _cuda_f32(sino, "sino")
+        out = self._empty(self.n, self.n)
+        _chk(_lib.lt_global_cp(self._p, sino.data_ptr(), n_iter, mu, out.data_ptr(), _stream(self.device)),
+             "lt_global_cp")
         return out
 
     def global_tv(self, sino: torch.Tensor, n_iter: int, lam: float, n_fgp: int = 100) -> torch.Tensor:

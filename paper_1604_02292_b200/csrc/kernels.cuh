@@ -1430,6 +1430,11 @@ __global__ void __launch_bounds__(256) k_conv(int na, int nd, int nk, const floa
 //   k_specmul:  S[kk][a][f] = U[k0+kk][a][f] * P[a][f]  (U already scaled by 1/L)
 //   k_croprows: b[k0+kk][a][d] = c[kk][a][d + d_c], d < N_d
 // ---------------------------------------------------------------------------
+__global__ void k_fill(long long n, float v, float* __restrict__ x) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) x[e] = v;
+}
+
 __global__ void k_scale(long long n, float s, float* __restrict__ x) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n) x[e] *= s;
@@ -1462,13 +1467,16 @@ __global__ void k_croprows(int nrows, int nd, int L, int dc, const float* __rest
 // Small kernels: disc raster, zero-frequency sums, disc gray value, p_c,
 // image (un)packing, crop, extended-ROI export, stitch.
 // ---------------------------------------------------------------------------
-// padded image + twin from a plain N x N image (src nullable: disc raster D)
+// padded image + twin from a plain N x N image (src nullable: disc raster D, P:L726-727;
+// disc = 2: the all-ones image)
 __global__ void k_pack(int n, int TP, const float* __restrict__ src, int disc, float* __restrict__ img,
                        float* __restrict__ imgT) {
     const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
     if (i >= n || j >= n) return;
     float v;
-    if (disc) {
+    if (disc == 2) {
+        v = 1.f;
+    } else if (disc) {
         const int u = 2 * j - n + 1, w = 2 * i - n + 1;
         v = (u * u + w * w <= n * n) ? 1.f : 0.f;
     } else {
@@ -1778,6 +1786,56 @@ __global__ void k_gfgp_out(int n, float lam, float beta_o, const float* __restri
     xprev[o] = x;
     rm[(long long)i * TP + PADL + j] = r;
     rmT[(long long)j * TP + PADL + i] = r;
+}
+
+// ---------------------------------------------------------------------------
+// Chambolle-Pock TV with diagonal preconditioning (NEXT-4(iii); oracle
+// or_global_cp): data dual, TV dual and primal steps on the full grid.
+// ---------------------------------------------------------------------------
+// sd = 1 / (W 1) per ray (0 where the ray misses the grid)
+__global__ void k_cp_recip(long long n, const float* __restrict__ w1, float* __restrict__ sd) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) sd[e] = w1[e] > 0.f ? 1.f / w1[e] : 0.f;
+}
+// tau = 1 / (W^T 1 + number of forward-difference terms touching the pixel)
+__global__ void k_cp_tau(int n, const float* __restrict__ wt1, float* __restrict__ tau) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const int terms = (i < n - 1) + (i > 0) + (j < n - 1) + (j > 0);
+    tau[(long long)i * n + j] = 1.f / (wt1[(long long)i * n + j] + (float)terms);
+}
+// yd <- (yd + sd (W xbar - p)) / (1 + sd)
+__global__ void k_cp_dual(long long n, const float* __restrict__ wx, const float* __restrict__ p,
+                          const float* __restrict__ sd, float* __restrict__ yd) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) yd[e] = fmaf(sd[e], wx[e] - p[e], yd[e]) / (1.f + sd[e]);
+}
+// (yp, yq) <- clip_[-mu, mu]((yp, yq) + grad xbar / 2); xbar padded [n][TP] at PADL
+__global__ void k_cp_tvdual(int n, int TP, float mu, const float* __restrict__ xb, float* __restrict__ yp,
+                            float* __restrict__ yq) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const long long o = (long long)i * n + j;
+    const float* xr = xb + (long long)i * TP + PADL + j;
+    const float dx = i < n - 1 ? xr[TP] - xr[0] : 0.f;
+    const float dy = j < n - 1 ? xr[1] - xr[0] : 0.f;
+    yp[o] = i < n - 1 ? fminf(mu, fmaxf(-mu, fmaf(0.5f, dx, yp[o]))) : 0.f;
+    yq[o] = j < n - 1 ? fminf(mu, fmaxf(-mu, fmaf(0.5f, dy, yq[o]))) : 0.f;
+}
+// x' = x - tau (W^T yd + grad^T (yp, yq)); xbar = 2 x' - x (padded + twin); x = x'
+__global__ void k_cp_primal(int n, int TP, const float* __restrict__ g, const float* __restrict__ yp,
+                            const float* __restrict__ yq, const float* __restrict__ tau, float* __restrict__ x,
+                            float* __restrict__ xb, float* __restrict__ xbT) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const long long o = (long long)i * n + j;
+    const float gt = -(yp[o] + yq[o]) + (i > 0 ? yp[o - n] : 0.f) + (j > 0 ? yq[o - 1] : 0.f);
+    const float xo = x[o];
+    const float xn = xo - tau[o] * (g[o] + gt);
+    x[o] = xn;
+    const float b = 2.f * xn - xo;
+    xb[(long long)i * TP + PADL + j] = b;
+    xbT[(long long)j * TP + PADL + i] = b;
 }
 
 __global__ void k_unpack(int n, int TP, const float* __restrict__ img, float* __restrict__ out) {

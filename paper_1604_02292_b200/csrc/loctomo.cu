@@ -120,6 +120,7 @@ struct lt_plan {
         size_t y, yT, s, v, xs, xprev;
         size_t xsblk[3], xsg[2], lams;
         size_t uhat, phat, fspec, freal, fwork;
+        size_t cp_sd, cp_tau, cp_yd;
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -881,6 +882,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     for (int l = 0; l < 3; ++l) f.xsblk[l] = take(std::max<size_t>(p->xsblk[l].size(), 1) * 4);
     for (int l = 0; l < 2; ++l) f.xsg[l] = take((size_t)n * n * fs);
     f.lams = take(R * fs);
+    f.cp_sd = take(ns * fs); f.cp_tau = take((size_t)n * n * fs); f.cp_yd = take(ns * fs);
     {   // FFT convolution cache: L = smallest power of two >= 2 N_d - 1
         int L = 1;
         while (L < 2 * n_det - 1) L <<= 1;
@@ -1231,6 +1233,68 @@ int lt_global_tv(lt_plan* p, const float* d_sino, int32_t n_iter, float lambda, 
         LT_LAUNCHED();
     }
     LT_CUDA(cudaMemcpyAsync(d_img, xprev, nb, cudaMemcpyDeviceToDevice, st));
+    return LT_OK;
+}
+
+int lt_global_cp(lt_plan* p, const float* d_sino, int32_t n_iter, float mu, float* d_img, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || !d_img || n_iter < 1 || !(mu >= 0.f)) return fail(LT_ERR_INVALID, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = p->n;
+    const long long ns = (long long)p->na * p->nd, nn = (long long)n * n;
+    float* xb = p->P<float>(p->off.gimg);
+    float* xbT = p->P<float>(p->off.gimgT);
+    float* s = p->P<float>(p->off.gsino);
+    float* g = p->P<float>(p->off.gplain);
+    float* yp = p->P<float>(p->off.gr);
+    float* yq = p->P<float>(p->off.gs);
+    float* x = p->P<float>(p->off.gxprev);
+    float* sd = p->P<float>(p->off.cp_sd);
+    float* tau = p->P<float>(p->off.cp_tau);
+    float* yd = p->P<float>(p->off.cp_yd);
+    const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float);
+    const Tiles gt = p->glob_tiles();
+    const dim3 g2 = grid2d(n, n), b2(32, 8);
+    // preconditioners: W 1 (rays) and W^T 1 (pixels)
+    LT_CUDA(cudaMemsetAsync(xb, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(xbT, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(g, 0, nn * sizeof(float), st));
+    k_pack<<<g2, b2, 0, st>>>(n, p->GTP, nullptr, 2, xb, xbT);            // ones image
+    LT_LAUNCHED();
+    if (int rc = launch_fp(*p, 0, gt, xb, xbT, 0, s, 0, nullptr, nullptr, st)) return rc;
+    k_cp_recip<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(ns, s, sd);
+    LT_LAUNCHED();
+    k_fill<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(ns, 1.f, s);
+    LT_LAUNCHED();
+    {
+        BpEpi e = epi0();
+        e.out = g; e.out_pitch = n;
+        const SinoView sv = view_full(s, p->nd);
+        if (int rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(*p, gt, sv, sv, e, st)) return rc;
+    }
+    k_cp_tau<<<g2, b2, 0, st>>>(n, g, tau);
+    LT_LAUNCHED();
+    // state: x = xbar = 0, duals 0
+    LT_CUDA(cudaMemsetAsync(xb, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(xbT, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(x, 0, nn * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(yp, 0, nn * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(yq, 0, nn * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(yd, 0, ns * sizeof(float), st));
+    for (int k = 0; k < n_iter; ++k) {
+        if (int rc = launch_fp(*p, 0, gt, xb, xbT, 0, s, 0, nullptr, nullptr, st)) return rc;     // W xbar
+        k_cp_dual<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(ns, s, d_sino, sd, yd);
+        LT_LAUNCHED();
+        k_cp_tvdual<<<g2, b2, 0, st>>>(n, p->GTP, mu, xb, yp, yq);
+        LT_LAUNCHED();
+        BpEpi e = epi0();
+        e.out = g; e.out_pitch = n;
+        const SinoView sv = view_full(yd, p->nd);
+        if (int rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(*p, gt, sv, sv, e, st)) return rc;            // W^T yd
+        k_cp_primal<<<g2, b2, 0, st>>>(n, p->GTP, g, yp, yq, tau, x, xb, xbT);
+        LT_LAUNCHED();
+    }
+    LT_CUDA(cudaMemcpyAsync(d_img, x, nn * sizeof(float), cudaMemcpyDeviceToDevice, st));
     return LT_OK;
 }
 

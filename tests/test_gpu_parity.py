@@ -490,3 +490,18 @@ def test_haar_solve_rejects_indivisible(lt):
     with pytest.raises(ValueError):
         plan.haar_solve(gpu(inp.sino), 0.01, 4)
     plan.haar_solve(gpu(inp.sino), 0.01, 3)                      # 40 = 5 * 8
+
+
+# ------------------------------------------------------------------ NEXT-4(iii): Chambolle-Pock TV
+
+@pytest.mark.parametrize("n,na,mu_scale", [(64, 32, 0.05), (48, 24, 0.0)])
+def test_global_cp_parity(lt, orc, n, na, mu_scale):
+    """Preconditioned Chambolle-Pock on the full grid against the oracle, same
+    iteration count (the iteration map is the same; fp32 vs fp64 only)."""
+    nd = nd_for(n)
+    inp = synth.make_inputs("C1", n=n, n_angles=na, n_det=nd)
+    mu = mu_scale * na * nd                     # mu = lambda / alpha
+    plan = lt.Plan(n, inp.angles, nd, [[n // 2, n // 2]], 8, 4, 2)
+    got = cpu(plan.global_cp(gpu(inp.sino), 40, mu))
+    ref = orc.global_cp(inp.sino.astype(np.float64), inp.angles, n, 40, mu)
+    assert relerr(got, ref) <= 1e-3

@@ -541,3 +541,42 @@ def test_local_haar_lambda0_equals_unregularized(orc):
     a = orc.local_solve(n, ang, nd, b, cen, 4, 4, mode="haar", lam=0.0, levels=3)
     t = orc.local_solve(n, ang, nd, b, cen, 4, 4, mode="tv", lam=0.0, n_fgp=10)
     assert relerr(a, t) < 1e-13
+
+
+# ------------------------------------------------------------------ NEXT-4(iii): Chambolle-Pock TV
+
+def _cp_problem():
+    n, nd = 8, 13
+    ang = synth.angles_for(32)          # W has full column rank (condition number ~50)
+    shapes = synth.random_shapes(n, 2, 0, synth.seeded_rng(11, 0))
+    return n, nd, ang, synth.analytic_sinogram(shapes, ang, nd)
+
+
+def test_cp_mu0_is_least_squares(orc):
+    """mu = 0: preconditioned CP minimises 1/2||Wx - p||^2; W has full column rank
+    here, so it converges to the unique least-squares solution (numpy lstsq of
+    the dense W assembled column by column from the oracle's W)."""
+    n, nd, ang, p = _cp_problem()
+    Wd = np.stack([orc.forward(np.eye(n * n)[k].reshape(n, n), ang, nd).ravel() for k in range(n * n)], axis=1)
+    assert np.linalg.matrix_rank(Wd) == n * n
+    ls = np.linalg.lstsq(Wd, p.ravel(), rcond=None)[0].reshape(n, n)
+    x = orc.global_cp(p, ang, n, 10000, 0.0)
+    assert relerr(x, ls) < 1e-10
+
+
+def test_cp_reaches_the_fista_tv_minimiser(orc):
+    """Same objective as global FISTA-TV (reading A14: mu = lam / alpha): both
+    converge to the unique minimiser of the strictly convex problem; CP (exact
+    proximal steps) ends no higher than FISTA with its inexact 300-step FGP prox."""
+    n, nd, ang, p = _cp_problem()
+    alpha = 1.0 / (len(ang) * nd)
+    lam = 0.002
+    mu = lam / alpha
+    def F(x):
+        r = orc.forward(x, ang, nd) - p
+        return 0.5 * np.sum(r * r) + mu * (np.abs(np.diff(x, axis=0)).sum() + np.abs(np.diff(x, axis=1)).sum())
+    xf = orc.global_tv(p, ang, n, 3000, lam, 300)
+    xc = orc.global_cp(p, ang, n, 30000, mu)
+    assert F(xc) <= F(xf) * (1 + 1e-12)
+    assert abs(F(xc) - F(xf)) <= 1e-5 * F(xf)
+    assert relerr(xc, xf) < 1e-4
