@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prior", default="config", choices=["config", "haar"],
-                    help="haar: NEXT-2 Haar-wavelet l1 prior (FISTA, 4 levels, lambda 0.02) instead of the config's")
+    ap.add_argument("--prior", default="config", choices=["config", "haar", "exterior"],
+                    help="haar: NEXT-2 Haar-wavelet l1 prior (FISTA, 4 levels, lambda 0.02) instead of the config's; "
+                         "exterior: NEXT-4(ii) exterior-subtraction box-SIRT (the prior art) for comparison")
     ap.add_argument("--xs-exact", action="store_true",
                     help="NEXT-4(i): x_s^k from the global SIRT iterate instead of the filtered backprojection")
     return ap.parse_args()
@@ -124,8 +125,8 @@ HAAR_LAM, HAAR_LEVELS = 0.02, 4
 
 
 def solve_mode(cfg, args) -> str:
-    if args.prior == "haar":
-        return "haar"
+    if args.prior in ("haar", "exterior"):
+        return args.prior
     return "tv" if "tv" in cfg.solver else "sirt"
 
 
@@ -210,6 +211,8 @@ def run_ours(args, cfg):
             plan.tv_solve(sino, lam_arg, cfg.n_fgp, out=out)
         elif mode == "haar":
             plan.haar_solve(sino, HAAR_LAM, HAAR_LEVELS, out=out)
+        elif mode == "exterior":
+            plan.exterior_solve(sino, 0.0, math.inf, out=out)
         else:
             plan.sirt_solve(sino, 0.0, math.inf, out=out)
         if sweep:
@@ -265,7 +268,7 @@ def run_ours(args, cfg):
             score_host[0].copy_(scores["mse"], non_blocking=True)
             score_host[1].copy_(scores["ssim"], non_blocking=True)
             torch.cuda.synchronize()
-    elif world == 1 and not trunc and mode != "haar":
+    elif world == 1 and not trunc and mode not in ("haar", "exterior"):
         def e2e_step():
             plan.solve_host(mode, sino_host, cfg.lam if mode == "tv" else 0.0,
                             0.0 if mode == "tv" else math.inf, cfg.n_fgp, image_host)
@@ -314,7 +317,7 @@ def run_ours(args, cfg):
     avg_ms = dom_ms / max(dom_n, 1)
     local_upd_per_step = upd_local
     nA = cfg.n_angles * Ptot_local          # pixel-angle updates of one A or A^T over all local ROIs
-    if dom == "fgp" and mode == "haar":
+    if dom == "fgp" and mode in ("haar", "exterior"):
         work = 0.0         # the Haar prox is a few flops per pixel: not a roofline kernel
     elif dom == "fgp":
         work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / max(dom_n, 1)
@@ -394,7 +397,8 @@ def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None, mode=None):
     t_conv = (time.perf_counter() - t0) * cfg.n_iter / n_conv_k
     g = cfg.n_roi // 2 + cfg.n_roi // 32 if roi_index is None else roi_index
     bconv = rng.standard_normal((n_iter_sample, cfg.n_angles, cfg.n_det)) * 1e-3
-    mode = {"sirt": "box", "tv": "tv", "haar": "haar", None: "tv" if "tv" in cfg.solver else "box"}[mode]
+    mode = {"sirt": "box", "tv": "tv", "haar": "haar", "exterior": "box",
+            None: "tv" if "tv" in cfg.solver else "box"}[mode]
     t0 = time.perf_counter()
     oracle.local_solve(n, inp.angles, cfg.n_det, bconv, inp.centres[g:g + 1], cfg.radius, cfg.margin, mode=mode,
                        lam=HAAR_LAM if mode == "haar" else cfg.lam, n_fgp=cfg.n_fgp, disc_c=c, use_disc=True,

@@ -150,6 +150,17 @@ int lt_global_sirt(lt_plan* plan, const float* d_sino, int32_t n_iter, float lo,
 int lt_global_tv(lt_plan* plan, const float* d_sino, int32_t n_iter, float lambda, int32_t n_fgp,
                  float* d_img, void* stream);
 
+/* Exterior subtraction (the prior art of P:L140-146,
+ * "subtracting simulated projections of a global reconstruction outside the
+ * region of interest from the acquired projections"), for comparison with the
+ * paper's method: the global reconstruction is xg = W^T C_{u_n} p_c + c D (FBP
+ * with the SIRT filter of Alg. 1, eq. sfbp, disc per the plan's
+ * flags; needs the filter bank), then for every local ROI box-SIRT on its
+ * extended rect L' (eq. sirtbox, n_iter iterations from 0) with the data
+ * p - W M_F xg.  d_cores as lt_sirt_solve.  Errors (2): lo > hi, null
+ * pointers, no bank. */
+int lt_exterior_solve(lt_plan* plan, const float* d_sino, float lo, float hi, float* d_cores, void* stream);
+
 /* Chambolle-Pock primal-dual TV solver with diagonal (row / column sum)
  * preconditioning on the full grid (the north
  * star's literal "TV-regularized primal-dual solver"; P:L351-353 names

@@ -230,6 +230,35 @@ def global_tv(p: np.ndarray, angles, n: int, n_iter: int, lam: float, n_fgp: int
     return x
 
 
+def exterior_solve(p: np.ndarray, angles, n: int, xg: np.ndarray, centres, radius: int, margin: int,
+                   n_iter: int, lo: float = 0.0, hi: float = np.inf, alpha: Optional[float] = None) -> np.ndarray:
+    """Exterior subtraction (prior art; NEXT-4(ii)): box-SIRT on
+    each extended ROI with the data p - W M_F xg.  Returns cores [R, 2r, 2r]."""
+    p = _f64(p); ang = _f64(angles); xg = np.ascontiguousarray(_f64(xg))
+    a = alpha_for(len(ang), p.shape[1]) if alpha is None else alpha
+    c = _i32(centres).reshape(-1, 2)
+    cores = np.zeros((c.shape[0], 2 * radius, 2 * radius))
+    _chk(_L().or_exterior_solve(n, len(ang), p.shape[1], _d(ang), _d(p), _d(xg), c.shape[0], _i(c), radius, margin,
+                                n_iter, ctypes.c_double(a), ctypes.c_double(lo), ctypes.c_double(hi), _d(cores)),
+         "or_exterior_solve")
+    return cores
+
+
+def fbp_filtered(p: np.ndarray, angles, n: int, n_k: int, use_disc: bool = True,
+                 bank: Optional[np.ndarray] = None) -> np.ndarray:
+    """Global FBP with the SIRT-approximating filter u_{n_k} (eq. sfbp P:L481-485,
+    Alg. 1) plus the disc correction: x = W^T C_{u_n} p_c + c D."""
+    p = _f64(p)
+    nd = p.shape[1]
+    if use_disc:
+        pc, c, _, D = disc(p, angles, n)
+    else:
+        pc, c, D = p, 0.0, np.zeros((n, n))
+    if bank is None:
+        bank = filter_bank(n, angles, nd, n_k)
+    return back(convolve(bank[n_k - 1], pc), angles, n) + c * D
+
+
 def global_cp(p: np.ndarray, angles, n: int, n_iter: int, mu: float) -> np.ndarray:
     """Chambolle-Pock TV with diagonal (row / column sum) preconditioning on the
     full grid, minimising 1/2||Wx - p||^2 + mu ||grad x||_1 (NEXT-4(iii))."""

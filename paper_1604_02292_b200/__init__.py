@@ -62,6 +62,7 @@ _SIGS = {
     "lt_tv_solve_lambdas": ([_P, _P, _P, _I, _P, _P], _I),
     "lt_haar_solve": ([_P, _P, _F, _I, _I, _P, _P], _I),
     "lt_global_cp": ([_P, _P, _I, _F, _P, _P], _I),
+    "lt_exterior_solve": ([_P, _P, _F, _F, _P, _P], _I),
     "lt_metrics": ([_P, _P, _I, _I, _I, _F, _P, _P, _P], _I),
     "lt_nelder_mead_1d": ([_P, _P, ctypes.c_double, ctypes.c_double, _I, _P, _P, _P], _I),
     "lt_launch_count": ([], _i64),
@@ -253,6 +254,16 @@ class Plan:
                 raise ValueError(f"{lams.size} lambdas for {self.R} local ROIs")
             _chk(_lib.lt_tv_solve_lambdas(self._p, sino.data_ptr(), lams.ctypes.data, n_fgp, out.data_ptr(),
                                           _stream(self.device)), "lt_tv_solve_lambdas")
+        return out
+
+    def exterior_solve(self, sino: torch.Tensor, lo: float = 0.0, hi: float = math.inf,
+                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Exterior-subtraction ROI reconstruction (the prior art; lt_exterior_solve)."""
+        sino = _cuda_f32(sino, "sino")
+        side = 2 * self.radius
+        out = self._empty(self.R, side, side) if out is None else out
+        _chk(_lib.lt_exterior_solve(self._p, sino.data_ptr(), lo, hi, out.data_ptr(), _stream(self.device)),
+             "lt_exterior_solve")
         return out
 
     def haar_solve(self, sino: torch.Tensor, lam: float, levels: int = 4, momentum: bool = True,

@@ -494,6 +494,7 @@ enum BpMode {
 struct BpEpi {
     const int* blist;                                      // sub-tile list (nullable: all sub-tiles of the tile)
     const float* xsg; int xsg_pitch;                       // global x_s^k = W^T b_k image (BOX/TV)
+    const float* xs_tile;                                  // nullable: per-tile x_s [tile][T][T] (p_tstride) instead
     float* out; long long out_tstride; int out_pitch;     // plain outputs
     float* y; float* yT; long long y_tstride;              // padded tile images (state)
     float* v; float* xs; long long p_tstride;              // plain [T][T] (TV)
@@ -639,7 +640,9 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
                     dval = (u * u + v * v <= n * n) ? discc : 0.f;      // D: centred disc, diameter N
                 }
                 // x_s^k = M_{L'} W^T b_k + c D: the global backprojection, read at this pixel
-                xsv[p] = __ldg(e.xsg + (long long)(ti.row0 + i) * e.xsg_pitch + (ti.col0 + j)) + dval;
+                // (exterior-subtraction mode: the per-ROI alpha W_{L'}^T p~, no disc term)
+                xsv[p] = e.xs_tile ? __ldg(e.xs_tile + (long long)r * e.p_tstride + (long long)i * T + j)
+                                   : __ldg(e.xsg + (long long)(ti.row0 + i) * e.xsg_pitch + (ti.col0 + j)) + dval;
                 yv[p] = e.y[(long long)r * e.y_tstride + (long long)i * t.TP + PADL + j];
             }
         }
@@ -1720,6 +1723,42 @@ __global__ void k_pad_truncated(int na, int nt, int nd, const float* __restrict_
     if (d >= nd) return;
     const int j = min(max(d - (nd - nt) / 2, 0), nt - 1);
     out[(long long)a * nd + d] = __ldg(in + (long long)a * nt + j);
+}
+
+// exterior subtraction (NEXT-4(ii)) helpers
+// padded image + twin of x + c D (D: centred disc of diameter N; disc value read from the device)
+__global__ void k_pack_disc(int n, int TP, const float* __restrict__ src, const float* __restrict__ discc, int use_disc,
+                            float* __restrict__ img, float* __restrict__ imgT) {
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= n || j >= n) return;
+    float v = src[(long long)i * n + j];
+    if (use_disc) {
+        const int u = 2 * j - n + 1, w = 2 * i - n + 1;
+        if (u * u + w * w <= n * n) v += *discc;
+    }
+    img[(long long)i * TP + PADL + j] = v;
+    imgT[(long long)j * TP + PADL + i] = v;
+}
+// every tile's padded image + twin = M_{L'} of a padded global image
+__global__ void k_extract_tiles(int T, int TP, const TileT* __restrict__ tiles, const float* __restrict__ g, int GTP,
+                                float* __restrict__ y, float* __restrict__ yT, long long y_tstride) {
+    const int r = blockIdx.z;
+    const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+    if (i >= T || j >= T) return;
+    const TileT ti = tiles[r];
+    const bool valid = i >= ti.vr0 && i < ti.vr1 && j >= ti.vc0 && j < ti.vc1;
+    const float v = valid ? g[(long long)(ti.row0 + i) * GTP + PADL + ti.col0 + j] : 0.f;
+    y[(long long)r * y_tstride + (long long)i * TP + PADL + j] = v;
+    yT[(long long)r * y_tstride + (long long)j * TP + PADL + i] = v;
+}
+// per-ROI window data p~ = (p - W xg)[window] + W_{L'} xg   (= p - W M_F xg on the window)
+__global__ void k_dwin(int na, int nd, int Wwin, const int* __restrict__ d0, const float* __restrict__ rg,
+                       const float* __restrict__ s, float* __restrict__ dw) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x, a = blockIdx.y, r = blockIdx.z;
+    if (w >= Wwin) return;
+    const int d = d0[r * na + a] + w;
+    const long long o = ((long long)r * na + a) * Wwin + w;
+    dw[o] = (d >= 0 && d < nd) ? rg[(long long)a * nd + d] + s[o] : 0.f;
 }
 
 // window -> full sinogram (zero outside the window)

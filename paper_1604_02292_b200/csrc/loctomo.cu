@@ -120,7 +120,7 @@ struct lt_plan {
         size_t y, yT, s, v, xs, xprev;
         size_t xsblk[3], xsg[2], lams;
         size_t uhat, phat, fspec, freal, fwork;
-        size_t cp_sd, cp_tau, cp_yd;
+        size_t cp_sd, cp_tau, cp_yd, dwin;
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -883,6 +883,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     for (int l = 0; l < 2; ++l) f.xsg[l] = take((size_t)n * n * fs);
     f.lams = take(R * fs);
     f.cp_sd = take(ns * fs); f.cp_tau = take((size_t)n * n * fs); f.cp_yd = take(ns * fs);
+    f.dwin = take(R * n_angles * p->Wwin * fs);
     {   // FFT convolution cache: L = smallest power of two >= 2 N_d - 1
         int L = 1;
         while (L < 2 * n_det - 1) L <<= 1;
@@ -1234,6 +1235,88 @@ int lt_global_tv(lt_plan* p, const float* d_sino, int32_t n_iter, float lambda, 
     }
     LT_CUDA(cudaMemcpyAsync(d_img, xprev, nb, cudaMemcpyDeviceToDevice, st));
     return LT_OK;
+}
+
+int lt_exterior_solve(lt_plan* p, const float* d_sino, float lo, float hi, float* d_cores, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
+    if (!(lo <= hi)) return fail(LT_ERR_INVALID, "lo <= hi required");
+    if (p->R == 0) return LT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    lt_plan& P = *p;
+    const int n = P.n;
+    // 1. global reconstruction xg = W^T C_{u_n} p_c + c D (FBP with the SIRT filter u_n, eq. sfbp)
+    float* pc = P.P<float>(P.off.pc);
+    if (P.flags & LT_DISC_ON) {
+        if (int rc = disc_correct(P, d_sino, pc, nullptr, st)) return rc;
+    } else {
+        LT_CUDA(cudaMemcpyAsync(pc, d_sino, (size_t)P.na * P.nd * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        LT_CUDA(cudaMemsetAsync(P.P<float>(P.off.discc32), 0, sizeof(float), st));
+    }
+    if (int rc = conv_cache(P, pc, st)) return rc;
+    const Tiles gt = P.glob_tiles();
+    float* xg = P.P<float>(P.off.gplain);
+    {
+        BpEpi ex = epi0();
+        ex.out = xg; ex.out_pitch = n;
+        const SinoView vb = view_full(P.P<float>(P.off.conv) + (long long)(P.n_iter - 1) * P.na * P.nd, P.nd);
+        if (int rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(P, gt, vb, vb, ex, st)) return rc;
+    }
+    float* gx = P.P<float>(P.off.gimg);
+    float* gxT = P.P<float>(P.off.gimgT);
+    const size_t gbytes = (size_t)P.GT * P.GTP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(gx, 0, gbytes, st));        // zero padding columns (Joseph taps)
+    LT_CUDA(cudaMemsetAsync(gxT, 0, gbytes, st));
+    k_pack_disc<<<grid2d(n, n), dim3(32, 8), 0, st>>>(n, P.GTP, xg, P.P<float>(P.off.discc32),
+                                                     (P.flags & LT_DISC_ON) ? 1 : 0, gx, gxT);
+    LT_LAUNCHED();
+    // 2. r_g = p - W xg on the full sinogram
+    float* rg = P.P<float>(P.off.gsino);
+    if (int rc = launch_fp(P, 2, gt, gx, gxT, 0, rg, 0, d_sino, nullptr, st)) return rc;
+    // 3. per ROI: p~ = r_g + W_{L'} xg on the window, x_d = alpha W_{L'}^T p~
+    Tiles t = P.roi_tiles();
+    const long long yts = P.ytile();
+    float* y = P.P<float>(P.off.y);
+    float* yT = P.P<float>(P.off.yT);
+    float* s = P.P<float>(P.off.s);
+    float* dw = P.P<float>(P.off.dwin);
+    float* xd = P.P<float>(P.off.xs);
+    LT_CUDA(cudaMemsetAsync(y, 0, (size_t)P.R * yts * sizeof(float), st));     // zero padding columns
+    LT_CUDA(cudaMemsetAsync(yT, 0, (size_t)P.R * yts * sizeof(float), st));
+    k_extract_tiles<<<dim3((P.T + 31) / 32, (P.T + 7) / 8, P.R), dim3(32, 8), 0, st>>>(
+        P.T, P.TP, P.P<TileT>(P.off.tiles), gx, P.GTP, y, yT, yts);
+    LT_LAUNCHED();
+    if (int rc = launch_fp_roi(P, t, y, yT, yts, s, (long long)P.na * P.Wwin, st)) return rc;
+    k_dwin<<<dim3((P.Wwin + 127) / 128, P.na, P.R), 128, 0, st>>>(P.na, P.nd, P.Wwin, P.P<int>(P.off.d0), rg, s, dw);
+    LT_LAUNCHED();
+    {
+        BpEpi e = epi0();
+        e.out = xd; e.out_tstride = P.ptile();
+        const SinoView vd = view_win(dw, P.Wwin, P.na);
+        if (int rc = launch_bp_t<1, BP_PLAIN_TILE>(P, t, vd, vd, e, st)) return rc;
+        const long long ne = (long long)P.R * P.ptile();
+        k_scale<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(ne, (float)P.alpha, xd);
+        LT_LAUNCHED();
+    }
+    // 4. box-SIRT on L' from 0: x <- clamp(x + x_d - alpha W_{L'}^T W_{L'} x); y holds x
+    LT_CUDA(cudaMemsetAsync(y, 0, (size_t)P.R * yts * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(yT, 0, (size_t)P.R * yts * sizeof(float), st));
+    for (int k = 0; k < P.n_iter; ++k) {
+        BpEpi e = epi0();
+        e.xs_tile = xd; e.p_tstride = P.ptile();
+        e.y = y; e.yT = yT; e.y_tstride = yts;
+        e.alpha = (float)P.alpha; e.lo = lo; e.hi = hi; e.last = 1;       // store x itself every iteration
+        if (k == 0) {
+            const SinoView v0 = view_win(dw, P.Wwin, P.na);
+            if (int rc = launch_bp_t<0, BP_BOX>(P, t, v0, v0, e, st)) return rc;
+        } else {
+            if (int rc = launch_fp_roi(P, t, y, yT, yts, s, (long long)P.na * P.Wwin, st)) return rc;
+            const SinoView vs = view_win(s, P.Wwin, P.na);
+            if (int rc = launch_bp_t<1, BP_BOX>(P, t, vs, vs, e, st)) return rc;
+        }
+    }
+    P.last_mode = 0;
+    return crop_cores(P, d_cores, st);
 }
 
 int lt_global_cp(lt_plan* p, const float* d_sino, int32_t n_iter, float mu, float* d_img, void* stream) {

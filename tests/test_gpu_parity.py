@@ -505,3 +505,33 @@ def test_global_cp_parity(lt, orc, n, na, mu_scale):
     got = cpu(plan.global_cp(gpu(inp.sino), 40, mu))
     ref = orc.global_cp(inp.sino.astype(np.float64), inp.angles, n, 40, mu)
     assert relerr(got, ref) <= 1e-3
+
+
+# ------------------------------------------------------------------ NEXT-4(ii): exterior subtraction
+
+def test_exterior_solve_parity(lt, orc):
+    """Exterior subtraction (prior art) with xg = FBP with the SIRT
+    filter u_n + c D: GPU against the oracle on interior and clipped ROIs."""
+    cfg = synth.config("C1")
+    inp = synth.make_inputs(cfg)
+    cen = np.array([[32, 32], [12, 50], [50, 14]], dtype=np.int32)
+    nit = 15
+    plan = lt.Plan(64, inp.angles, 91, cen, 12, 8, nit)
+    plan.filter_bank()
+    got = cpu(plan.exterior_solve(gpu(inp.sino), 0.0, math.inf))
+    p64 = inp.sino.astype(np.float64)
+    xg = orc.fbp_filtered(p64, inp.angles, 64, nit)
+    ref = orc.exterior_solve(p64, inp.angles, 64, xg, cen, 12, 8, nit)
+    for q in range(3):
+        assert relerr(got[q], ref[q]) <= 1e-3, q
+
+
+def test_exterior_solve_full_grid_is_global_sirt(lt, orc):
+    """Full-grid ROI: no exterior, so the result is global box-SIRT (GPU vs GPU and oracle)."""
+    inp = synth.make_inputs("C1", n=48, n_angles=24, n_det=nd_for(48))
+    nit = 12
+    plan = lt.Plan(48, inp.angles, nd_for(48), [[24, 24]], 24, 0, nit)
+    plan.filter_bank()
+    core = cpu(plan.exterior_solve(gpu(inp.sino), 0.0, math.inf))[0]
+    ref = orc.global_box(inp.sino.astype(np.float64), inp.angles, 48, nit)
+    assert relerr(core, ref) <= 1e-4

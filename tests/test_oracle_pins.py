@@ -580,3 +580,35 @@ def test_cp_reaches_the_fista_tv_minimiser(orc):
     assert F(xc) <= F(xf) * (1 + 1e-12)
     assert abs(F(xc) - F(xf)) <= 1e-5 * F(xf)
     assert relerr(xc, xf) < 1e-4
+
+
+# ------------------------------------------------------------------ NEXT-4(ii): exterior subtraction
+
+def test_exterior_full_grid_is_global_box_sirt(orc):
+    """A ROI covering the grid has no exterior (M_F = 0): whatever the
+    global reconstruction, the exterior-subtraction solve is global box-SIRT."""
+    n, nd, ang, p = _small_problem(n=16)
+    xg = np.random.default_rng(3).random((n, n))
+    cores = orc.exterior_solve(p, ang, n, xg, [[8, 8]], 8, 0, 12)
+    ref = orc.global_box(p, ang, n, 12)
+    assert relerr(cores[0], ref) < 1e-12
+
+
+def test_exterior_with_exact_exterior_is_local_sirt_of_the_roi_data(orc):
+    """With consistent data p = W x_true and xg = x_true, p - W M_F xg = W M_L' x_true:
+    the ROI solve is box-SIRT on L' for data generated by the ROI part alone
+    (checked against global box-SIRT of the masked object restricted to L')."""
+    n, nd = 16, 23
+    ang = synth.angles_for(14)
+    xt = np.random.default_rng(4).random((n, n))
+    p = orc.forward(xt, ang, nd)
+    cen, r, m = [[8, 7]], 3, 2
+    rect = orc.roi_rects(n, cen, r, m)[0]
+    cores = orc.exterior_solve(p, ang, n, xt, cen, r, m, 10, lo=-np.inf, hi=np.inf)
+    # the same iteration written with the global operators and the mask
+    M = np.zeros((n, n)); M[rect[4]:rect[5], rect[6]:rect[7]] = 1.0
+    pl = orc.forward(M * xt, ang, nd)
+    x = np.zeros((n, n)); alpha = orc.alpha_for(len(ang), nd)
+    for _ in range(10):
+        x = x + alpha * M * orc.back(pl - orc.forward(M * x, ang, nd), ang, n)
+    assert relerr(cores[0], x[rect[0]:rect[1], rect[2]:rect[3]]) < 1e-12
