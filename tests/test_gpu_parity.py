@@ -535,3 +535,19 @@ def test_exterior_solve_full_grid_is_global_sirt(lt, orc):
     core = cpu(plan.exterior_solve(gpu(inp.sino), 0.0, math.inf))[0]
     ref = orc.global_box(inp.sino.astype(np.float64), inp.angles, 48, nit)
     assert relerr(core, ref) <= 1e-4
+
+
+def test_tv_solve_C3_subset(lt, orc):
+    """C3 geometry (limited angle, extended side 192: 6-CTA FGP clusters) with the
+    TV solver on seeded (partly clipped) ROIs, 12 iterations x 30 FGP steps."""
+    cfg = synth.config("C3")
+    inp = synth.make_inputs("C3")
+    n_iter, n_fgp = 12, 30
+    cen = np.concatenate([inp.centres[:3], np.array([[48, 48], [976, 960]], dtype=np.int32)])
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.tv_solve(gpu(inp.sino), cfg.lam, n_fgp))
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, n_iter,
+                       mode="tv", lam=cfg.lam, n_fgp=n_fgp)
+    for q in range(len(cen)):
+        assert relerr(cores[q], ref[q]) <= 1e-3, q
