@@ -105,6 +105,12 @@ struct lt_plan {
     size_t fwork_bytes = 0;
     cufftHandle plan_r2c_p = 0, plan_r2c_k = 0, plan_c2r_k = 0;
     bool spec_ready = false;
+    // CUDA graph of the local iteration loop (replayed while its key is unchanged)
+    cudaGraphExec_t gexec = nullptr;
+    double gkey[10] = {0};
+    long long g_nlaunch = 0;
+    cudaStream_t gs = nullptr;                       // capture / replay stream (the caller's may be the legacy one)
+    cudaEvent_t gev_in = nullptr, gev_out = nullptr;
     int stitch_cap = 0;           // max list entries
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
@@ -636,6 +642,54 @@ int crop_cores(lt_plan& p, float* d_cores, cudaStream_t st) {
     return LT_OK;
 }
 
+// The local iteration loop (n x 3-4 launches) as one CUDA graph: captured on
+// the first solve with a given (mode, bounds, lambda, n_FGP, lambda array,
+// Haar momentum, sinogram pointer) and replayed afterwards; every input of the
+// loop lives in the workspace, so a replay sees the new data.  Off under
+// per-kernel timing (the timing events would not repeat) and with two ROI
+// streams; LT_GRAPH=0 disables it.
+int run_local(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, const float* d_sino, cudaStream_t st) {
+    static int use = -1;
+    if (use < 0) { const char* e = getenv("LT_GRAPH"); use = !(e && atoi(e) == 0); }
+    if (!use || g_timing || (p.nsplit > 1 && p.R >= 2)) return local_iterations(p, mode, lo, hi, lam, nfgp, d_sino, st);
+    if (mode == 1)
+        if (int rc = ensure_fgp_beta(nfgp, st)) return rc;   // (synchronous on first use: not inside a capture)
+    if (!p.gs) {
+        LT_CUDA(cudaStreamCreateWithFlags(&p.gs, cudaStreamNonBlocking));
+        LT_CUDA(cudaEventCreateWithFlags(&p.gev_in, cudaEventDisableTiming));
+        LT_CUDA(cudaEventCreateWithFlags(&p.gev_out, cudaEventDisableTiming));
+    }
+    // fork onto the graph stream, join back after the replay
+    LT_CUDA(cudaEventRecord(p.gev_in, st));
+    LT_CUDA(cudaStreamWaitEvent(p.gs, p.gev_in, 0));
+    const cudaStream_t caller = st;
+    st = p.gs;
+    const double key[10] = {(double)mode, (double)lo, (double)hi, (double)lam, (double)nfgp, (double)p.lam_array,
+                            (double)p.haar_momentum, (double)(uintptr_t)d_sino, (double)(uintptr_t)p.ws, 1.0};
+    if (!p.gexec || memcmp(key, p.gkey, sizeof key) != 0) {
+        if (p.gexec) { cudaGraphExecDestroy(p.gexec); p.gexec = nullptr; }
+        cudaGraph_t g = nullptr;
+        const long long n0 = g_launches.load();
+        LT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const int rc = local_iterations(p, mode, lo, hi, lam, nfgp, d_sino, st);
+        const cudaError_t ec = cudaStreamEndCapture(st, &g);
+        if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+        LT_CUDA(ec);
+        const cudaError_t ei = cudaGraphInstantiate(&p.gexec, g, 0);
+        cudaGraphDestroy(g);
+        LT_CUDA(ei);
+        p.g_nlaunch = g_launches.load() - n0;   // counted again at every replay
+        g_launches.fetch_sub(p.g_nlaunch);
+        memcpy(p.gkey, key, sizeof key);
+    }
+    LT_CUDA(cudaGraphLaunch(p.gexec, st));
+    g_launches.fetch_add(p.g_nlaunch);
+    LT_CUDA(cudaEventRecord(p.gev_out, st));
+    LT_CUDA(cudaStreamWaitEvent(caller, p.gev_out, 0));
+    p.last_mode = mode;
+    return LT_OK;
+}
+
 int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfgp, float* d_cores, cudaStream_t st) {
     float* pc = p.P<float>(p.off.pc);
     if (p.flags & LT_XS_EXACT) {
@@ -648,8 +702,7 @@ int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfg
     }
     if (!(p.flags & LT_XS_EXACT))
         if (int rc = conv_cache(p, pc, st)) return rc;
-    if (int rc = local_iterations(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode != 0 ? a0 : 0.f, nfgp,
-                                  d_sino, st))
+    if (int rc = run_local(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode != 0 ? a0 : 0.f, nfgp, d_sino, st))
         return rc;
     return crop_cores(p, d_cores, st);
 }
@@ -959,6 +1012,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     }
     p->bound = true;
     p->bank_ready = p->wd_ready = p->spec_ready = false;
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
     return LT_OK;
 }
 
@@ -1524,6 +1578,10 @@ void lt_plan_destroy(lt_plan* p) {
     }
     for (int g = 0; g < 3; ++g)
         if (p->gev[g]) cudaEventDestroy(p->gev[g]);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->gs) cudaStreamDestroy(p->gs);
+    if (p->gev_in) cudaEventDestroy(p->gev_in);
+    if (p->gev_out) cudaEventDestroy(p->gev_out);
     if (p->plan_r2c_p) cufftDestroy(p->plan_r2c_p);
     if (p->plan_r2c_k) cufftDestroy(p->plan_r2c_k);
     if (p->plan_c2r_k) cufftDestroy(p->plan_c2r_k);
