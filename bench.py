@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--prior", default="config", choices=["config", "haar", "exterior"],
                     help="haar: NEXT-2 Haar-wavelet l1 prior (FISTA, 4 levels, lambda 0.02) instead of the config's; "
                          "exterior: NEXT-4(ii) exterior-subtraction box-SIRT (the prior art) for comparison")
+    ap.add_argument("--combine", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: stitch reading the peers' cores over NVLink (CUDA IPC, one kernel) or NCCL all-gather + stitch")
     ap.add_argument("--xs-exact", action="store_true",
                     help="NEXT-4(i): x_s^k from the global SIRT iterate instead of the filtered backprojection")
     return ap.parse_args()
@@ -190,6 +192,13 @@ def run_ours(args, cfg):
     cores = torch.zeros(spr, side, side, device="cuda")
     image = torch.empty(cfg.n, cfg.n, device="cuda")
     gathered = torch.empty(world * spr, side, side, device="cuda") if world > 1 else None
+    peer = None
+    if world > 1 and args.combine == "peer":
+        try:
+            peer = ltd.PeerCombine(plan, cores, slot_roi, spr)
+        except Exception as e:   # e.g. no CUDA IPC between these devices: NCCL all-gather instead
+            print(f"peer combine unavailable ({e}); using the NCCL all-gather", file=sys.stderr)
+            peer = None
 
     # lambda-sweep workloads (L1, NEXT-1): every ROI carries its own lambda; the
     # step scores each core against the ground truth (MSE, SSIM) instead of combining
@@ -218,7 +227,9 @@ def run_ours(args, cfg):
         if sweep:
             scores["mse"], scores["ssim"] = lt.metrics(out, truth_cores)
             return
-        if world > 1:
+        if peer is not None:
+            peer.combine(image)                            # stitch reading the peers' cores over NVLink
+        elif world > 1:
             ltd.gather_cores(cores, out=gathered)          # NCCL all-gather over NVLink
             plan.combine(gathered, slot_roi, out=image)
         else:
@@ -358,6 +369,8 @@ def run_ours(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(cfg, args, world),
+        "combine": ("peer-memory stitch (CUDA IPC over NVLink, one kernel)" if peer is not None else
+                    "NCCL all-gather + stitch" if world > 1 else "local stitch"),
         "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
         "fgp_gpix_it_s": round(fgp_pi / (ms_per_step / 1e3) / 1e9, 2),
         "bank_ms": round(bank_ms, 2),

@@ -137,6 +137,27 @@ int lt_get_ext(const lt_plan* plan, float* d_ext, void* stream);
 int lt_combine_rois(const lt_plan* plan, const float* d_cores_all, int32_t n_slots,
                     const int32_t* h_slot_roi, float* d_image, void* stream);
 
+/* Combine over peer memory (the all-gather and the stitch in one
+ * kernel): like lt_combine_rois, but slot s of the gathered layout is read in
+ * place from rank s / slots_per_rank's core buffer, h_peer_cores[rank]
+ * (a host array of `world` <= 64 DEVICE pointers valid in this process: the
+ * own buffer and the others' buffers mapped with lt_ipc_open_handle, read over
+ * NVLink), at index s % slots_per_rank ([slots_per_rank][2r][2r] each).
+ * h_slot_roi: the global ROI of each of the world * slots_per_rank slots
+ * (-1 = empty).  The caller orders the peers' solves before this call (e.g. a
+ * stream sync + process-group barrier) and this call before the peers
+ * overwrite their buffers.  Same image, bitwise, as lt_combine_rois on the
+ * all-gathered cores.  Errors (2): null pointers, world outside 1..64. */
+int lt_combine_peers(const lt_plan* plan, const float* const* h_peer_cores, int32_t world, int32_t slots_per_rank,
+                     const int32_t* h_slot_roi, float* d_image, void* stream);
+
+/* CUDA IPC for lt_combine_peers: the 64-byte handle of a device allocation
+ * (h_handle: host buffer of 64 bytes), opening a peer's handle in this process
+ * (peer access over NVLink enabled lazily) and closing it. */
+int lt_ipc_get_handle(const void* d_ptr, void* h_handle);
+int lt_ipc_open_handle(const void* h_handle, void** d_ptr);
+int lt_ipc_close(void* d_ptr);
+
 /* End-to-end entry with HOST buffers (pinned recommended): copies h_sino in,
  * runs lt_sirt_solve (mode 0) or lt_tv_solve (mode 1), combines this rank's
  * cores into h_image (N x N).  Synchronous. */

@@ -63,6 +63,10 @@ _SIGS = {
     "lt_haar_solve": ([_P, _P, _F, _I, _I, _P, _P], _I),
     "lt_global_cp": ([_P, _P, _I, _F, _P, _P], _I),
     "lt_exterior_solve": ([_P, _P, _F, _F, _P, _P], _I),
+    "lt_combine_peers": ([_P, _P, _I, _I, _P, _P, _P], _I),
+    "lt_ipc_get_handle": ([_P, _P], _I),
+    "lt_ipc_open_handle": ([_P, _P], _I),
+    "lt_ipc_close": ([_P], _I),
     "lt_metrics": ([_P, _P, _I, _I, _I, _F, _P, _P, _P], _I),
     "lt_nelder_mead_1d": ([_P, _P, ctypes.c_double, ctypes.c_double, _I, _P, _P, _P], _I),
     "lt_launch_count": ([], _i64),
@@ -308,6 +312,17 @@ class Plan:
                                   _stream(self.device)), "lt_combine_rois")
         return out
 
+    def combine_peers(self, peer_ptrs: Sequence[int], slots_per_rank: int, slot_roi: Sequence[int],
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Combine reading every rank's [slots_per_rank, 2r, 2r] core buffer in place
+        (device pointers valid in this process; lt_combine_peers)."""
+        ptrs = (ctypes.c_void_p * len(peer_ptrs))(*[int(v) for v in peer_ptrs])
+        slots = np.ascontiguousarray(np.asarray(slot_roi, dtype=np.int32))
+        out = self._empty(self.n, self.n) if out is None else out
+        _chk(_lib.lt_combine_peers(self._p, ptrs, len(peer_ptrs), int(slots_per_rank), slots.ctypes.data,
+                                   out.data_ptr(), _stream(self.device)), "lt_combine_peers")
+        return out
+
     def solve_host(self, mode: str, sino_host: torch.Tensor, p0: float, p1: float = 0.0, n_fgp: int = 100,
                    image_host: Optional[torch.Tensor] = None) -> torch.Tensor:
         """End-to-end with host buffers (pinned tensors recommended)."""
@@ -403,3 +418,21 @@ def nelder_mead_1d(f, t_lo: float, t_hi: float, budget: int):
     if err:
         raise err[0]
     return tb.value, fb.value, ne.value
+
+
+def ipc_handle(t: torch.Tensor) -> bytes:
+    """64-byte CUDA IPC handle of the allocation holding t (lt_ipc_get_handle)."""
+    buf = ctypes.create_string_buffer(64)
+    _chk(_lib.lt_ipc_get_handle(t.data_ptr(), buf), "lt_ipc_get_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """Device pointer of a peer's allocation in this process (lt_ipc_open_handle)."""
+    ptr = ctypes.c_void_p(0)
+    _chk(_lib.lt_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)), "lt_ipc_open_handle")
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _chk(_lib.lt_ipc_close(ctypes.c_void_p(ptr)), "lt_ipc_close")

@@ -1770,10 +1770,14 @@ __global__ void k_scatter_win(int na, int nd, int Wwin, const int* __restrict__ 
     sino[(long long)a * nd + d] = (w >= 0 && w < Wwin) ? win[(long long)a * Wwin + w] : 0.f;
 }
 
-// combine: CTA per 32x32 image block, fixed ascending-ROI order (A19)
+// combine: CTA per 32x32 image block, fixed ascending-ROI order (A19).
+// peers == nullptr: slot s is cores[s]; else slot s lives in rank s / spr's
+// core buffer (peers[rank], a local or CUDA-IPC-mapped NVLink peer pointer)
+// at index s % spr: the all-gather and the stitch in one pass over peer memory.
 __global__ void k_stitch(int n, int side, int nbx, const int* __restrict__ lst_off, const int* __restrict__ lst,
                          const int* __restrict__ slot_r0, const int* __restrict__ slot_c0,
-                         const float* __restrict__ cores, float* __restrict__ img) {
+                         const float* __restrict__ cores, float* __restrict__ img,
+                         const float* const* __restrict__ peers = nullptr, int spr = 1) {
     const int bx = blockIdx.x % nbx, by = blockIdx.x / nbx;
     const int j = bx * 32 + threadIdx.x;
     const int beg = lst_off[blockIdx.x], end = lst_off[blockIdx.x + 1];
@@ -1785,7 +1789,9 @@ __global__ void k_stitch(int n, int side, int nbx, const int* __restrict__ lst_o
             const int s = lst[q];
             const int li = i - slot_r0[s], lj = j - slot_c0[s];
             if (li >= 0 && li < side && lj >= 0 && lj < side) {
-                sum += cores[((long long)s * side + li) * side + lj];
+                const float* c = peers ? peers[s / spr] + (long long)(s % spr) * side * side
+                                       : cores + (long long)s * side * side;
+                sum += c[(long long)li * side + lj];
                 ++cnt;
             }
         }

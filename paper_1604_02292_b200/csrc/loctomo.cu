@@ -46,6 +46,7 @@ int fail(int code, const char* fmt, ...) {
     } while (0)
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr int LT_MAX_PEERS = 64;
 
 // ---- optional per-kernel-class timing (CUDA events on the launch stream) ----
 enum { TC_FP = 0, TC_BP = 1, TC_FGP = 2, TC_CONV = 3, TC_N = 4 };
@@ -126,7 +127,7 @@ struct lt_plan {
         size_t y, yT, s, v, xs, xprev;
         size_t xsblk[3], xsg[2], lams;
         size_t uhat, phat, fspec, freal, fwork;
-        size_t cp_sd, cp_tau, cp_yd, dwin;
+        size_t cp_sd, cp_tau, cp_yd, dwin, peers;
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -707,7 +708,8 @@ int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfg
     return crop_cores(p, d_cores, st);
 }
 
-int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot_roi, float* d_image, cudaStream_t st) {
+int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot_roi, float* d_image, cudaStream_t st,
+            const float* const* h_peers = nullptr, int world = 0, int spr = 1) {
     const int side = 2 * p.radius;
     const int nb = (p.n + 31) / 32;
     std::vector<std::vector<std::pair<int, int>>> buckets((size_t)nb * nb);
@@ -738,7 +740,15 @@ int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot
     if (!lst.empty()) LT_CUDA(cudaMemcpyAsync(d_lst, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     LT_CUDA(cudaMemcpyAsync(d_r0, r0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
     LT_CUDA(cudaMemcpyAsync(d_c0, c0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
-    k_stitch<<<nb * nb, dim3(32, 8), 0, st>>>(p.n, side, nb, d_off, d_lst, d_r0, d_c0, d_cores, d_image);
+    const float* const* d_peers = nullptr;
+    if (h_peers) {
+        if (world < 1 || world > LT_MAX_PEERS || spr < 1 || (long long)world * spr < n_slots)
+            return fail(LT_ERR_INVALID, "combine_peers: bad world %d / slots per rank %d", world, spr);
+        const float** tab = p.P<const float*>(p.off.peers);
+        LT_CUDA(cudaMemcpyAsync(tab, h_peers, world * sizeof(float*), cudaMemcpyHostToDevice, st));
+        d_peers = tab;
+    }
+    k_stitch<<<nb * nb, dim3(32, 8), 0, st>>>(p.n, side, nb, d_off, d_lst, d_r0, d_c0, d_cores, d_image, d_peers, spr);
     LT_LAUNCHED();
     // pageable copies above are staged synchronously by the driver before returning
     return LT_OK;
@@ -937,6 +947,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.lams = take(R * fs);
     f.cp_sd = take(ns * fs); f.cp_tau = take((size_t)n * n * fs); f.cp_yd = take(ns * fs);
     f.dwin = take(R * n_angles * p->Wwin * fs);
+    f.peers = take(LT_MAX_PEERS * sizeof(void*));
     {   // FFT convolution cache: L = smallest power of two >= 2 N_d - 1
         int L = 1;
         while (L < 2 * n_det - 1) L <<= 1;
@@ -1193,6 +1204,39 @@ int lt_combine_rois(const lt_plan* p, const float* d_cores_all, int32_t n_slots,
     if (int rc = check_plan(p)) return rc;
     if (!d_image || n_slots < 0 || (n_slots > 0 && (!d_cores_all || !h_slot_roi))) return fail(LT_ERR_INVALID, "bad arguments");
     return combine(*p, d_cores_all, n_slots, h_slot_roi, d_image, (cudaStream_t)stream);
+}
+
+int lt_combine_peers(const lt_plan* p, const float* const* h_peer_cores, int32_t world, int32_t slots_per_rank,
+                     const int32_t* h_slot_roi, float* d_image, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_image || !h_peer_cores || !h_slot_roi || world < 1 || slots_per_rank < 1)
+        return fail(LT_ERR_INVALID, "bad arguments");
+    for (int g = 0; g < world; ++g)
+        if (!h_peer_cores[g]) return fail(LT_ERR_INVALID, "null core buffer of rank %d", g);
+    return combine(*p, nullptr, world * slots_per_rank, h_slot_roi, d_image, (cudaStream_t)stream, h_peer_cores, world,
+                   slots_per_rank);
+}
+
+int lt_ipc_get_handle(const void* d_ptr, void* h_handle) {
+    if (!d_ptr || !h_handle) return fail(LT_ERR_INVALID, "null pointer");
+    cudaIpcMemHandle_t h;
+    LT_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    memcpy(h_handle, &h, sizeof h);
+    return LT_OK;
+}
+
+int lt_ipc_open_handle(const void* h_handle, void** d_ptr) {
+    if (!h_handle || !d_ptr) return fail(LT_ERR_INVALID, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, h_handle, sizeof h);
+    LT_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return LT_OK;
+}
+
+int lt_ipc_close(void* d_ptr) {
+    if (!d_ptr) return fail(LT_ERR_INVALID, "null pointer");
+    LT_CUDA(cudaIpcCloseMemHandle(d_ptr));
+    return LT_OK;
 }
 
 int lt_solve_host(lt_plan* p, int32_t mode, const float* h_sino, float p0, float p1, int32_t n_fgp, float* h_image,

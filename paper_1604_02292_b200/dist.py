@@ -63,3 +63,55 @@ def setup_combine(plan, group=None) -> Tuple[int, np.ndarray]:
     lists = exchange_local_lists(plan.local_rois, group) if world > 1 else [list(plan.local_rois)]
     spr = slots_per_rank(lists)
     return spr, slot_table(lists, spr)
+
+
+class PeerCombine:
+    """Combine over NVLink peer memory (lt_combine_peers): every rank's core
+    buffer [slots_per_rank, 2r, 2r] is mapped into every other rank with CUDA
+    IPC once; each combine then reads the peers' cores in place inside the
+    stitch kernel (no all-gather copy).  Ordering: the solves of all ranks
+    complete before any stitch (stream sync + barrier), and every stitch
+    completes before any rank overwrites its buffer (sync + barrier again)."""
+
+    def __init__(self, plan, cores: torch.Tensor, slot_roi: np.ndarray, spr: int, group=None):
+        import torch.distributed as dist
+        import paper_1604_02292_b200 as lt
+        self.plan, self.cores, self.slot_roi, self.spr, self.group = plan, cores, slot_roi, spr, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self._opened = []
+        if self.world == 1:
+            self.ptrs = [cores.data_ptr()]
+            return
+        # the IPC handle names the whole cudaMalloc segment of torch's caching
+        # allocator: torch reports the storage's offset inside it (_share_cuda_);
+        # add the tensor's offset inside the storage
+        seg_off = int(cores.untyped_storage()._share_cuda_()[3])
+        info = (lt.ipc_handle(cores), seg_off + cores.storage_offset() * cores.element_size())
+        infos: List = [None] * self.world
+        dist.all_gather_object(infos, info, group=group)
+        self.ptrs = []
+        for g, (h, off) in enumerate(infos):
+            if g == self.rank:
+                self.ptrs.append(cores.data_ptr())
+            else:
+                p = lt.ipc_open(h)
+                self._opened.append(p)
+                self.ptrs.append(p + off)
+
+    def combine(self, out: torch.Tensor) -> torch.Tensor:
+        import torch.distributed as dist
+        if self.world > 1:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)
+        self.plan.combine_peers(self.ptrs, self.spr, self.slot_roi, out=out)
+        if self.world > 1:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)
+        return out
+
+    def close(self):
+        import paper_1604_02292_b200 as lt
+        for p in self._opened:
+            lt.ipc_close(p)
+        self._opened = []
