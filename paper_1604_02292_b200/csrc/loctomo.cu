@@ -112,6 +112,11 @@ struct lt_plan {
     long long g_nlaunch = 0;
     cudaStream_t gs = nullptr;                       // capture / replay stream (the caller's may be the legacy one)
     cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+    // side stream for the global x_s backprojection of the NEXT iteration (it
+    // only waits for the ROI BP that read the previous x_s, so it overlaps the
+    // FGP and the forward projection; LT_XS_OVERLAP=0 disables)
+    cudaStream_t xst = nullptr;
+    cudaEvent_t xev_bp = nullptr, xev_xs = nullptr;
     int stitch_cap = 0;           // max list entries
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
@@ -521,10 +526,32 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
     const int* blist = p.P<int>(p.off.xsblk[gl]);
     const int nbl = (int)p.xsblk[gl].size();
     if (exact) { xsg = p.P<float>(p.off.gimg) + PADL; xsg_pitch = p.GTP; }   // the global SIRT iterate
+    static int overlap_env = -1;
+    if (overlap_env < 0) { const char* e = getenv("LT_XS_OVERLAP"); overlap_env = !(e && atoi(e) == 0); }
+    const bool side = overlap_env && !exact && !fst && nbl > 0;
+    if (side && !p.xst) {
+        LT_CUDA(cudaStreamCreateWithFlags(&p.xst, cudaStreamNonBlocking));
+        LT_CUDA(cudaEventCreateWithFlags(&p.xev_bp, cudaEventDisableTiming));
+        LT_CUDA(cudaEventCreateWithFlags(&p.xev_xs, cudaEventDisableTiming));
+    }
+    auto xs_bp = [&](int k, cudaStream_t sx) -> int {
+        BpEpi ex = epi0();
+        ex.blist = blist; ex.out = xsg; ex.out_pitch = p.n;
+        const SinoView vb = view_full(p.P<float>(p.off.conv) + (long long)k * ns, p.nd);
+        return launch_bp_t<1, BP_PLAIN_GLOBAL>(p, p.glob_tiles(), vb, vb, ex, sx, nbl);
+    };
+    if (side) {   // x_s^0 on the side stream, after everything queued so far
+        LT_CUDA(cudaEventRecord(p.xev_bp, st));
+        LT_CUDA(cudaStreamWaitEvent(p.xst, p.xev_bp, 0));
+        if (int rc = xs_bp(0, p.xst)) return rc;
+        LT_CUDA(cudaEventRecord(p.xev_xs, p.xst));
+    }
     double tk = 1.0;
     for (int k = 0; k < p.n_iter; ++k) {
         const float* bk = p.P<float>(p.off.conv) + (long long)k * ns;
-        if (exact) {   // x^k = x^{k-1} + alpha W^T (p - W x^{k-1}) on the full grid, x^0 = 0 (eq. sirtit)
+        if (side) {
+            // x_s^k was queued on the side stream; its ROI BP waits for it below
+        } else if (exact) {   // x^k = x^{k-1} + alpha W^T (p - W x^{k-1}) on the full grid, x^0 = 0 (eq. sirtit)
             const Tiles gt = p.glob_tiles();
             float* gx = p.P<float>(p.off.gimg);
             float* gxT = p.P<float>(p.off.gimgT);
@@ -535,10 +562,7 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
             const SinoView sv = view_full(r, p.nd);
             if (int rc = launch_bp_t<1, BP_GSIRT>(p, gt, sv, sv, eg, st)) return rc;
         } else {   // (independent of y: overlaps the previous FGP of this group)
-            BpEpi ex = epi0();
-            ex.blist = blist; ex.out = xsg; ex.out_pitch = p.n;
-            const SinoView vb = view_full(bk, p.nd);
-            if (int rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(p, p.glob_tiles(), vb, vb, ex, st, nbl)) return rc;
+            if (int rc = xs_bp(k, st)) return rc;
         }
         if (fst && k > 0) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));    // previous FGP of this group
         BpEpi e = epi0();
@@ -549,14 +573,22 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
         e.alpha = (float)p.alpha; e.lo = lo; e.hi = hi; e.last = (k == p.n_iter - 1);
         if (k == 0) {
             // y^0 = 0: W_{L'} y^0 = 0, no gather
+            if (side) LT_CUDA(cudaStreamWaitEvent(st, p.xev_xs, 0));
             const SinoView v0 = view_full(bk, p.nd);
             if (mode == 0) { if (int rc = launch_bp_t<0, BP_BOX>(p, t, v0, v0, e, st)) return rc; }
             else { if (int rc = launch_bp_t<0, BP_TV>(p, t, v0, v0, e, st)) return rc; }
         } else {
             if (int rc = launch_fp_roi(p, t, y, yT, yts, s, (long long)p.na * p.Wwin, st)) return rc;
+            if (side) LT_CUDA(cudaStreamWaitEvent(st, p.xev_xs, 0));
             const SinoView vs = view_win(s, p.Wwin, p.na);
             if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vs, vs, e, st)) return rc; }
             else { if (int rc = launch_bp_t<1, BP_TV>(p, t, vs, vs, e, st)) return rc; }
+        }
+        if (side && k + 1 < p.n_iter) {   // x_s^{k+1} may overwrite x_s^k once this ROI BP has read it
+            LT_CUDA(cudaEventRecord(p.xev_bp, st));
+            LT_CUDA(cudaStreamWaitEvent(p.xst, p.xev_bp, 0));
+            if (int rc = xs_bp(k + 1, p.xst)) return rc;
+            LT_CUDA(cudaEventRecord(p.xev_xs, p.xst));
         }
         if (mode == 1) {
             const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
@@ -1624,6 +1656,9 @@ void lt_plan_destroy(lt_plan* p) {
         if (p->gev[g]) cudaEventDestroy(p->gev[g]);
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     if (p->gs) cudaStreamDestroy(p->gs);
+    if (p->xst) cudaStreamDestroy(p->xst);
+    if (p->xev_bp) cudaEventDestroy(p->xev_bp);
+    if (p->xev_xs) cudaEventDestroy(p->xev_xs);
     if (p->gev_in) cudaEventDestroy(p->gev_in);
     if (p->gev_out) cudaEventDestroy(p->gev_out);
     if (p->plan_r2c_p) cufftDestroy(p->plan_r2c_p);
