@@ -1761,6 +1761,32 @@ __global__ void k_dwin(int na, int nd, int Wwin, const int* __restrict__ d0, con
     dw[o] = (d >= 0 && d < nd) ? rg[(long long)a * nd + d] + s[o] : 0.f;
 }
 
+// global forward projection from tile windows: out[a][d] = sum over tiles (fixed
+// order) of win[t][a][d - d0[t][a]] where inside the window; epilogues as k_fp
+// (mode 1: out = v, aux_out = aux_in + alpha v; mode 2: out = aux_in - v)
+__global__ void k_winsum(int mode, int na, int nd, int Wwin, int ntiles, const int* __restrict__ d0,
+                         const float* __restrict__ win, float* __restrict__ out, const float* __restrict__ aux_in,
+                         float* __restrict__ aux_out, float alpha) {
+    extern __shared__ int sd0[];
+    const int a = blockIdx.y;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) sd0[t] = d0[t * na + a];
+    __syncthreads();
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= nd) return;
+    float acc = 0.f;
+    for (int t = 0; t < ntiles; ++t) {
+        const int w = d - sd0[t];
+        if (w >= 0 && w < Wwin) acc += __ldg(win + ((long long)t * na + a) * Wwin + w);
+    }
+    const long long o = (long long)a * nd + d;
+    if (mode == 2) {
+        out[o] = aux_in[o] - acc;
+    } else {
+        out[o] = acc;
+        if (mode == 1) aux_out[o] = fmaf(alpha, acc, aux_in ? aux_in[o] : 0.f);
+    }
+}
+
 // window -> full sinogram (zero outside the window)
 __global__ void k_scatter_win(int na, int nd, int Wwin, const int* __restrict__ d0,
                               const float* __restrict__ win, float* __restrict__ sino) {

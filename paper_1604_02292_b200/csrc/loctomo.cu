@@ -85,9 +85,12 @@ struct lt_plan {
     // host tables
     std::vector<AngF> angf;
     std::vector<double> cs64, sn64, A64, B64;
-    std::vector<TileT> tiles, gtile;
-    std::vector<int> d0, gd0;
-    std::vector<double> tauc, gtauc;
+    std::vector<TileT> tiles, gtile, ttiles;
+    std::vector<int> d0, gd0, td0;
+    std::vector<double> tauc, gtauc, ttauc;
+    // tiled global forward projection: the grid cut into Tg x Tg tiles, each
+    // projected by the ROI kernel onto its window, windows summed per bin
+    int Tg = 0, TPg = 0, Wg = 0, NTg = 0;
     std::vector<int> fpgroups;    // [ngroups][FP_GA] angle indices of one orientation, -1 padded
     // BP_SUB^2 image blocks that the global x_s^k backprojection must cover: list 0 for
     // all local ROIs, lists 1 and 2 for the two pipelined ROI groups (halves)
@@ -133,6 +136,7 @@ struct lt_plan {
         size_t xsblk[3], xsg[2], lams;
         size_t uhat, phat, fspec, freal, fwork;
         size_t cp_sd, cp_tau, cp_yd, dwin, peers;
+        size_t ttiles, td0, ttauc, tstack, tstackT, twin;
         size_t tt, ttT, tw;
         size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
         size_t total;
@@ -145,6 +149,7 @@ struct lt_plan {
     }
     Tiles roi_tiles() const { return Tiles{T, TP, Wwin, R, P<TileT>(off.tiles), P<int>(off.d0), P<double>(off.tauc)}; }
     Tiles glob_tiles() const { return Tiles{GT, GTP, nd, 1, P<TileT>(off.gtile), P<int>(off.gd0), P<double>(off.gtauc)}; }
+    Tiles tile_tiles() const { return Tiles{Tg, TPg, Wg, NTg, P<TileT>(off.ttiles), P<int>(off.td0), P<double>(off.ttauc)}; }
     long long ytile() const { return (long long)T * TP; }
     long long ptile() const { return (long long)T * T; }
 };
@@ -210,6 +215,33 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
     dim3 grid(p.ngroups, t.ntiles);
     ScopedTimer tm(TC_FP, st);
     k_fp_roi<<<grid, 256, smem, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+// Global forward projection W x of a padded global image (+ twin): the grid is
+// cut into Tg x Tg tiles (k_extract_tiles), every tile is projected onto its
+// detector window by the shared-memory ROI projector (k_fp_roi2), and k_winsum
+// adds the windows per bin in fixed tile order, with the k_fp epilogues
+// (mode 0: W x; 1: Alg. 1 bank update; 2: p - W x).  LT_GFP=direct keeps the
+// single-pass k_fp.
+int global_fp(const lt_plan& p, int mode, const float* img, const float* imgT, float* out, const float* aux_in,
+              float* aux_out, cudaStream_t st) {
+    static int direct = -1;
+    if (direct < 0) { const char* e = getenv("LT_GFP"); direct = (e && !strcmp(e, "direct")) ? 1 : 0; }
+    if (direct || p.TPg > FP2_P || p.Wg > 32 * FP_U)
+        return launch_fp(p, mode, p.glob_tiles(), img, imgT, 0, out, 0, aux_in, aux_out, st);
+    const Tiles tt = p.tile_tiles();
+    float* stack = p.P<float>(p.off.tstack);
+    float* stackT = p.P<float>(p.off.tstackT);
+    float* win = p.P<float>(p.off.twin);
+    const long long ts = (long long)p.Tg * p.TPg;
+    k_extract_tiles<<<dim3((p.Tg + 31) / 32, (p.Tg + 7) / 8, p.NTg), dim3(32, 8), 0, st>>>(
+        p.Tg, p.TPg, tt.tile, img, p.GTP, stack, stackT, ts);
+    LT_LAUNCHED();
+    if (int rc = launch_fp_roi(p, tt, stack, stackT, ts, win, (long long)p.na * p.Wg, st)) return rc;
+    k_winsum<<<dim3((p.nd + 255) / 256, p.na), 256, p.NTg * sizeof(int), st>>>(
+        mode, p.na, p.nd, p.Wg, p.NTg, tt.d0, win, out, aux_in, aux_out, (float)p.alpha);
     LT_LAUNCHED();
     return LT_OK;
 }
@@ -378,7 +410,7 @@ int ensure_wd(lt_plan& p, cudaStream_t st) {
     LT_CUDA(cudaMemsetAsync(giT, 0, gbytes, st));
     k_pack<<<grid2d(p.n, p.n), dim3(32, 8), 0, st>>>(p.n, p.GTP, nullptr, 1, gi, giT);
     LT_LAUNCHED();
-    if (int rc = launch_fp(p, 0, p.glob_tiles(), gi, giT, 0, p.P<float>(p.off.wd), 0, nullptr, nullptr, st)) return rc;
+    if (int rc = global_fp(p, 0, gi, giT, p.P<float>(p.off.wd), nullptr, nullptr, st)) return rc;
     k_rowsum<<<p.na, 256, 0, st>>>(p.nd, p.P<float>(p.off.wd), p.P<double>(p.off.wdsum));
     LT_LAUNCHED();
     p.wd_ready = true;
@@ -556,7 +588,7 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
             float* gx = p.P<float>(p.off.gimg);
             float* gxT = p.P<float>(p.off.gimgT);
             float* r = p.P<float>(p.off.gsino);
-            if (int rc = launch_fp(p, 2, gt, gx, gxT, 0, r, 0, d_sino, nullptr, st)) return rc;
+            if (int rc = global_fp(p, 2, gx, gxT, r, d_sino, nullptr, st)) return rc;
             BpEpi eg = epi0();
             eg.y = gx; eg.yT = gxT; eg.alpha = (float)p.alpha;
             const SinoView sv = view_full(r, p.nd);
@@ -950,6 +982,30 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         p->gd0.assign(n_angles, 0);
         p->gtauc.assign(n_angles, 0.5 * (n_det - 1));
     }
+    // global tiling for the forward projector (same tables as ROI tiles, margin 0)
+    {
+        const int Tg = std::min(256, n);
+        const int h = (Tg + 1) / 2;
+        p->Tg = 2 * h; p->TPg = (p->Tg + PADL + PADR + 3) & ~3; p->Wg = window_width(h);
+        const int nt = (n + p->Tg - 1) / p->Tg;
+        p->NTg = nt * nt;
+        p->ttiles.resize(p->NTg);
+        p->td0.resize((size_t)p->NTg * n_angles);
+        p->ttauc.resize((size_t)p->NTg * n_angles);
+        for (int bi = 0; bi < nt; ++bi)
+            for (int bj = 0; bj < nt; ++bj) {
+                const int q = bi * nt + bj;
+                TileT t;
+                t.row0 = bi * p->Tg; t.col0 = bj * p->Tg;
+                t.vr0 = 0; t.vr1 = std::min(p->Tg, n - t.row0);
+                t.vc0 = 0; t.vc1 = std::min(p->Tg, n - t.col0);
+                t.pad0 = t.pad1 = 0;
+                p->ttiles[q] = t;
+                // tile centre point (x, y) = (col0 + h - N/2, N/2 - row0 - h)
+                tile_window(*p, t.col0 + h - 0.5 * n, 0.5 * n - t.row0 - h, p->Wg, &p->td0[(size_t)q * n_angles],
+                            &p->ttauc[(size_t)q * n_angles]);
+            }
+    }
     // workspace layout
     const size_t fs = sizeof(float);
     const size_t ns = (size_t)n_angles * n_det, R = std::max(p->R, 1);
@@ -964,6 +1020,10 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.cs64 = take(n_angles * 8); f.sn64 = take(n_angles * 8); f.A64 = take(n_angles * 8); f.B64 = take(n_angles * 8);
     f.tiles = take(R * sizeof(TileT)); f.d0 = take(R * n_angles * 4); f.tauc = take(R * n_angles * 8);
     f.gtile = take(sizeof(TileT)); f.gd0 = take(n_angles * 4); f.gtauc = take(n_angles * 8);
+    f.ttiles = take(p->NTg * sizeof(TileT)); f.td0 = take((size_t)p->NTg * n_angles * 4);
+    f.ttauc = take((size_t)p->NTg * n_angles * 8);
+    f.tstack = take((size_t)p->NTg * p->Tg * p->TPg * fs); f.tstackT = take((size_t)p->NTg * p->Tg * p->TPg * fs);
+    f.twin = take((size_t)p->NTg * n_angles * p->Wg * fs);
     f.fpgroups = take(p->fpgroups.size() * 4);
     f.bank = take((size_t)n_iter * ns * fs); f.conv = take((size_t)n_iter * ns * fs);
     f.pc = take(ns * fs); f.wd = take(ns * fs); f.wdsum = take(n_angles * 8); f.psum = take(n_angles * 8);
@@ -1032,6 +1092,12 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(up(p->off.gtile, p->gtile.data(), sizeof(TileT)));
     LT_CUDA(up(p->off.gd0, p->gd0.data(), na * 4));
     LT_CUDA(up(p->off.gtauc, p->gtauc.data(), na * 8));
+    LT_CUDA(up(p->off.ttiles, p->ttiles.data(), p->ttiles.size() * sizeof(TileT)));
+    LT_CUDA(up(p->off.td0, p->td0.data(), p->td0.size() * 4));
+    LT_CUDA(up(p->off.ttauc, p->ttauc.data(), p->ttauc.size() * 8));
+    // the tile stack's padding columns stay zero (k_extract_tiles writes the tile columns only)
+    LT_CUDA(cudaMemsetAsync(p->ws + p->off.tstack, 0, (size_t)p->NTg * p->Tg * p->TPg * sizeof(float), st));
+    LT_CUDA(cudaMemsetAsync(p->ws + p->off.tstackT, 0, (size_t)p->NTg * p->Tg * p->TPg * sizeof(float), st));
     LT_CUDA(up(p->off.fpgroups, p->fpgroups.data(), p->fpgroups.size() * 4));
     for (int l = 0; l < 3; ++l)
         if (!p->xsblk[l].empty()) LT_CUDA(up(p->off.xsblk[l], p->xsblk[l].data(), p->xsblk[l].size() * 4));
@@ -1100,7 +1166,7 @@ int lt_filter_bank(lt_plan* p, void* stream) {
     for (int k = 0; k < p->n_iter; ++k) {
         float* bk = p->P<float>(p->off.bank) + k * ns;
         const float* bprev = k ? bk - ns : nullptr;
-        if (int rc = launch_fp(*p, 1, gt, c, cT, 0, v, 0, bprev, bk, st)) return rc;
+        if (int rc = global_fp(*p, 1, c, cT, v, bprev, bk, st)) return rc;
         if (k + 1 < p->n_iter) {
             BpEpi e = epi0();
             e.y = c; e.yT = cT; e.y_tstride = 0; e.alpha = (float)p->alpha;
@@ -1145,7 +1211,7 @@ int lt_project(const lt_plan* cp, int32_t roi, const float* d_img, float* d_sino
         LT_CUDA(cudaMemsetAsync(giT, 0, gbytes, st));
         k_pack<<<grid2d(p->n, p->n), dim3(32, 8), 0, st>>>(p->n, p->GTP, d_img, 0, gi, giT);
         LT_LAUNCHED();
-        return launch_fp(*p, 0, p->glob_tiles(), gi, giT, 0, d_sino, 0, nullptr, nullptr, st);
+        return global_fp(*p, 0, gi, giT, d_sino, nullptr, nullptr, st);
     }
     float* tt = p->P<float>(p->off.tt);
     float* ttT = p->P<float>(p->off.ttT);
@@ -1301,7 +1367,7 @@ int lt_global_sirt(lt_plan* p, const float* d_sino, int32_t n_iter, float lo, fl
     LT_CUDA(cudaMemsetAsync(xT, 0, gbytes, st));
     const Tiles gt = p->glob_tiles();
     for (int k = 0; k < n_iter; ++k) {
-        if (int rc = launch_fp(*p, 2, gt, x, xT, 0, r, 0, d_sino, nullptr, st)) return rc;   // r = p - W x
+        if (int rc = global_fp(*p, 2, x, xT, r, d_sino, nullptr, st)) return rc;   // r = p - W x
         BpEpi e = epi0();
         e.y = x; e.yT = xT; e.alpha = (float)p->alpha; e.lo = lo; e.hi = hi;
         const SinoView sv = view_full(r, p->nd);
@@ -1336,7 +1402,7 @@ int lt_global_tv(lt_plan* p, const float* d_sino, int32_t n_iter, float lambda, 
     const dim3 g2 = grid2d(n, n), b2(32, 8);
     double tk = 1.0;
     for (int k = 0; k < n_iter; ++k) {
-        if (int rc = launch_fp(*p, 2, gt, xm, xmT, 0, r, 0, d_sino, nullptr, st)) return rc;
+        if (int rc = global_fp(*p, 2, xm, xmT, r, d_sino, nullptr, st)) return rc;
         BpEpi e = epi0();
         e.y = xm; e.out = v; e.alpha = (float)p->alpha;
         const SinoView sv = view_full(r, p->nd);
@@ -1402,7 +1468,7 @@ int lt_exterior_solve(lt_plan* p, const float* d_sino, float lo, float hi, float
     LT_LAUNCHED();
     // 2. r_g = p - W xg on the full sinogram
     float* rg = P.P<float>(P.off.gsino);
-    if (int rc = launch_fp(P, 2, gt, gx, gxT, 0, rg, 0, d_sino, nullptr, st)) return rc;
+    if (int rc = global_fp(P, 2, gx, gxT, rg, d_sino, nullptr, st)) return rc;
     // 3. per ROI: p~ = r_g + W_{L'} xg on the window, x_d = alpha W_{L'}^T p~
     Tiles t = P.roi_tiles();
     const long long yts = P.ytile();
@@ -1474,7 +1540,7 @@ int lt_global_cp(lt_plan* p, const float* d_sino, int32_t n_iter, float mu, floa
     LT_CUDA(cudaMemsetAsync(g, 0, nn * sizeof(float), st));
     k_pack<<<g2, b2, 0, st>>>(n, p->GTP, nullptr, 2, xb, xbT);            // ones image
     LT_LAUNCHED();
-    if (int rc = launch_fp(*p, 0, gt, xb, xbT, 0, s, 0, nullptr, nullptr, st)) return rc;
+    if (int rc = global_fp(*p, 0, xb, xbT, s, nullptr, nullptr, st)) return rc;
     k_cp_recip<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(ns, s, sd);
     LT_LAUNCHED();
     k_fill<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(ns, 1.f, s);
@@ -1495,7 +1561,7 @@ int lt_global_cp(lt_plan* p, const float* d_sino, int32_t n_iter, float mu, floa
     LT_CUDA(cudaMemsetAsync(yq, 0, nn * sizeof(float), st));
     LT_CUDA(cudaMemsetAsync(yd, 0, ns * sizeof(float), st));
     for (int k = 0; k < n_iter; ++k) {
-        if (int rc = launch_fp(*p, 0, gt, xb, xbT, 0, s, 0, nullptr, nullptr, st)) return rc;     // W xbar
+        if (int rc = global_fp(*p, 0, xb, xbT, s, nullptr, nullptr, st)) return rc;     // W xbar
         k_cp_dual<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(ns, s, d_sino, sd, yd);
         LT_LAUNCHED();
         k_cp_tvdual<<<g2, b2, 0, st>>>(n, p->GTP, mu, xb, yp, yq);
