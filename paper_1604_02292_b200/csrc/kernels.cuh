@@ -477,9 +477,7 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
 // NS = 0: no gather (y = 0 at k = 1), NS = 1: one sinogram.
 // ---------------------------------------------------------------------------
 constexpr int BP_CA = 32;   // angles per staged chunk
-constexpr int BP_SUB = 64;  // sub-tile side (pixels)
-constexpr int BP_PR = 8;    // rows per thread (x 2 columns, 32 apart)
-constexpr int BP_SW = 96;   // bins per angle per sub-tile (>= 63*sqrt2 + 4), a multiple of 32
+constexpr int BP_SUB = 64;  // default sub-tile side (pixels); 32 for small ROI batches
 
 enum BpMode {
     BP_PLAIN_TILE = 0,   // out plain [tile][T][T]  (stage-wise parity, lt_backproject)
@@ -502,29 +500,33 @@ struct BpEpi {
     float alpha, lo, hi; int last;
 };
 
-template <int NS, int MODE>
+template <int NS, int MODE, int SUB = BP_SUB>
 __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoView s2, BpEpi e) {
     static_assert(NS == 0 || NS == 1, "one gathered sinogram at most");
+    static_assert(SUB == 64 || SUB == 32, "64x64 (2 columns x 8 rows per thread) or 32x32 (1 x 4) sub-tiles");
+    constexpr int COLS = SUB / 32;                // columns per thread (32 apart)
+    constexpr int BP_PR = SUB * SUB / (256 * COLS);   // rows per thread
+    constexpr int BP_SW = SUB == 64 ? 96 : 64;        // window bins (>= (SUB-1) sqrt2 + 4, a multiple of 32)
     __shared__ float2 sw[BP_CA][BP_SW];          // (v[m], v[m+1]) / c_a, m relative to the window centre
     __shared__ float4 sa[BP_CA];                 // (cos, sin, K' = 1 - 1/(2c), 1/c)
     __shared__ float sanch[BP_CA];
 
     const int r = blockIdx.y;
     const int T = t.T, na = g.na;
-    const int nsx = (T + BP_SUB - 1) / BP_SUB;
+    const int nsx = (T + SUB - 1) / SUB;
     const int sub = e.blist ? __ldg(e.blist + blockIdx.x) : (int)blockIdx.x;
     const int sty = sub / nsx, stx = sub - sty * nsx;
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    const int pj0 = stx * BP_SUB + lane;                  // columns pj0, pj0 + 32
-    const int pi0 = sty * BP_SUB + wq * BP_PR;            // rows pi0 .. pi0 + BP_PR - 1
+    const int pj0 = stx * SUB + lane;                  // columns pj0, pj0 + 32
+    const int pi0 = sty * SUB + wq * BP_PR;            // rows pi0 .. pi0 + BP_PR - 1
     const double Lc = 0.5 * (T - 1);
-    const double hs = 0.5 * (BP_SUB - 1);
-    const double dxc = stx * BP_SUB + hs - Lc, dyc = sty * BP_SUB + hs - Lc;
+    const double hs = 0.5 * (SUB - 1);
+    const double dxc = stx * SUB + hs - Lc, dyc = sty * SUB + hs - Lc;
     const float dx = (float)lane - (float)hs, dy0 = (float)(wq * BP_PR) - (float)hs;
 
-    float2 acc[2][BP_PR];                         // (left-tap, right-tap) partial sums per pixel
+    float2 acc[COLS][BP_PR];                      // (left-tap, right-tap) partial sums per pixel
     #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < COLS; ++h)
         #pragma unroll
         for (int p = 0; p < BP_PR; ++p) acc[h][p] = make_float2(0.f, 0.f);
     // Staging, software-pipelined: the next chunk's window bins are loaded into
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
             const float t00 = fmaf(dx, A4.x, fmaf(-dy0, A4.y, sanch[q]));   // column pj0, row pi0
             const unsigned rowb = opaque_u32(swbase + (unsigned)(q * BP_SW * 8));
             #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < COLS; ++h) {
                 const float t0 = h ? fmaf(32.f, A4.x, t00) : t00;
                 #pragma unroll
                 for (int p = 0; p < BP_PR; p += 2) {
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     const TileT ti = t.tile[r];
     const int n = g.n;
     #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < COLS; ++h) {
     const int pj = pj0 + 32 * h;
     float g1[BP_PR];
     #pragma unroll

@@ -77,6 +77,7 @@ struct lt_plan {
     int n = 0, na = 0, nd = 0, nroi_all = 0, radius = 0, margin = 0, h = 0;
     int T = 0, TP = 0, Wwin = 0, n_iter = 0, flags = 0, rank = 0, world = 1;
     int GT = 0, GTP = 0;          // global tile (whole image)
+    int num_sms = 148;            // of the bound device (launch sizing)
     double alpha = 0.0;
     std::vector<double> ang;
     std::vector<int> cen;         // [nroi_all][2]
@@ -246,14 +247,22 @@ int global_fp(const lt_plan& p, int mode, const float* img, const float* imgT, f
     return LT_OK;
 }
 
+// 64 x 64 sub-tiles per CTA; 32 x 32 when a batch would give fewer than about
+// two waves of 64 x 64 CTAs (small ROI counts: C2, C3, 8-GPU shards), so the
+// SMs stay busy (block lists are always in 64 x 64 units)
 template <int NS, int MODE>
 int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const SinoView& s2, const BpEpi& e,
                 cudaStream_t st, int nblist = 0) {
-    const int nsx = (t.T + BP_SUB - 1) / BP_SUB;
     if (e.blist && nblist == 0) return LT_OK;
-    dim3 grid(e.blist ? nblist : nsx * nsx, t.ntiles);
+    const int nsx = (t.T + BP_SUB - 1) / BP_SUB;
+    const long long ctas64 = e.blist ? nblist : (long long)nsx * nsx * t.ntiles;
     ScopedTimer tm(TC_BP, st);
-    k_bp<NS, MODE><<<grid, 256, 0, st>>>(p.geo(), t, s1, s2, e);
+    if (!e.blist && ctas64 < 2LL * 3 * p.num_sms) {
+        const int nsx32 = (t.T + 31) / 32;
+        k_bp<NS, MODE, 32><<<dim3(nsx32 * nsx32, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
+    } else {
+        k_bp<NS, MODE, BP_SUB><<<dim3(e.blist ? nblist : nsx * nsx, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
+    }
     LT_LAUNCHED();
     return LT_OK;
 }
@@ -386,7 +395,12 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
             const char* e = getenv("LT_FGP2_CFG");
             cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : !strcmp(e, "2x16b") ? 3 : 0;
         }
-        if (cfgv == 1) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
+        // small batches: 16-row CTAs (twice the CTAs per tile) while the 32-row
+        // layout would not fill one wave of SMs
+        int nsm = 148;
+        { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
+        const bool small = ntiles * ((rows + 31) / 32) < nsm && rows > 16;
+        if (cfgv == 1 || (cfgv == 0 && small && (rows + 15) / 16 <= 16)) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
         if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
         if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, 0, true>(A, rows, ntiles, st);
         return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
@@ -1077,6 +1091,11 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     if (((uintptr_t)d_ws) & 255) return fail(LT_ERR_INVALID, "workspace must be 256-byte aligned");
     cudaStream_t st = (cudaStream_t)stream;
     p->ws = (char*)d_ws;
+    {
+        int dev = 0;
+        LT_CUDA(cudaGetDevice(&dev));
+        LT_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
     auto up = [&](size_t o, const void* src, size_t bytes_) {
         return cudaMemcpyAsync(p->ws + o, src, bytes_, cudaMemcpyHostToDevice, st);
     };
