@@ -162,150 +162,18 @@ __global__ void __launch_bounds__(128) k_fp(Geo g, Tiles t, FpArgs f) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// Forward projection W_{L'} for a batch of ROI tiles, shared-memory staged.
-// CTA = (tile r, group of up to FP_GA angles of one orientation); the CTA's
-// 256 threads own the group's rays (angle-major, window bins consecutive in
-// a warp).  The tile is streamed through shared memory in bands of FP_BL
-// lines (rows of y for row-driven angles, rows of the transposed twin for
-// column-driven ones; cp.async double buffering), and every ray accumulates
-// its Joseph taps for the lines of the band it crosses.  Same arithmetic as
-// k_fp (fp64 anchor per ray and band, fp32 offsets < 34 px).
-// ---------------------------------------------------------------------------
-constexpr int FP_GA = 8;     // angles per CTA (one warp per angle)
-constexpr int FP_BL = 16;    // lines per staged band
+constexpr int FP_GA = 8;     // angles per CTA of the ROI forward projector (one warp per angle)
 constexpr int FP_U = 12;     // rays per lane: window width <= 32 * FP_U
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-constexpr int FP_P = 264;    // shared-memory band pitch (floats): tiles up to T = 256
-
-// one ray through the 32 lines of a staged band: Joseph taps at
-// pos(i) = base + f0 + 0.5 + i*B, fully unrolled, row offsets are immediates
+// keeps ptxas from re-materialising a folded address bias (a mov it cannot see through)
 __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
     unsigned y;
-    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));   // keeps ptxas from splitting the folded bias
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
     return y;
 }
 
-template <bool CLAMP>
-__device__ __forceinline__ float fp_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
-    // a shuffled copy is not rematerialized by ptxas, so the folded bias stays in one register
-    const unsigned rowbase = __shfl_sync(0xffffffffu, rowbase_, threadIdx.x & 31);
-    float acc = 0.f;
-    #pragma unroll
-    for (int i = 0; i < FP_BL; ++i) {
-        float tt = fmaf((float)i, Bf, f0);
-        if (CLAMP) tt = fminf(fmaxf(tt, lo), hi);
-        const float rm = tt + MAGICF;
-        unsigned addr;
-        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(__float_as_int(rm)), "r"(rowbase));
-        const float gg = tt - (rm - MAGICF);
-        float v0, v1;
-        const unsigned ai = addr + (unsigned)(i * FP_P * 4);
-        asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];" : "=f"(v0), "=f"(v1) : "r"(ai));
-        acc = fmaf(0.5f, v0 + v1, acc);
-        acc = fmaf(gg, v1 - v0, acc);
-    }
-    return acc;
-}
-
-__global__ void __launch_bounds__(256) k_fp_roi(Geo g, Tiles t, FpArgs f, const int* __restrict__ groups) {
-    extern __shared__ float4 smf4[];
-    float* band = reinterpret_cast<float*>(smf4);          // [2][FP_BL][FP_P]
-    const int r = blockIdx.y, grp = blockIdx.x;
-    const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a = groups[grp * FP_GA + warp];                 // this warp's angle (-1: idle warp)
-    const int a0 = groups[grp * FP_GA];
-    const int col = g.ang[a0].col;
-    const TileT ti = t.tile[r];
-    const int lv0 = col ? ti.vc0 : ti.vr0, lv1 = col ? ti.vc1 : ti.vr1;
-    const int pv0 = col ? ti.vr0 : ti.vc0, pv1 = col ? ti.vr1 : ti.vc1;
-    const double Lc = 0.5 * (T - 1);
-    const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
-    double A = 0.0, B = 0.0, tauc = 0.0;
-    int d0 = 0;
-    if (a >= 0) {
-        A = g.A64[a]; B = g.B64[a];
-        tauc = t.tauc[r * na + a];
-        d0 = __ldg(t.d0 + r * na + a);
-    }
-    const float Bf = (float)B;
-    __shared__ float sacc[FP_GA][32 * FP_U];                 // per-ray accumulators
-    for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += 256) (&sacc[0][0])[e] = 0.f;
-    float* acc = sacc[warp];
-
-    const int q4 = TP / 4;       // float4 per staged line
-    auto stage = [&](int buf, int l0) {
-        float* dst = band + buf * FP_BL * FP_P;
-        const int nl = min(FP_BL, T - l0);
-        const float* s0 = src + (long long)l0 * TP;
-        for (int e = threadIdx.x; e < FP_BL * q4; e += 256) {
-            const int line = e / q4, c4 = e - line * q4;
-            if (line < nl) cp_async16(dst + line * FP_P + c4 * 4, s0 + (long long)line * TP + c4 * 4);
-            else reinterpret_cast<float4*>(dst + line * FP_P)[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        cp_async_commit();
-    };
-    const int lbeg = (lv0 / FP_BL) * FP_BL;
-    if (lbeg < lv1) stage(0, lbeg);
-    int buf = 0;
-    for (int l0 = lbeg; l0 < lv1; l0 += FP_BL, buf ^= 1) {
-        if (l0 + FP_BL < lv1) { stage(buf ^ 1, l0 + FP_BL); cp_async_wait<1>(); }
-        else cp_async_wait<0>();
-        __syncthreads();
-        if (a >= 0) {
-            const unsigned sbase = (unsigned)__cvta_generic_to_shared(band + buf * FP_BL * FP_P + PADL);
-            const double Bl = (double)(FP_BL - 1) * B;
-            #pragma unroll 1
-            for (int u = 0; u < FP_U; ++u) {
-                const int w = lane + 32 * u;
-                const int d = d0 + w;
-                const bool ray = w < Wwin && d >= 0 && d < g.nd;
-                // position (pixel index along the line) of the ray at the band's first line
-                const double p0 = Lc + ((double)w - tauc) * A + ((double)l0 - Lc) * B;
-                const double pmin = fmin(p0, p0 + Bl), pmax = fmax(p0, p0 + Bl);
-                const bool useful = ray && pmax > pv0 - 2.0 && pmin < (double)pv1 + 1.0;
-                if (!__any_sync(0xffffffffu, useful)) continue;
-                const bool safe = pmin >= -3.0 && pmax <= (double)T + 1.5;
-                const double fb = floor(p0);
-                // lanes without a useful ray read a fixed in-bounds spot (pos = 0, step 0)
-                const int ib = useful ? (int)fb : 0;
-                const float f0 = useful ? (float)(p0 - fb) - 0.5f : -0.5f;
-                const float Bu = useful ? Bf : 0.f;
-                // rowbase folds the magic-number bias: addr = rowbase + 4*bits(tt + MAGIC)
-                const unsigned rowbase = sbase + 4u * (unsigned)(ib - MAGICI);
-                float v;
-                if (__all_sync(0xffffffffu, safe || !useful)) {
-                    v = fp_band_ray<false>(rowbase, f0, Bu, 0.f, 0.f);
-                } else {
-                    // clamp into the zero padding: pos in [-3, T + 2) relative to ib
-                    const float lo = (float)(-3 - ib) - 0.5f, hi = (float)(T + 2 - ib) - 0.5f;
-                    v = fp_band_ray<true>(rowbase, f0, Bu, lo, hi);
-                }
-                if (useful) acc[w] += v;
-            }
-        }
-        __syncthreads();
-    }
-    if (a >= 0) {
-        const float invc = g.ang[a].invc;
-        for (int w = lane; w < Wwin; w += 32) {
-            const int d = d0 + w;
-            f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = (d >= 0 && d < g.nd) ? acc[w] * invc : 0.f;
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
-// k_fp_roi2: the same W_{L'} as k_fp_roi, restructured for the sm_100 FP32
+// k_fp_roi2: W_{L'} for a batch of ROI tiles, built for the sm_100 FP32
 // datapath and the shared-memory crossbar:
 //  * the band is staged as interpolation pairs (S[m], D[m]) = (v[m] + v[m+1],
 //    v[m+1] - v[m]) (one 64-bit entry per pixel, built once per band and shared
@@ -703,24 +571,14 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
 // ---------------------------------------------------------------------------
 // FGP TV prox (Beck & Teboulle, named at P:L661-663; A13/A14),
 // anisotropic, Neumann boundary on each tile's valid rectangle, fused with
-// the FISTA update of Alg. 3 (lines 7-9, corrected per A12).
-//
-// One thread-block CLUSTER per tile, all FGP state in REGISTERS for all n_FGP
-// iterations.  Thread (j, g) of CTA k owns column j of a strip of FR = 16
-// consecutive rows (strip index k*G + g): b, r, s, p, q, z are 16-entry
-// register arrays.  Neighbours: row above/below = same thread (register) or
-// the adjacent strip's halo row in shared memory -- the CTA's own (g +- 1) or
-// the neighbour CTA's via DSMEM; column left/right = warp shuffle, or the
-// adjacent warp's lane-0/31 halo column in shared memory.  Two cluster
-// barriers per FGP iteration (z needs r above / s left; the dual step needs
-// z below / z right); halos are double buffered by iteration parity.
+// the FISTA update of Alg. 3 (lines 7-9, corrected per A12): arguments, the
+// momentum table and the cluster (DSMEM / mbarrier) helpers of k_fgp2.
 // ---------------------------------------------------------------------------
 
 struct FgpArgs {
     const float* b; int b_pitch; long long b_tstride;   // input image(s)
     const TileT* tiles;                                 // valid rect per tile (nullable: whole H x W)
     int H, W;                                           // when tiles == nullptr
-    int G, NTW;                                         // strips per CTA, threads per strip row (32 | NTW)
     float lam; int nfgp;
     const float* lams;                                  // nullable: per-tile lambda (lambda sweep, NEXT-1)
     float* out; int out_pitch; long long out_tstride;   // MODE 0
@@ -736,20 +594,6 @@ __device__ __forceinline__ float clip1(float v) { return fminf(1.f, fmaxf(-1.f, 
 // t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2 (Beck & Teboulle), computed on the host in fp64
 constexpr int FGP_MAX_IT = 4096;
 __constant__ float c_fgp_beta[FGP_MAX_IT];
-
-// Cluster barrier between the FGP phases.  LT_FGP_BARRIER 0: cg cluster.sync()
-// (release/acquire at cluster scope; ptxas emits MEMBAR.ALL.GPU);
-// 1: CTA-scope fence + relaxed arrive + acquire wait (experiment).
-#ifndef LT_FGP_BARRIER
-#define LT_FGP_BARRIER 0
-#endif
-__device__ __forceinline__ void fgp_cluster_barrier(cg::cluster_group& cl) {
-#if LT_FGP_BARRIER == 1
-    asm volatile("fence.acq_rel.cta;\n\tbarrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-#else
-    cl.sync();
-#endif
-}
 
 // DSMEM push with transaction-count completion (sm_90+): a producer stores one
 // float into a neighbour CTA's shared memory and the bytes complete on the
@@ -776,255 +620,6 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
         "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
-}
-
-// The duals are stored shifted, p' = (p + 1)/2 in [0, 1] (likewise q, r, s):
-// the projection onto [-1, 1] becomes the .SAT modifier of one FFMA, the
-// FGP momentum is affine-invariant, and L(p, q) = 2 L(p', q') because the
-// constant shifts cancel in the divergence.  A dual that does not exist
-// (outside the valid rectangle, last row / column) is p' = 1/2.
-template <int MODE, int FR, int NT>
-__global__ void __launch_bounds__(NT, 1) k_fgp(FgpArgs A) {
-    extern __shared__ __align__(16) float sm[];
-    cg::cluster_group cl = cg::this_cluster();
-    const int K = (int)cl.num_blocks();
-    const int kr = (int)cl.block_rank();
-    const int tile = blockIdx.y;
-    int vr0 = 0, vc0 = 0, Hv = A.H, Wv = A.W;
-    if (A.tiles) {
-        const TileT ti = A.tiles[tile];
-        vr0 = ti.vr0; vc0 = ti.vc0; Hv = ti.vr1 - ti.vr0; Wv = ti.vc1 - ti.vc0;
-    }
-    const int G = A.G, NTW = A.NTW, nw = NTW >> 5;
-    const int j = threadIdx.x, g = threadIdx.y;
-    const int lane = j & 31, warp = j >> 5;
-    const int i0 = (kr * G + g) * FR;
-    const bool colv = j < Wv;
-    const bool has_up = kr > 0, has_dn = kr < K - 1;
-    // shared memory
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm);   // [0,1] r from above, [2,3] z from below
-    float* rx_r = sm + 8;                    // [2][NTW] last r row of the CTA above (st.async target)
-    float* rx_z = rx_r + 2 * NTW;            // [2][NTW] first z row of the CTA below
-    float* hr = rx_z + 2 * NTW;              // [2][G][NTW] last row of r per strip
-    float* hz = hr + 2 * G * NTW;            // [2][G][NTW] first row of z per strip
-    float* hp = hz + 2 * G * NTW;            // [G][NTW]    last row of p (epilogue)
-    float* cs = hp + G * NTW;                // [2][G][nw+1][FR] slot w+1: lane-31 column of s of warp w; slot 0 zero
-    float* cz = cs + 2 * G * (nw + 1) * FR;  // [2][G][nw+1][FR] slot w: lane-0 column of z of warp w; slot nw zero
-    float* cq = cz + 2 * G * (nw + 1) * FR;  // [G][nw][FR]    lane-31 column of q (epilogue)
-    const int nzero = 4 * NTW + 5 * G * NTW + 4 * G * (nw + 1) * FR + G * nw * FR;
-    const int tid = g * NTW + j, nthr = NTW * G;
-    for (int e = tid; e < nzero; e += nthr) {
-        // z halos (rx_z, hz, cz) start at 0; dual halos (rx_r, hr, hp, cs, cq) at the shifted zero 1/2
-        const float* a_ = rx_r + e;
-        const bool zbuf = (a_ >= rx_z && a_ < rx_z + 2 * NTW) || (a_ >= hz && a_ < hz + 2 * G * NTW) ||
-                          (a_ >= cz && a_ < cz + 2 * G * (nw + 1) * FR);
-        rx_r[e] = zbuf ? 0.f : 0.5f;
-    }
-    if (tid == 0) {
-        for (int q_ = 0; q_ < 4; ++q_) mbar_init(smem_u32(bars + q_), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-
-    // 1024-thread CTAs (NT = 1024, full 256-column tiles) keep b in shared memory
-    // to stay within 64 registers; the others keep it in registers
-    // 1024-thread CTAs (NT = 1024, full 256-column tiles, 32 rows per CTA) keep
-    // b, p, q in shared memory (each is touched once per iteration) and r, s, z
-    // in registers, to stay within 64 registers; the others keep all in registers
-    constexpr bool BSM = NT >= 1024;
-    constexpr int BNT = 256;                    // NTW of the BSM variant
-    float breg[BSM ? 1 : FR], r[FR], s[FR], preg[BSM ? 1 : FR], qreg[BSM ? 1 : FR], z[FR];
-    float* bsm = cq + G * nw * FR + (g * FR) * BNT + j;     // [G][FR][256] (BSM only)
-    float* psm = bsm + G * FR * BNT;                          // [G][FR][256]
-    float* qsm = psm + G * FR * BNT;                          // [G][FR][256]
-    auto bval = [&](int k) -> float { if constexpr (BSM) return bsm[k * BNT]; else return breg[k]; };
-    auto pval = [&](int k) -> float { if constexpr (BSM) return psm[k * BNT]; else return preg[k]; };
-    auto qval = [&](int k) -> float { if constexpr (BSM) return qsm[k * BNT]; else return qreg[k]; };
-    auto pset = [&](int k, float v) { if constexpr (BSM) psm[k * BNT] = v; else preg[k] = v; };
-    auto qset = [&](int k, float v) { if constexpr (BSM) qsm[k * BNT] = v; else qreg[k] = v; };
-    const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)(vr0 + i0) * A.b_pitch + vc0 + j;
-    #pragma unroll
-    for (int k = 0; k < FR; ++k) {
-        const float bv = (colv && i0 + k < Hv) ? __ldg(bsrc + (long long)k * A.b_pitch) : 0.f;
-        if constexpr (BSM) bsm[k * BNT] = bv; else breg[k] = bv;
-        r[k] = 0.5f; s[k] = 0.5f; pset(k, 0.5f); qset(k, 0.5f);
-    }
-    // step sizes with the boundary masks folded in: gamma = 0 where the dual
-    // component does not exist (p: rows >= Hv-1 or invalid column; q: column
-    // >= Wv-1 or invalid row); a dual that starts at 0 with step 0 stays 0.
-    const float lam = A.lams ? __ldg(A.lams + tile) : A.lam;
-    const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
-    const float gam = lam > 0.f ? 1.f / (16.f * lam) : 0.f;   // step 1/(8 lam) on p = 2p' - 1
-    const float gq_col = (j < Wv - 1) ? gam : 0.f;
-    const float gp_col = colv ? gam : 0.f;
-    const int kp = Hv - 1 - i0;                 // rows k < kp have p
-    const int kq = Hv - i0;                     // rows k < kq have q
-    cl.sync();
-    const unsigned up_rank = has_up ? kr - 1 : kr, dn_rank = has_dn ? kr + 1 : kr;
-    // remote targets: my last strip pushes r to the CTA below, my first strip pushes z to the CTA above
-    const unsigned rem_rx_r = mapa(smem_u32(rx_r + j), dn_rank);
-    const unsigned rem_bar_r = mapa(smem_u32(bars + 0), dn_rank);
-    const unsigned rem_rx_z = mapa(smem_u32(rx_z + j), up_rank);
-    const unsigned rem_bar_z = mapa(smem_u32(bars + 2), up_rank);
-    const unsigned row_bytes = NTW * 4;
-    const int hstride = G * NTW;
-    const int cstride = G * (nw + 1) * FR;
-    const int nit = lam > 0.f ? A.nfgp : 0;
-    const unsigned bar0 = smem_u32(bars);     // r from above: bar0 + 8*parity; z from below: bar0 + 16 + 8*parity
-    // one FGP iteration; CB = parity of the iteration (compile time, so every
-    // halo address below is loop invariant)
-    auto fgp_iter = [&](int it, auto cbc) {
-        constexpr int cb = decltype(cbc)::value, pb = cb ^ 1;
-        if (tid == 0) {
-            if (has_dn) mbar_expect_tx(bar0 + 16 + 8 * cb, row_bytes);   // z row of it, from below
-            if (has_up) mbar_expect_tx(bar0 + 8 * cb, row_bytes);        // r row of it, from above
-        }
-        // ---- phase A: z = b - lam L(r, s)
-        {
-            // lane 0 reads the halo slot of this warp, the others the zero pad slot
-            const float4* csl = reinterpret_cast<const float4*>(cs + pb * cstride + (g * (nw + 1) + (lane == 0 ? warp : 0)) * FR);
-            #pragma unroll
-            for (int k = 0; k < FR; k += 4) {
-                const float4 h = csl[k / 4];
-                const float hv[4] = {h.x, h.y, h.z, h.w};
-                #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float sh = __shfl_up_sync(0xffffffffu, s[k + e], 1);
-                    z[k + e] = lane == 0 ? hv[e] : sh;
-                }
-            }
-        }
-        // row 0 first (it needs the row above, possibly from the CTA above) and push
-        // it at once, so the exchange overlaps rows 1..FR-1
-        {
-            float rabove = 0.5f;
-            if (g > 0) {
-                rabove = hr[pb * hstride + (g - 1) * NTW + j];
-            } else if (has_up && it > 0) {
-                mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
-                rabove = rx_r[pb * NTW + j];
-            }
-            z[0] = bval(0) - lam2 * (r[0] + s[0] - rabove - z[0]);
-            if (g == 0 && has_up) st_async_f32(rem_rx_z + cb * row_bytes, z[0], rem_bar_z + cb * 8);
-            hz[cb * hstride + g * NTW + j] = z[0];
-        }
-        #pragma unroll
-        for (int k = 1; k < FR; ++k) z[k] = bval(k) - lam2 * (r[k] + s[k] - r[k - 1] - z[k]);
-        if (lane == 0) {
-            float* czw = cz + cb * cstride + (g * (nw + 1) + warp) * FR;
-            #pragma unroll
-            for (int k = 0; k < FR; k += 4) *reinterpret_cast<float4*>(czw + k) = make_float4(z[k], z[k + 1], z[k + 2], z[k + 3]);
-        }
-        __syncthreads();
-        // ---- phase B: dual ascent, projection on [-1,1], FGP momentum
-        const float beta = c_fgp_beta[it];
-        float zr[FR];
-        {
-            // lane 31 reads the next warp's slot, the others the zero pad slot after the last warp
-            const float4* czr = reinterpret_cast<const float4*>(cz + cb * cstride + (g * (nw + 1) + (lane == 31 ? warp + 1 : nw)) * FR);
-            #pragma unroll
-            for (int k = 0; k < FR; k += 4) {
-                const float4 h = czr[k / 4];
-                const float hv[4] = {h.x, h.y, h.z, h.w};
-                #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float zh = __shfl_down_sync(0xffffffffu, z[k + e], 1);
-                    zr[k + e] = lane == 31 ? hv[e] : zh;
-                }
-            }
-        }
-        // last row first (it needs the row below, possibly from the CTA below) and push it
-        {
-            constexpr int k = FR - 1;
-            float zbelow = 0.f;
-            if (g < G - 1) {
-                zbelow = hz[cb * hstride + (g + 1) * NTW + j];
-            } else if (has_dn) {
-                mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
-                zbelow = rx_z[cb * NTW + j];
-            }
-            const float gp = k < kp ? gp_col : 0.f;
-            const float gq = k < kq ? gq_col : 0.f;
-            const float pn = __saturatef(fmaf(gp, z[k] - zbelow, r[k]));
-            const float qn = __saturatef(fmaf(gq, z[k] - zr[k], s[k]));
-            r[k] = fmaf(beta, pn - pval(k), pn);
-            s[k] = fmaf(beta, qn - qval(k), qn);
-            pset(k, pn);
-            qset(k, qn);
-            if (g == G - 1 && has_dn) st_async_f32(rem_rx_r + cb * row_bytes, r[k], rem_bar_r + cb * 8);
-            hr[cb * hstride + g * NTW + j] = r[k];
-        }
-        if (kq >= FR && kp >= FR) {             // interior strip: no row masks
-            #pragma unroll
-            for (int k = 0; k < FR - 1; ++k) {
-                const float pn = __saturatef(fmaf(gp_col, z[k] - z[k + 1], r[k]));
-                const float qn = __saturatef(fmaf(gq_col, z[k] - zr[k], s[k]));
-                r[k] = fmaf(beta, pn - pval(k), pn);
-                s[k] = fmaf(beta, qn - qval(k), qn);
-                pset(k, pn);
-                qset(k, qn);
-            }
-        } else {
-            #pragma unroll
-            for (int k = 0; k < FR - 1; ++k) {
-                const float gp = k < kp ? gp_col : 0.f;
-                const float gq = k < kq ? gq_col : 0.f;
-                const float pn = __saturatef(fmaf(gp, z[k] - z[k + 1], r[k]));
-                const float qn = __saturatef(fmaf(gq, z[k] - zr[k], s[k]));
-                r[k] = fmaf(beta, pn - pval(k), pn);
-                s[k] = fmaf(beta, qn - qval(k), qn);
-                pset(k, pn);
-                qset(k, qn);
-            }
-        }
-        if (lane == 31) {
-            float* csw = cs + cb * cstride + (g * (nw + 1) + warp + 1) * FR;
-            #pragma unroll
-            for (int k = 0; k < FR; k += 4) *reinterpret_cast<float4*>(csw + k) = make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]);
-        }
-        __syncthreads();
-    };
-    int it = 0;
-    for (; it + 1 < nit; it += 2) {
-        fgp_iter(it, std::integral_constant<int, 0>{});
-        fgp_iter(it + 1, std::integral_constant<int, 1>{});
-    }
-    if (it < nit) fgp_iter(it, std::integral_constant<int, 0>{});
-    // ---- x = b - lam L(p, q), then the epilogue
-    float p[FR], q[FR];
-    #pragma unroll
-    for (int k = 0; k < FR; ++k) { p[k] = pval(k); q[k] = qval(k); }
-    hp[g * NTW + j] = p[FR - 1];
-    if (lane == 31) {
-        #pragma unroll
-        for (int k = 0; k < FR; ++k) cq[(g * nw + warp) * FR + k] = q[k];
-    }
-    cl.sync();
-    const float* hp_up = g > 0 ? hp + (g - 1) * NTW : (has_up ? cl.map_shared_rank(hp, kr - 1) + (G - 1) * NTW : nullptr);
-    const float pabove = hp_up ? hp_up[j] : 0.5f;
-    const float* cql = cq + (g * nw + warp - 1) * FR;
-    #pragma unroll
-    for (int k = 0; k < FR; ++k) {
-        const float pup = k > 0 ? p[k - 1] : pabove;
-        float ql = __shfl_up_sync(0xffffffffu, q[k], 1);
-        if (lane == 0) ql = warp > 0 ? cql[k] : 0.5f;
-        const float x = bval(k) - lam2 * (p[k] + q[k] - pup - ql);
-        const int i = i0 + k;
-        if (colv && i < Hv) {
-            if (MODE == 0) {
-                A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + j] = x;
-            } else {
-                const int ti_ = vr0 + i, tj = vc0 + j;                 // tile-local coords
-                const long long pl = (long long)tile * A.p_tstride + (long long)ti_ * A.T + tj;
-                const float xp = A.xprev[pl];
-                const float rr = x + A.beta_o * (x - xp);             // FISTA extrapolation (A12)
-                const float yv = rr - A.xs[pl];                         // x_L^k = r - x_s^k
-                A.xprev[pl] = x;
-                A.y[(long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + tj] = yv;
-                A.yT[(long long)tile * A.y_tstride + (long long)tj * A.TP + PADL + ti_] = yv;
-            }
-        }
-    }
-    cl.sync();   // keep shared memory alive until every neighbour has read its halo
 }
 
 // ---------------------------------------------------------------------------

@@ -192,30 +192,18 @@ int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, cons
     return LT_OK;
 }
 
-// ROI-batch forward projection (shared-memory staged; falls back to the
-// direct-read kernel when the staged band would not fit)
+// ROI-batch forward projection (shared-memory staged k_fp_roi2; the
+// single-pass k_fp for tiles wider than its band)
 int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
                   float* out, long long out_ts, cudaStream_t st) {
-    static int fpv = -1;
-    if (fpv < 0) { const char* e = getenv("LT_FP_V"); fpv = (e && atoi(e) == 1) ? 1 : 2; }
-    if (t.TP > FP_P || t.Wwin > 32 * FP_U)
+    if (t.TP > FP2_P || t.Wwin > 32 * FP_U)
         return launch_fp(p, 0, t, img, imgT, img_ts, out, out_ts, nullptr, nullptr, st);
-    if (fpv == 2 && t.TP <= FP2_P) {
-        const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)FP_GA * 32 * FP_U * sizeof(float);
-        LT_CUDA(cudaFuncSetAttribute(k_fp_roi2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
-        dim3 grid(p.ngroups, t.ntiles);
-        ScopedTimer tm(TC_FP, st);
-        k_fp_roi2<<<grid, 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
-        LT_LAUNCHED();
-        return LT_OK;
-    }
-    const size_t smem = (size_t)2 * FP_BL * FP_P * sizeof(float);
-    LT_CUDA(cudaFuncSetAttribute(k_fp_roi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)FP_GA * 32 * FP_U * sizeof(float);
+    LT_CUDA(cudaFuncSetAttribute(k_fp_roi2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
     dim3 grid(p.ngroups, t.ntiles);
     ScopedTimer tm(TC_FP, st);
-    k_fp_roi<<<grid, 256, smem, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
+    k_fp_roi2<<<grid, 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
     LT_LAUNCHED();
     return LT_OK;
 }
@@ -282,53 +270,10 @@ SinoView view_win(const float* base, int Wwin, int na) {
     return SinoView{base, (long long)na * Wwin, Wwin, 0, Wwin};
 }
 
-// FGP cluster configuration (k_fgp): NTW threads per strip row (one per
-// column), strips of FR rows, G strips per CTA (<= NT threads), K CTAs per
-// cluster covering all rows of a tile.  FR = 8 (512-thread CTAs, 16 warps per
-// SM) by default; LT_FGP_FR=16 selects 16-row strips in 256-thread CTAs.
-struct FgpCfg { int NTW, G, K, FR, NT; size_t smem; };
-
-int fgp_config(int rows, int cols, int nfgp, FgpCfg* c) {
-    if (rows < 1 || cols < 1 || cols > 256) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
-    static int fr_env = -1, nt_env = -1;
-    if (fr_env < 0) { const char* e = getenv("LT_FGP_FR"); fr_env = (e && atoi(e) == 16) ? 16 : 8; }
-    if (nt_env < 0) { const char* e = getenv("LT_FGP_NT"); nt_env = (e && atoi(e) == 1024) ? 1024 : 512; }
-    const int ntw = 32 * ((cols + 31) / 32);
-    const int FRv = fr_env, NT = FRv == 8 ? ((nt_env == 1024 && ntw == 256) ? 1024 : 512) : 256;
-    const int strips = (rows + FRv - 1) / FRv;
-    const int G = std::max(1, std::min(strips, NT / ntw));
-    const int K = (strips + G - 1) / G;
-    if (K > 16) return fail(LT_ERR_INVALID, "FGP tile %dx%d needs a %d-CTA cluster (> 16)", rows, cols, K);
-    const int nw = ntw / 32;
-    c->NTW = ntw; c->G = G; c->K = K; c->FR = FRv; c->NT = NT;
-    c->smem = (size_t)(8 + 4 * ntw + 5 * G * ntw + 4 * G * (nw + 1) * FRv + G * nw * FRv + (NT >= 1024 ? 3 * G * FRv * 256 : 0)) * sizeof(float);
-    (void)nfgp;
-    return LT_OK;
-}
-
-template <int MODE, int FRv, int NT>
-int launch_fgp_t(FgpArgs A, const FgpCfg& c, int ntiles, cudaStream_t st) {
-    A.G = c.G;
-    A.NTW = c.NTW;
-    auto kern = k_fgp<MODE, FRv, NT>;
-    LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
-    if (c.K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof cfg);
-    cfg.gridDim = dim3(c.K, ntiles, 1);
-    cfg.blockDim = dim3(c.NTW, c.G, 1);
-    cfg.dynamicSmemBytes = c.smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = c.K;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    ScopedTimer tm(TC_FGP, st);
-    LT_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
-    LT_LAUNCHED();
+// the FGP kernel supports extended ROIs up to 256 x 256 (32 lanes x 8 columns)
+int fgp_check(int rows, int cols) {
+    if (rows < 1 || cols < 1 || cols > 256 || rows > 256)
+        return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported (extended ROI side <= 256)", rows, cols);
     return LT_OK;
 }
 
@@ -379,37 +324,24 @@ int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     return LT_OK;
 }
 
-int fgp_version() {
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("LT_FGP_V"); v = (e && atoi(e) == 1) ? 1 : 2; }
-    return v;
-}
-
 template <int MODE>
 int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
-    if (rows < 1 || cols < 1 || cols > 256) return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported", rows, cols);
+    if (int rc = fgp_check(rows, cols)) return rc;
     if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
-    if (fgp_version() == 2) {
-        static int cfgv = -1;
-        if (cfgv < 0) {
-            const char* e = getenv("LT_FGP2_CFG");
-            cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : !strcmp(e, "2x16b") ? 3 : 0;
-        }
-        // small batches: 16-row CTAs (twice the CTAs per tile) while the 32-row
-        // layout would not fill one wave of SMs
-        int nsm = 148;
-        { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
-        const bool small = ntiles * ((rows + 31) / 32) < nsm && rows > 16;
-        if (cfgv == 1 || (cfgv == 0 && small && (rows + 15) / 16 <= 16)) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
-        if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
-        if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, 0, true>(A, rows, ntiles, st);
-        return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
+    static int cfgv = -1;
+    if (cfgv < 0) {
+        const char* e = getenv("LT_FGP2_CFG");
+        cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : !strcmp(e, "2x16b") ? 3 : 0;
     }
-    FgpCfg c;
-    if (int rc = fgp_config(rows, cols, A.nfgp, &c)) return rc;
-    if (c.FR == 8 && c.NT == 1024) return launch_fgp_t<MODE, 8, 1024>(A, c, ntiles, st);
-    if (c.FR == 8) return launch_fgp_t<MODE, 8, 512>(A, c, ntiles, st);
-    return launch_fgp_t<MODE, 16, 256>(A, c, ntiles, st);
+    // small batches: 16-row CTAs (twice the CTAs per tile) while the 32-row
+    // layout would not fill one wave of SMs
+    int nsm = 148;
+    { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
+    const bool small = ntiles * ((rows + 31) / 32) < nsm && rows > 16;
+    if (cfgv == 1 || (cfgv == 0 && small && (rows + 15) / 16 <= 16)) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
+    if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
+    if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, 0, true>(A, rows, ntiles, st);
+    return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
 }
 
 dim3 grid2d(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }
@@ -1296,8 +1228,7 @@ int lt_tv_solve(lt_plan* p, const float* d_sino, float lambda, int32_t n_fgp, fl
     if (int rc = check_plan(p)) return rc;
     if (!d_sino || (!d_cores && p->R > 0)) return fail(LT_ERR_INVALID, "null pointer");
     if (!(lambda >= 0.f) || n_fgp < 1 || n_fgp > 4096) return fail(LT_ERR_INVALID, "lambda >= 0 and 1 <= n_fgp <= 4096 required");
-    FgpCfg fc;
-    if (int rc = fgp_config(p->T, p->T, n_fgp, &fc)) return rc;
+    if (int rc = fgp_check(p->T, p->T)) return rc;
     if (p->R == 0) return LT_OK;
     return solve(*p, 1, d_sino, lambda, 0.f, n_fgp, d_cores, (cudaStream_t)stream);
 }
@@ -1634,8 +1565,7 @@ int lt_tv_solve_lambdas(lt_plan* p, const float* d_sino, const float* h_lambdas,
     if (n_fgp < 1 || n_fgp > 4096) return fail(LT_ERR_INVALID, "1 <= n_fgp <= 4096 required");
     for (int q = 0; q < p->R; ++q)
         if (!(h_lambdas[q] >= 0.f)) return fail(LT_ERR_INVALID, "lambda[%d] must be >= 0", q);
-    FgpCfg fc;
-    if (int rc = fgp_config(p->T, p->T, n_fgp, &fc)) return rc;
+    if (int rc = fgp_check(p->T, p->T)) return rc;
     if (p->R == 0) return LT_OK;
     cudaStream_t st = (cudaStream_t)stream;
     LT_CUDA(cudaMemcpyAsync(p->P<float>(p->off.lams), h_lambdas, (size_t)p->R * sizeof(float), cudaMemcpyHostToDevice, st));

@@ -1,12 +1,12 @@
 """FGP kernel variants: time on C4-shaped tiles (256 x 256^2, 100 iterations)
 and check against the fp64 oracle on full and clipped tile shapes.
-Run once per variant (the library reads LT_FGP_V / LT_FGP2_CFG once)."""
+Run once per variant (the library reads LT_FGP2_CFG once)."""
 import os, sys
 sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_1604_02292_b200 as lt
 import oracle
-tag = f"V={os.environ.get('LT_FGP_V', '2')} cfg={os.environ.get('LT_FGP2_CFG', '-')}"
+tag = f"cfg={os.environ.get('LT_FGP2_CFG', '-')}"
 torch.manual_seed(0)
 x = torch.rand(256, 256, 256, device='cuda')
 for _ in range(2): lt.fgp_batch(x, 0.05, 100)

@@ -1,6 +1,5 @@
 """Per-kernel timing inside a C4 solve on one stream (LT_SPLIT=1), CUDA events
-per launch class (lt_timing), plus parity of the ROI projector against the
-previous kernel version when LT_FP_V is toggled by the caller."""
+per launch class (lt_timing)."""
 import os, sys
 os.environ.setdefault("LT_SPLIT", "1")
 sys.path.insert(0, '.')
