@@ -623,7 +623,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fgp2: the same FGP + FISTA epilogue as k_fgp, laid out for the sm_100
+// k_fgp2: the FGP TV prox + FISTA epilogue, laid out for the sm_100
 // paired FP32 datapath (FFMA2 / FADD2: two fp32 lanes per instruction).
 //
 // Warp w of CTA k owns FR full rows (rows (k*NW + w)*FR ...) of the tile, 256
