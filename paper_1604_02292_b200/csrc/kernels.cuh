@@ -682,7 +682,19 @@ struct Fgp2Smem {
     static constexpr int bsm = hp + NW * FGP2_ROW;             // [NW][FR][256] b (BSM variant)
     static constexpr int total = bsm;
     static constexpr int total_bsm = bsm + NW * FR * FGP2_ROW;
+    // MODE 1: [NW][FR][2][256] xprev and x_s rows, fetched with cp.async at
+    // kernel start (they are inputs the FGP loop never touches) and read by the epilogue
+    static constexpr int xin_floats = NW * FR * 2 * FGP2_ROW;
 };
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
 
 // BSM: b (read once per iteration) lives in shared memory instead of registers,
 // so the kernel fits 128 registers and two CTAs (two tiles) share an SM: one
@@ -753,6 +765,33 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             r[k][c2] = f2s(0.5f); s[k][c2] = f2s(0.5f); p[k][c2] = f2s(0.5f); q[k][c2] = f2s(0.5f);
         }
         if constexpr (BSM) row_st(bs + k * FGP2_ROW, lane, bv);
+    }
+    // FISTA state for the epilogue: asynchronous copies into shared memory now,
+    // consumed after the FGP loop (each lane reads back only its own columns)
+    float* xin = sm + (BSM ? SM::total_bsm : SM::total) + (w * FR) * 2 * FGP2_ROW;
+    const bool vec_p = ((vc0 | A.T) & 3) == 0;
+    if constexpr (MODE == 1) {
+        #pragma unroll
+        for (int k = 0; k < FR; ++k) {
+            const int i = i0 + k;
+            if (i >= Hv) continue;
+            const long long prow = (long long)tile * A.p_tstride + (long long)(vr0 + i) * A.T + vc0 + x0;
+            float* dx = xin + k * 2 * FGP2_ROW + x0;
+            #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (vec_p && x0 + 4 * h + 3 < Wv) {
+                    cp_async16(dx + 4 * h, A.xprev + prow + 4 * h);
+                    cp_async16(dx + FGP2_ROW + 4 * h, A.xs + prow + 4 * h);
+                } else {
+                    #pragma unroll
+                    for (int c = 4 * h; c < 4 * h + 4; ++c)
+                        if (x0 + c < Wv) {
+                            cp_async4(dx + c, A.xprev + prow + c);
+                            cp_async4(dx + FGP2_ROW + c, A.xs + prow + c);
+                        }
+                }
+            }
+        }
     }
     const float lam = A.lams ? __ldg(A.lams + tile) : A.lam;
     const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
@@ -904,60 +943,100 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) pup0[c2] = f2s(0.5f);
     }
-    // FISTA state of all rows first (independent loads in flight together)
-    float xpv[MODE == 1 ? FR : 1][8], xsv[MODE == 1 ? FR : 1][8];
-    if constexpr (MODE == 1) {
-        #pragma unroll
-        for (int k = 0; k < FR; ++k) {
-            const int i = i0 + k;
-            const long long prow = (long long)tile * A.p_tstride + (long long)(vr0 + i) * A.T + vc0 + x0;
-            #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const bool ok = i < Hv && x0 + c < Wv;
-                xpv[k][c] = ok ? __ldcs(A.xprev + prow + c) : 0.f;
-                xsv[k][c] = ok ? __ldcs(A.xs + prow + c) : 0.f;
-            }
-        }
-    }
+    // the neighbour's halo row has been read: arrive now, wait at exit (keeps
+    // shared memory alive until every neighbour has read its halo)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if constexpr (MODE == 1) cp_async_commit_wait_all();
+    const bool vec_y = (vc0 & 3) == 0;                  // y rows: PADL + vc0 + x0, TP % 4 == 0
+    const bool vec_yT = FR == 4 && (vr0 & 3) == 0;      // yT columns: PADL + vr0 + i0 + k
+    float xall[FR][8];
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
         float ql = __shfl_up_sync(0xffffffffu, q[k][3].y, 1);
         if (lane == 0) ql = 0.5f;
-        float xv[8];
         float2 bk[4];
         bget(k, bk);
         #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) {
             const float2 pu = k > 0 ? p[k - 1][c2] : pup0[c2];
             const float qlx = c2 > 0 ? q[k][c2 - 1].y : ql;
-            xv[2 * c2] = bk[c2].x - lam2 * (p[k][c2].x + q[k][c2].x - pu.x - qlx);
-            xv[2 * c2 + 1] = bk[c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
+            xall[k][2 * c2] = bk[c2].x - lam2 * (p[k][c2].x + q[k][c2].x - pu.x - qlx);
+            xall[k][2 * c2 + 1] = bk[c2].y - lam2 * (p[k][c2].y + q[k][c2].y - pu.y - q[k][c2].x);
         }
-        if (i < Hv) {
-            if constexpr (MODE == 0) {
+        if (i >= Hv) continue;
+        if constexpr (MODE == 0) {
+            #pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (x0 + c < Wv) A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + x0 + c] = xall[k][c];
+        } else {
+            const int ti_ = vr0 + i;
+            const long long prow = (long long)tile * A.p_tstride + (long long)ti_ * A.T + vc0 + x0;
+            float* yrow = A.y + (long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + vc0 + x0;
+            const float* sx = xin + k * 2 * FGP2_ROW + x0;
+            float xp[8], xsv[8];
+            *reinterpret_cast<float4*>(xp) = *reinterpret_cast<const float4*>(sx);
+            *reinterpret_cast<float4*>(xp + 4) = *reinterpret_cast<const float4*>(sx + 4);
+            *reinterpret_cast<float4*>(xsv) = *reinterpret_cast<const float4*>(sx + FGP2_ROW);
+            *reinterpret_cast<float4*>(xsv + 4) = *reinterpret_cast<const float4*>(sx + FGP2_ROW + 4);
+            float yv[8];
+            #pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float x = xall[k][c];
+                const float rr = x + A.beta_o * (x - xp[c]);          // FISTA extrapolation (A12)
+                yv[c] = rr - xsv[c];                                  // x_L^k = r - x_s^k
+            }
+            #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (x0 + 4 * h + 3 < Wv && vec_p) {
+                    *reinterpret_cast<float4*>(A.xprev + prow + 4 * h) =
+                        make_float4(xall[k][4 * h], xall[k][4 * h + 1], xall[k][4 * h + 2], xall[k][4 * h + 3]);
+                } else {
+                    #pragma unroll
+                    for (int c = 4 * h; c < 4 * h + 4; ++c)
+                        if (x0 + c < Wv) A.xprev[prow + c] = xall[k][c];
+                }
+                if (x0 + 4 * h + 3 < Wv && vec_y) {
+                    *reinterpret_cast<float4*>(yrow + 4 * h) = make_float4(yv[4 * h], yv[4 * h + 1], yv[4 * h + 2], yv[4 * h + 3]);
+                } else {
+                    #pragma unroll
+                    for (int c = 4 * h; c < 4 * h + 4; ++c)
+                        if (x0 + c < Wv) yrow[c] = yv[c];
+                }
+            }
+            if (vec_yT) {
+                // the warp's FR = 4 rows are consecutive: the transposed copy of
+                // column c is one 16-byte store per lane, written after the last row
                 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    if (x0 + c < Wv) A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + x0 + c] = xv[c];
+                for (int c = 0; c < 8; ++c) xall[k][c] = yv[c];
             } else {
-                const int ti_ = vr0 + i;
-                const long long prow = (long long)tile * A.p_tstride + (long long)ti_ * A.T + vc0 + x0;
-                float* yrow = A.y + (long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + vc0 + x0;
                 float* ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + ti_;
                 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    if (x0 + c >= Wv) continue;
-                    const float x = xv[c];
-                    const float rr = x + A.beta_o * (x - xpv[k][c]);          // FISTA extrapolation (A12)
-                    const float yv = rr - xsv[k][c];                          // x_L^k = r - x_s^k
-                    A.xprev[prow + c] = x;
-                    yrow[c] = yv;
-                    ycol[(long long)c * A.TP] = yv;
-                }
+                for (int c = 0; c < 8; ++c)
+                    if (x0 + c < Wv) ycol[(long long)c * A.TP] = yv[c];
             }
         }
     }
-    cl.sync();   // keep shared memory alive until every neighbour has read its halo
+    if constexpr (MODE == 1) {
+        if (vec_yT && i0 < Hv) {
+            float* ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + vr0 + i0;
+            if (i0 + 3 < Hv) {
+                #pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (x0 + c < Wv)
+                        *reinterpret_cast<float4*>(ycol + (long long)c * A.TP) =
+                            make_float4(xall[0][c], xall[FR > 1 ? 1 : 0][c], xall[FR > 2 ? 2 : 0][c], xall[FR > 3 ? 3 : 0][c]);
+            } else {
+                #pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    #pragma unroll
+                    for (int k = 0; k < FR; ++k)
+                        if (x0 + c < Wv && i0 + k < Hv) ycol[(long long)c * A.TP + k] = xall[k][c];
+            }
+        }
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+
 }
 
 // ---------------------------------------------------------------------------

@@ -301,7 +301,8 @@ template <int MODE, int FR, int NW, int SYNC, bool BSM = false>
 int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
-    const size_t smem = (size_t)(BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) * sizeof(float);
+    const size_t smem = (size_t)((BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) +
+                                 (MODE == 1 ? Fgp2Smem<FR, NW>::xin_floats : 0)) * sizeof(float);
     auto kern = k_fgp2<MODE, FR, NW, SYNC, BSM>;
     LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
