@@ -655,6 +655,21 @@ __device__ __forceinline__ void row_ld(const float* row, int lane, float2 (&v)[4
     v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
     v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
 }
+// the same through 32-bit shared-window addresses (loop-invariant bases, no
+// generic-to-shared conversion inside the iteration loop)
+__device__ __forceinline__ void row_st_s(unsigned row, int lane, const float2 (&v)[4]) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + 16u * lane),
+                 "f"(v[0].x), "f"(v[0].y), "f"(v[1].x), "f"(v[1].y) : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + 512u + 16u * lane),
+                 "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y) : "memory");
+}
+__device__ __forceinline__ void row_ld_s(unsigned row, int lane, float2 (&v)[4]) {
+    float a0, a1, a2, a3, b0, b1, b2, b3;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3) : "r"(row + 16u * lane) : "memory");
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(row + 512u + 16u * lane) : "memory");
+    v[0] = make_float2(a0, a1); v[1] = make_float2(a2, a3);
+    v[2] = make_float2(b0, b1); v[3] = make_float2(b2, b3);
+}
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -672,13 +687,17 @@ template <int V> struct Parity { __device__ __forceinline__ operator int() const
 
 template <int FR, int NW>
 struct Fgp2Smem {
+    // halo rows, one slot per warp and parity, so every warp reads its halo
+    // from the same place whichever warp or CTA wrote it:
+    //   hr[par][j]: the r row above warp j (j = 0: pushed by the CTA above over
+    //               DSMEM; j > 0: the last row of warp j - 1)
+    //   hz[par][j]: the z row below warp j - 1 (j < NW: the first row of warp j;
+    //               j = NW: pushed by the CTA below)
+    // slots never written keep their initial value (r: the shifted zero 1/2, z: 0)
     static constexpr int bars = 0;                             // 4 x u64: r from above [2], z from below [2]
-    static constexpr int wbar = 8;                             // [NW][4] u64: r row of warp w ready [2], z row [2]
-    static constexpr int rx_r = wbar + 8 * NW;                 // [2][256] r row pushed by the CTA above
-    static constexpr int rx_z = rx_r + 2 * FGP2_ROW;           // [2][256] z row pushed by the CTA below
-    static constexpr int hr = rx_z + 2 * FGP2_ROW;             // [2][NW][256] last r row of each warp
-    static constexpr int hz = hr + 2 * NW * FGP2_ROW;          // [2][NW][256] first z row of each warp
-    static constexpr int hp = hz + 2 * NW * FGP2_ROW;          // [NW][256] last p row (epilogue)
+    static constexpr int hr = 8;                               // [2][NW + 1][256]
+    static constexpr int hz = hr + 2 * (NW + 1) * FGP2_ROW;    // [2][NW + 1][256]
+    static constexpr int hp = hz + 2 * (NW + 1) * FGP2_ROW;    // [NW][256] last p row (epilogue)
     static constexpr int bsm = hp + NW * FGP2_ROW;             // [NW][FR][256] b (BSM variant)
     static constexpr int total = bsm;
     static constexpr int total_bsm = bsm + NW * FR * FGP2_ROW;
@@ -717,28 +736,13 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     const int x0 = lane * 8;                    // first column of this lane
     const bool has_up = kr > 0, has_dn = kr < K - 1;
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + SM::bars);
-    float* rx_r = sm + SM::rx_r;
-    float* rx_z = sm + SM::rx_z;
-    float* hr = sm + SM::hr;
-    float* hz = sm + SM::hz;
     float* hp = sm + SM::hp;
-    for (int e = threadIdx.x; e < SM::total - SM::rx_r; e += NW * 32) {
-        const int o = SM::rx_r + e;
-        const bool zb = (o >= SM::rx_z && o < SM::hr) || (o >= SM::hz && o < SM::hp);
-        sm[o] = zb ? 0.f : 0.5f;               // z halos start at 0, dual halos at the shifted zero 1/2
-    }
-    unsigned long long* wbar = reinterpret_cast<unsigned long long*>(sm + SM::wbar);
+    for (int e = threadIdx.x; e < SM::hp - SM::hr; e += NW * 32)
+        sm[SM::hr + e] = SM::hr + e >= SM::hz ? 0.f : 0.5f;   // z halos start at 0, dual halos at the shifted zero 1/2
     if (threadIdx.x == 0) {
         for (int q_ = 0; q_ < 4; ++q_) mbar_init(smem_u32(bars + q_), 1);
-        for (int q_ = 0; q_ < 4 * NW; ++q_) mbar_init(smem_u32(wbar + q_), 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // warp-to-warp signals (no CTA barrier in the iteration loop): warp w
-    // arrives on wr(w, parity) after storing its last r row, on wz(w, parity)
-    // after storing its first z row; its neighbours wait on them
-    const unsigned wbar0 = smem_u32(wbar);
-    auto wr = [&](int ww, int par) { return wbar0 + 8u * (4 * ww + par); };
-    auto wz = [&](int ww, int par) { return wbar0 + 8u * (4 * ww + 2 + par); };
 
     float2 breg[BSM ? 1 : FR][4], r[FR][4], s[FR][4], p[FR][4], q[FR][4], z[FR][4];
     float* bs = sm + SM::bsm + (w * FR) * FGP2_ROW;          // this warp's b rows (BSM)
@@ -805,10 +809,16 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     for (int c2 = 0; c2 < 4; ++c2) gq2[c2] = make_float2(gq[2 * c2], gq[2 * c2 + 1]);
     cl.sync();
     const unsigned up_rank = has_up ? kr - 1 : kr, dn_rank = has_dn ? kr + 1 : kr;
-    const unsigned rem_rx_r = mapa(smem_u32(rx_r), dn_rank);      // my last warp's r row -> CTA below
+    constexpr unsigned RB = FGP2_ROW * 4u;             // bytes per staged row
+    constexpr unsigned PS = (NW + 1) * RB;             // bytes per parity of hr / hz
+    const unsigned s_hr = smem_u32(sm + SM::hr), s_hz = smem_u32(sm + SM::hz);
+    // this warp's halo slots: r from above, z from below (read); r / z it publishes (written)
+    const unsigned up_slot = s_hr + w * RB, dn_slot = s_hz + (w + 1) * RB;
+    const unsigned rem_rx_r = mapa(s_hr, dn_rank);                 // my last warp's r row -> slot 0 of the CTA below
     const unsigned rem_bar_r = mapa(smem_u32(bars + 0), dn_rank);
-    const unsigned rem_rx_z = mapa(smem_u32(rx_z), up_rank);      // my first warp's z row -> CTA above
+    const unsigned rem_rx_z = mapa(s_hz + NW * RB, up_rank);       // my first warp's z row -> slot NW of the CTA above
     const unsigned rem_bar_z = mapa(smem_u32(bars + 2), up_rank);
+    const unsigned my_r_slot = s_hr + (w + 1) * RB, my_z_slot = s_hz + w * RB;
     constexpr unsigned row_bytes = FGP2_ROW * 4;
     const int nit = lam > 0.f ? A.nfgp : 0;
     const unsigned bar0 = smem_u32(bars);
@@ -818,8 +828,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     #pragma unroll
     for (int k = 0; k < FR; ++k) gp[k] = (i0 + k < Hv - 1) ? gam : 0.f;
 
-    // SYNC 0: CTA barrier after each phase; 1: warp-to-warp mbarrier signals
-    // (parity cb: compile-time in the barrier variant, so every halo address is loop invariant)
+    // CTA barrier after each phase (parity cb compile-time, so every halo address is loop invariant)
     auto fgp_iter = [&](int it, auto cbv) {
         const int cb = cbv, pb = cb ^ 1;
         if (lane == 0) {   // the consuming warp arms its DSMEM receive buffers
@@ -834,15 +843,10 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             if (k > 0) {
                 #pragma unroll
                 for (int c2 = 0; c2 < 4; ++c2) rup[c2] = r[k - 1][c2];
-            } else if (w > 0 && it > 0) {
-                if constexpr (SYNC == 1) mbar_wait(wr(w - 1, pb), ((it - 1) >> 1) & 1);
-                row_ld(hr + (pb * NW + w - 1) * FGP2_ROW, lane, rup);
-            } else if (w == 0 && has_up && it > 0) {
-                mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
-                row_ld(rx_r + pb * FGP2_ROW, lane, rup);
             } else {
-                #pragma unroll
-                for (int c2 = 0; c2 < 4; ++c2) rup[c2] = f2s(0.5f);
+                // slot of parity pb: written in iteration it - 1 (still 1/2 at it = 0)
+                if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
+                row_ld_s(up_slot + pb * PS, lane, rup);
             }
             float sl = __shfl_up_sync(0xffffffffu, s[k][3].y, 1);
             if (lane == 0) sl = 0.5f;
@@ -862,14 +866,11 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 z[k][c2].y = fmaf(lam2, s[k][c2].x, t[c2].y);
             }
             if (k == 0) {
-                if (w == 0 && has_up) row_push(rem_rx_z + cb * row_bytes, lane, z[0], rem_bar_z + cb * 8);
-                if (w > 0) {
-                    row_st(hz + (cb * NW + w) * FGP2_ROW, lane, z[0]);
-                    if constexpr (SYNC == 1) mbar_arrive(wz(w, cb));
-                }
+                if (w == 0 && has_up) row_push(rem_rx_z + cb * PS, lane, z[0], rem_bar_z + cb * 8);
+                if (w > 0) row_st_s(my_z_slot + cb * PS, lane, z[0]);
             }
         }
-        if constexpr (SYNC == 0) __syncthreads();
+        __syncthreads();
         // ---- phase B: dual ascent, projection on [0, 1] (shifted), FGP momentum;
         // last row first and publish it
         const float beta = c_fgp_beta[it];
@@ -881,15 +882,9 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             if (k < FR - 1) {
                 #pragma unroll
                 for (int c2 = 0; c2 < 4; ++c2) zb[c2] = z[k + 1][c2];
-            } else if (w < NW - 1) {
-                if constexpr (SYNC == 1) mbar_wait(wz(w + 1, cb), (it >> 1) & 1);
-                row_ld(hz + (cb * NW + w + 1) * FGP2_ROW, lane, zb);
-            } else if (has_dn) {
-                mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
-                row_ld(rx_z + cb * FGP2_ROW, lane, zb);
             } else {
-                #pragma unroll
-                for (int c2 = 0; c2 < 4; ++c2) zb[c2] = f2s(0.f);
+                if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
+                row_ld_s(dn_slot + cb * PS, lane, zb);
             }
             const float zr = __shfl_down_sync(0xffffffffu, z[k][0].x, 1);   // lane 31: masked by gq
             const float gpk = gp[k];
@@ -912,25 +907,19 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 q[k][c2] = qn;
             }
             if (k == FR - 1) {
-                if (w == NW - 1 && has_dn) row_push(rem_rx_r + cb * row_bytes, lane, r[FR - 1], rem_bar_r + cb * 8);
-                if (w < NW - 1) {
-                    row_st(hr + (cb * NW + w) * FGP2_ROW, lane, r[FR - 1]);
-                    if constexpr (SYNC == 1) mbar_arrive(wr(w, cb));
-                }
+                if (w == NW - 1 && has_dn) row_push(rem_rx_r + cb * PS, lane, r[FR - 1], rem_bar_r + cb * 8);
+                if (w < NW - 1) row_st_s(my_r_slot + cb * PS, lane, r[FR - 1]);
             }
         }
-        if constexpr (SYNC == 0) __syncthreads();
+        __syncthreads();
     };
-    if constexpr (SYNC == 0) {
+    {
         int it = 0;
         for (; it + 1 < nit; it += 2) {
             fgp_iter(it, Parity<0>{});
             fgp_iter(it + 1, Parity<1>{});
         }
         if (it < nit) fgp_iter(it, Parity<0>{});
-    } else {
-        #pragma unroll 1
-        for (int it = 0; it < nit; ++it) fgp_iter(it, it & 1);
     }
 
     // ---- x = b - lam2 L(p', q'), then the epilogue
