@@ -323,7 +323,9 @@ def run_ours(args, cfg):
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # FP32 lanes x FMA, DESIGN.md §Roofline
     # dominant kernel class over the timed region (rank 0's stream)
-    dom = max(ktimes, key=lambda k: ktimes[k][0])
+    # (the x_s backprojection "xs" runs on a side stream, overlapped with the
+    # main stream's kernels: reported per class, not a roofline candidate)
+    dom = max((k for k in ktimes if k != "xs"), key=lambda k: ktimes[k][0])
     dom_ms, dom_n = ktimes[dom]
     avg_ms = dom_ms / max(dom_n, 1)
     local_upd_per_step = upd_local
@@ -334,8 +336,8 @@ def run_ours(args, cfg):
         work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / max(dom_n, 1)
     elif dom == "fp":      # one W_{L'} y per iteration 2..n
         work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / max(dom_n, 1)
-    elif dom == "bp":      # x_s^k = M_{L'} W^T b_k (n) and W_{L'}^T s (n - 1), counted per ROI as in the method
-        work = JOSEPH_FLOPS_PER_UPDATE * nA * (2 * n_iter - 1) * args.steps / max(dom_n, 1)
+    elif dom == "bp":      # W_{L'}^T s of iterations 2..n (iteration 1 has s = 0: no gather)
+        work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / max(dom_n, 1)
     else:
         work = 0.0
     achieved = work / (avg_ms / 1e3) / 1e12

@@ -255,11 +255,13 @@ int lt_pad_truncated(const float* d_in, int32_t n_angles, int32_t n_trunc, int32
 int64_t lt_launch_count(void);
 
 /* Per-kernel-class device timing (bench.py's roofline): when enabled, every
- * launch of the Joseph forward (class 0), backprojection (1), FGP (2) and
- * convolution (3) kernels is bracketed by CUDA events recorded on its launch
- * stream.  lt_timing_read synchronizes on the recorded events, writes the
- * summed milliseconds and launch counts per class (host arrays of 4) and
- * clears the records. */
+ * launch of the Joseph forward (class 0), ROI / global-iteration
+ * backprojection (1), FGP (2), convolution (3) and block-listed global x_s
+ * backprojection (4, the side-stream M_{L'} W^T b_k of Alg. 3) kernels is
+ * bracketed by CUDA events recorded on its launch stream.  lt_timing_read
+ * synchronizes on the recorded events, writes the summed milliseconds and
+ * launch counts per class (host arrays of 5) and clears the records.  Timing
+ * disables the CUDA-graph replay of the local iterations. */
 void lt_timing_enable(int32_t on);
 int lt_timing_read(double* h_ms, int64_t* h_count);
 

@@ -108,7 +108,7 @@ def launch_count() -> int:
     return int(_lib.lt_launch_count())
 
 
-KERNEL_CLASSES = ("fp", "bp", "fgp", "conv")
+KERNEL_CLASSES = ("fp", "bp", "fgp", "conv", "xs")
 
 
 def timing_enable(on: bool = True) -> None:
@@ -118,8 +118,8 @@ def timing_enable(on: bool = True) -> None:
 
 def timing_read() -> dict:
     """{class: (total_ms, launches)} since the last read (synchronizes on the events)."""
-    ms = np.zeros(4, dtype=np.float64)
-    cnt = np.zeros(4, dtype=np.int64)
+    ms = np.zeros(len(KERNEL_CLASSES), dtype=np.float64)
+    cnt = np.zeros(len(KERNEL_CLASSES), dtype=np.int64)
     _chk(_lib.lt_timing_read(ms.ctypes.data, cnt.ctypes.data), "lt_timing_read")
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
 

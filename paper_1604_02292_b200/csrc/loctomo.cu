@@ -49,7 +49,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int LT_MAX_PEERS = 64;
 
 // ---- optional per-kernel-class timing (CUDA events on the launch stream) ----
-enum { TC_FP = 0, TC_BP = 1, TC_FGP = 2, TC_CONV = 3, TC_N = 4 };
+enum { TC_FP = 0, TC_BP = 1, TC_FGP = 2, TC_CONV = 3, TC_XS = 4, TC_N = 5 };
 struct TimerRec { int cls; cudaEvent_t a, b; };
 bool g_timing = false;
 std::vector<TimerRec> g_recs;
@@ -244,7 +244,7 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
     if (e.blist && nblist == 0) return LT_OK;
     const int nsx = (t.T + BP_SUB - 1) / BP_SUB;
     const long long ctas64 = e.blist ? nblist : (long long)nsx * nsx * t.ntiles;
-    ScopedTimer tm(TC_BP, st);
+    ScopedTimer tm(e.blist ? TC_XS : TC_BP, st);   // block-listed launches: the global x_s backprojection
     if (!e.blist && ctas64 < 2LL * 3 * p.num_sms) {
         const int nsx32 = (t.T + 31) / 32;
         k_bp<NS, MODE, 32><<<dim3(nsx32 * nsx32, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
@@ -777,8 +777,8 @@ const char* lt_last_error(void) { return g_err.c_str(); }
 void lt_timing_enable(int32_t on) { g_timing = on != 0; }
 
 int lt_timing_read(double* h_ms, int64_t* h_count) {
-    double ms[TC_N] = {0, 0, 0, 0};
-    int64_t cnt[TC_N] = {0, 0, 0, 0};
+    double ms[TC_N] = {};
+    int64_t cnt[TC_N] = {};
     for (auto& r : g_recs) {
         float t = 0.f;
         LT_CUDA(cudaEventSynchronize(r.b));
