@@ -121,6 +121,7 @@ def algorithmic_counts(cfg, plan_rects, n_iter):
 # FP32 operations per unit, DESIGN.md §Roofline (counted from the formulas, not the SASS)
 FGP_FLOPS_PER_PX_IT = 21.0      # z (5) + two dual steps with clip (10) + momentum (6)
 JOSEPH_FLOPS_PER_UPDATE = 8.0   # hat weight (2 FMA-equivalents) + 2 taps x FMA, per pixel-angle
+FP_SMEM_BYTES_PER_STEP = 8.0    # forward projector: one staged (S, D) fp32 pair read per ray-line step
 
 
 HAAR_LAM, HAAR_LEVELS = 0.02, 4
@@ -322,45 +323,65 @@ def run_ours(args, cfg):
     pk, pk_src = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # FP32 lanes x FMA, DESIGN.md §Roofline
-    # dominant kernel class over the timed region (rank 0's stream)
-    # (the x_s backprojection "xs" runs on a side stream, overlapped with the
-    # main stream's kernels: reported per class, not a roofline candidate)
-    dom = max((k for k in ktimes if k != "xs"), key=lambda k: ktimes[k][0])
-    dom_ms, dom_n = ktimes[dom]
-    avg_ms = dom_ms / max(dom_n, 1)
-    local_upd_per_step = upd_local
+    smem_peak_gbs = 148 * 128 * sm_max * 1e6 / 1e9            # shared-memory crossbar, 128 B/clk/SM
     nA = cfg.n_angles * Ptot_local          # pixel-angle updates of one A or A^T over all local ROIs
-    if dom == "fgp" and mode in ("haar", "exterior"):
-        work = 0.0         # the Haar prox is a few flops per pixel: not a roofline kernel
-    elif dom == "fgp":
-        work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / max(dom_n, 1)
-    elif dom == "fp":      # one W_{L'} y per iteration 2..n
-        work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / max(dom_n, 1)
-    elif dom == "bp":      # W_{L'}^T s of iterations 2..n (iteration 1 has s = 0: no gather)
-        work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / max(dom_n, 1)
-    else:
-        work = 0.0
-    achieved = work / (avg_ms / 1e3) / 1e12
-    kname = {"fgp": "k_fgp2", "fp": "k_fp_roi2", "bp": "k_bp_roi", "conv": "k_conv"}[dom]
-    traffic, traffic_src = None, None
+    # Joseph ray-line steps of one W_{L'} over all local ROIs: per angle c_a P
+    # (a line of w valid pixels is crossed by c_a w rays, c_a = max(|cos|, |sin|))
+    c_sum = float(np.sum(np.maximum(np.abs(np.cos(inp.angles)), np.abs(np.sin(inp.angles)))))
+    fp_steps = c_sum * Ptot_local
+    traffic_all = {}
     try:   # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            tj = json.load(f)
-        if kname in tj:
-            # the capture's launches cover all R ROIs; scale to this run's launch size
-            traffic = float(tj[kname]["dram_bytes_per_launch"]) * (plan.R / float(tj[kname].get("rois_per_launch", plan.R)))
-            traffic_src = tj[kname]["source"]
+            traffic_all = json.load(f)
     except Exception:
-        traffic = None
-    roofline = {"kernel": kname,
-                "bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak_tflops, 1),
-                "unit": "TFLOP/s", "frac": round(achieved / alu_peak_tflops, 4), "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
-                "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)",
-                "work_per_unit": ("21 FP32 flops per pixel-iteration" if dom == "fgp" else
-                                  f"{JOSEPH_FLOPS_PER_UPDATE:g} FP32 flops per pixel-angle update"),
-                "avg_launch_ms": round(avg_ms, 4), "launches": dom_n,
-                "share_of_step": round(dom_ms / elapsed_ms, 3)}
+        traffic_all = {}
+
+    def roofline_of(cls):
+        """Roofline entry of one main-stream kernel class."""
+        ms, n = ktimes[cls]
+        if n == 0 or ms <= 0:
+            return None
+        avg_ms = ms / n
+        kname = {"fgp": "k_fgp2", "fp": "k_fp_roi2", "bp": "k_bp_roi"}[cls]
+        if cls == "fgp":
+            if mode in ("haar", "exterior"):
+                return None      # the Haar prox is a few flops per pixel: not a roofline kernel
+            work = fgp_local * args.steps * FGP_FLOPS_PER_PX_IT / n
+            ent = {"bound": "alu", "peak": round(alu_peak_tflops, 1), "unit": "TFLOP/s",
+                   "achieved": work / (avg_ms / 1e3) / 1e12,
+                   "work_per_unit": f"{FGP_FLOPS_PER_PX_IT:g} FP32 flops per pixel-iteration",
+                   "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)"}
+        elif cls == "fp":        # one W_{L'} y per iteration 2..n; one (S, D) pair (8 B) per ray-line step
+            work = FP_SMEM_BYTES_PER_STEP * fp_steps * (n_iter - 1) * args.steps / n
+            ent = {"bound": "smem", "peak": round(smem_peak_gbs, 1), "unit": "GB/s",
+                   "achieved": work / (avg_ms / 1e3) / 1e9,
+                   "work_per_unit": f"{FP_SMEM_BYTES_PER_STEP:g} B of staged (S, D) pairs per Joseph ray-line step",
+                   "peak_source": f"derived: 148 SM x 128 B/clk shared-memory crossbar x {sm_max:.0f} MHz ({pk_src} clock)"}
+        else:                    # W_{L'}^T s of iterations 2..n (iteration 1 has s = 0: no gather)
+            work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / n
+            ent = {"bound": "alu", "peak": round(alu_peak_tflops, 1), "unit": "TFLOP/s",
+                   "achieved": work / (avg_ms / 1e3) / 1e12,
+                   "work_per_unit": f"{JOSEPH_FLOPS_PER_UPDATE:g} FP32 flops per pixel-angle update",
+                   "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)"}
+        traffic, traffic_src = None, None
+        if kname in traffic_all:   # the capture's launches cover all R ROIs; scale to this run's launch size
+            tj = traffic_all[kname]
+            traffic = float(tj["dram_bytes_per_launch"]) * (plan.R / float(tj.get("rois_per_launch", plan.R)))
+            traffic_src = tj["source"]
+        ent["achieved"] = round(ent["achieved"], 3)
+        ent.update({"kernel": kname, "frac": round(ent["achieved"] / ent["peak"], 4), "traffic": traffic,
+                    "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
+                    "avg_launch_ms": round(avg_ms, 4), "launches": n,
+                    "share_of_step": round(ms / elapsed_ms, 3)})
+        return ent
+
+    rooflines = {c: roofline_of(c) for c in ("fp", "bp", "fgp")}
+    rooflines = {c: v for c, v in rooflines.items() if v is not None}
+    # dominant kernel class over the timed region (rank 0's main stream; the x_s
+    # backprojection "xs" runs on a side stream, overlapped: reported per class only)
+    dom = max(rooflines, key=lambda c: ktimes[c][0])
+    roofline = {k: rooflines[dom][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+    roofline.update({k: v for k, v in rooflines[dom].items() if k not in roofline})
     kshare = {k: {"ms_per_step": round(v[0] / args.steps, 3), "launches_per_step": v[1] // args.steps}
               for k, v in ktimes.items()}
     cpu = None
@@ -383,6 +404,7 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": int(2 * plan.R * 8 if sweep else cfg.n * cfg.n * 4),
                 "ms_per_step": round(e2e_ms, 3)},
         "roofline": roofline,
+        "rooflines": rooflines,
         "hbm_peak_gbs": pk.get("hbm_gbs"),
         "clocks": clk,
         "cpu_baseline": cpu,
