@@ -683,6 +683,9 @@ __device__ __forceinline__ void row_push(unsigned remote_row, int lane, const fl
 }
 
 constexpr int FGP2_ROW = 256;     // columns per warp row (32 lanes x 8)
+#ifndef FGP_HALO_LAST
+#define FGP_HALO_LAST 1           // rows that read a halo are computed last in their phase
+#endif
 template <int V> struct Parity { __device__ __forceinline__ operator int() const { return V; } };
 
 template <int FR, int NW>
@@ -838,7 +841,8 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         // ---- phase A: z = b - lam2 L(r, s); row 0 first (its upper neighbour
         // may come from another warp or CTA) and publish it at once
         #pragma unroll
-        for (int k = 0; k < FR; ++k) {
+        for (int kk = 0; kk < FR; ++kk) {
+            const int k = FGP_HALO_LAST ? (kk + 1) % FR : kk;     // halo row 0 last: 1, ..., FR-1, 0
             float2 rup[4];
             if (k > 0) {
                 #pragma unroll
@@ -877,7 +881,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         const float2 beta2 = f2s(beta);
         #pragma unroll
         for (int kk = 0; kk < FR; ++kk) {
-            const int k = (kk + FR - 1) % FR;     // FR-1, 0, 1, ..., FR-2
+            const int k = FGP_HALO_LAST ? kk : (kk + FR - 1) % FR;   // halo row FR-1 last: 0, ..., FR-1
             float2 zb[4];
             if (k < FR - 1) {
                 #pragma unroll
