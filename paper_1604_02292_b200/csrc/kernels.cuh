@@ -683,6 +683,12 @@ __device__ __forceinline__ void row_push(unsigned remote_row, int lane, const fl
 }
 
 constexpr int FGP2_ROW = 256;     // columns per warp row (32 lanes x 8)
+// producer / consumer named barriers between two neighbouring warps (ids 1..15; 0 = __syncthreads)
+__device__ __forceinline__ void bar_arrive2(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void bar_sync2(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+#ifndef FGP_NAMED_BARS
+#define FGP_NAMED_BARS 0          // 1: named-barrier hand-over (measured slower: 1.35 vs 1.26 ms, C4 tiles)
+#endif
 #ifndef FGP_HALO_LAST
 #define FGP_HALO_LAST 1           // rows that read a halo are computed last in their phase
 #endif
@@ -831,7 +837,12 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     #pragma unroll
     for (int k = 0; k < FR; ++k) gp[k] = (i0 + k < Hv - 1) ? gam : 0.f;
 
-    // CTA barrier after each phase (parity cb compile-time, so every halo address is loop invariant)
+    // Halo hand-over between the warps of the CTA: NBAR (NW <= 8, with the halo
+    // rows computed last): producer / consumer named barriers per warp pair,
+    // so a warp waits only for the neighbour whose row it reads, and only
+    // before that row; otherwise a CTA barrier after each phase.  Parity cb is
+    // compile-time, so every halo address is loop invariant.
+    constexpr bool NBAR = FGP_HALO_LAST && NW <= 8 && FGP_NAMED_BARS;
     auto fgp_iter = [&](int it, auto cbv) {
         const int cb = cbv, pb = cb ^ 1;
         if (lane == 0) {   // the consuming warp arms its DSMEM receive buffers
@@ -850,6 +861,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             } else {
                 // slot of parity pb: written in iteration it - 1 (still 1/2 at it = 0)
                 if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
+                if constexpr (NBAR) { if (w > 0 && it > 0) bar_sync2(NW + w - 1); }   // r row of warp w - 1
                 row_ld_s(up_slot + pb * PS, lane, rup);
             }
             float sl = __shfl_up_sync(0xffffffffu, s[k][3].y, 1);
@@ -872,9 +884,10 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             if (k == 0) {
                 if (w == 0 && has_up) row_push(rem_rx_z + cb * PS, lane, z[0], rem_bar_z + cb * 8);
                 if (w > 0) row_st_s(my_z_slot + cb * PS, lane, z[0]);
+                if constexpr (NBAR) { if (w > 0) bar_arrive2(w); }           // z row -> warp w - 1
             }
         }
-        __syncthreads();
+        if constexpr (!NBAR) __syncthreads();
         // ---- phase B: dual ascent, projection on [0, 1] (shifted), FGP momentum;
         // last row first and publish it
         const float beta = c_fgp_beta[it];
@@ -888,6 +901,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 for (int c2 = 0; c2 < 4; ++c2) zb[c2] = z[k + 1][c2];
             } else {
                 if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
+                if constexpr (NBAR) { if (w < NW - 1) bar_sync2(w + 1); }     // z row of warp w + 1
                 row_ld_s(dn_slot + cb * PS, lane, zb);
             }
             const float zr = __shfl_down_sync(0xffffffffu, z[k][0].x, 1);   // lane 31: masked by gq
@@ -913,9 +927,10 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             if (k == FR - 1) {
                 if (w == NW - 1 && has_dn) row_push(rem_rx_r + cb * PS, lane, r[FR - 1], rem_bar_r + cb * 8);
                 if (w < NW - 1) row_st_s(my_r_slot + cb * PS, lane, r[FR - 1]);
+                if constexpr (NBAR) { if (w < NW - 1 && it + 1 < nit) bar_arrive2(NW + w); }   // r row -> warp w + 1
             }
         }
-        __syncthreads();
+        if constexpr (!NBAR) __syncthreads();
     };
     {
         int it = 0;
