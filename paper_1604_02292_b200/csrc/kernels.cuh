@@ -689,6 +689,9 @@ __device__ __forceinline__ void bar_sync2(int id) { asm volatile("bar.sync %0, 6
 #ifndef FGP_NAMED_BARS
 #define FGP_NAMED_BARS 0          // 1: named-barrier hand-over (measured slower: 1.35 vs 1.26 ms, C4 tiles)
 #endif
+#ifndef FGP_BAR_LATE
+#define FGP_BAR_LATE 0            // 1: barrier before each halo row (measured slower: 1.30 vs 1.26 ms)
+#endif
 #ifndef FGP_HALO_LAST
 #define FGP_HALO_LAST 1           // rows that read a halo are computed last in their phase
 #endif
@@ -843,6 +846,9 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     // before that row; otherwise a CTA barrier after each phase.  Parity cb is
     // compile-time, so every halo address is loop invariant.
     constexpr bool NBAR = FGP_HALO_LAST && NW <= 8 && FGP_NAMED_BARS;
+    // BAR_LATE: the CTA barrier sits right before each phase's halo row instead
+    // of at the phase end (same count; the segments between barriers balance)
+    constexpr bool BAR_LATE = FGP_HALO_LAST && !NBAR && FGP_BAR_LATE;
     auto fgp_iter = [&](int it, auto cbv) {
         const int cb = cbv, pb = cb ^ 1;
         if (lane == 0) {   // the consuming warp arms its DSMEM receive buffers
@@ -859,6 +865,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 #pragma unroll
                 for (int c2 = 0; c2 < 4; ++c2) rup[c2] = r[k - 1][c2];
             } else {
+                if constexpr (BAR_LATE) __syncthreads();   // every warp has published its r row of it - 1
                 // slot of parity pb: written in iteration it - 1 (still 1/2 at it = 0)
                 if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
                 if constexpr (NBAR) { if (w > 0 && it > 0) bar_sync2(NW + w - 1); }   // r row of warp w - 1
@@ -887,7 +894,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 if constexpr (NBAR) { if (w > 0) bar_arrive2(w); }           // z row -> warp w - 1
             }
         }
-        if constexpr (!NBAR) __syncthreads();
+        if constexpr (!NBAR && !BAR_LATE) __syncthreads();
         // ---- phase B: dual ascent, projection on [0, 1] (shifted), FGP momentum;
         // last row first and publish it
         const float beta = c_fgp_beta[it];
@@ -900,6 +907,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 #pragma unroll
                 for (int c2 = 0; c2 < 4; ++c2) zb[c2] = z[k + 1][c2];
             } else {
+                if constexpr (BAR_LATE) __syncthreads();   // every warp has published its z row of it
                 if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
                 if constexpr (NBAR) { if (w < NW - 1) bar_sync2(w + 1); }     // z row of warp w + 1
                 row_ld_s(dn_slot + cb * PS, lane, zb);
@@ -930,7 +938,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 if constexpr (NBAR) { if (w < NW - 1 && it + 1 < nit) bar_arrive2(NW + w); }   // r row -> warp w + 1
             }
         }
-        if constexpr (!NBAR) __syncthreads();
+        if constexpr (!NBAR && !BAR_LATE) __syncthreads();
     };
     {
         int it = 0;

@@ -8,7 +8,7 @@ template <int KIND>
 __global__ void kern(float* out, long long* cyc, float a, float b) {
     float2 x[NCH];
     float y[NCH];
-    for (int c = 0; c < NCH; ++c) { x[c % NCH] = make_float2(threadIdx.x * 1e-3f + c, c * 0.5f); y[c % NCH] = c * 0.25f; }
+    for (int c = 0; c < NCH; ++c) { x[c % NCH] = make_float2(threadIdx.x * 1e-3f + c, c * 0.5f); y[c % NCH] = c * 0.25f + threadIdx.x * 1e-3f; }
     const float2 a2 = make_float2(a, a), b2 = make_float2(b, b);
     long long t0 = clock64();
     #pragma unroll 1
@@ -21,6 +21,9 @@ __global__ void kern(float* out, long long* cyc, float a, float b) {
             if (KIND == 3) { x[c % NCH] = __fadd2_rn(x[c % NCH], b2); }                           // FADD2
             if (KIND == 4) { x[c % NCH] = __ffma2_rn(x[c % NCH], a2, b2); y[c % NCH] = __saturatef(fmaf(y[c % NCH], a, b)); }   // mix 1:1
             if (KIND == 5) { y[c % NCH] = fmaxf(y[c % NCH] * a, b); }                             // FMUL + FMNMX
+            if (KIND == 6) { unsigned u = __float_as_uint(y[c % NCH]); u = (u ^ 0x1234u) + (unsigned)c; y[c % NCH] = __uint_as_float(u); }   // LOP3 + IADD3 (-> IADD3/LOP3)
+            if (KIND == 7) { unsigned u = __float_as_uint(y[c % NCH]); u = (u >> 3) + (u << 5); y[c % NCH] = __uint_as_float(u); }   // SHF + LEA
+            if (KIND == 8) { unsigned u = __float_as_uint(y[c % NCH]); u = (u & 0x7FFFFFu) | 0x3F800000u; y[c % NCH] = __saturatef(fmaf(__uint_as_float(u + 0x100u), a, b)); }   // LOP3 + IADD + FFMA.SAT
         }
     }
     long long t1 = clock64();
@@ -42,7 +45,7 @@ void run(const char* name, float* d, long long* dc, int nsm) {
         int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
         long long hc[1024]; cudaMemcpy(hc, dc, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
         double cyc = 0; for (int i = 0; i < nsm; ++i) cyc += hc[i]; cyc /= nsm;
-        const double ninst = (double)IT * 4 * NCH * (KIND == 4 ? 2 : KIND == 5 ? 2 : 1) * w;   // per SMSP (warp-instr)
+        const double ninst = (double)IT * 4 * NCH * (KIND == 4 ? 2 : KIND == 5 ? 2 : KIND >= 6 ? 2 : 1) * w;   // per SMSP (warp-instr)
         printf("%-10s warps/SMSP=%d: %.3f ms, %.0f cyc (%.0f MHz), %.3f warp-inst/clk/SMSP\n", name, w, ms, cyc, cyc / (ms * 1e3), ninst / cyc);
     }
 }
@@ -51,5 +54,6 @@ int main() {
     float* d; cudaMalloc(&d, nsm * 1024 * sizeof(float)); long long* dc; cudaMalloc(&dc, 1024 * sizeof(long long));
     run<0>("FFMA", d, dc, nsm); run<1>("FFMA.SAT", d, dc, nsm); run<2>("FFMA2", d, dc, nsm);
     run<3>("FADD2", d, dc, nsm); run<4>("FFMA2+SAT", d, dc, nsm); run<5>("FMUL+FMNMX", d, dc, nsm);
+    run<6>("LOP3+IADD", d, dc, nsm); run<7>("SHF+LEA", d, dc, nsm); run<8>("LOP+ADD+SAT", d, dc, nsm);
     return 0;
 }
