@@ -689,6 +689,9 @@ __device__ __forceinline__ void bar_sync2(int id) { asm volatile("bar.sync %0, 6
 #ifndef FGP_NAMED_BARS
 #define FGP_NAMED_BARS 0          // 1: named-barrier hand-over (measured slower: 1.35 vs 1.26 ms, C4 tiles)
 #endif
+#ifndef FGP_HALO_PREFETCH
+#define FGP_HALO_PREFETCH 0       // 1: halo rows loaded at the phase start (255 registers; measured slower: 1.59 ms)
+#endif
 #ifndef FGP_BAR_LATE
 #define FGP_BAR_LATE 0            // 1: barrier before each halo row (measured slower: 1.30 vs 1.26 ms)
 #endif
@@ -857,6 +860,12 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         }
         // ---- phase A: z = b - lam2 L(r, s); row 0 first (its upper neighbour
         // may come from another warp or CTA) and publish it at once
+        // halo rows published before the last barrier: loaded now, used last
+        // (the DSMEM rows wait on their mbarrier first, at the halo row)
+        constexpr bool PRE = FGP_HALO_LAST && !NBAR && !BAR_LATE && FGP_HALO_PREFETCH;
+        const bool up_local = !(w == 0 && has_up);
+        float2 rpre[4];
+        if constexpr (PRE) { if (up_local) row_ld_s(up_slot + pb * PS, lane, rpre); }
         #pragma unroll
         for (int kk = 0; kk < FR; ++kk) {
             const int k = FGP_HALO_LAST ? (kk + 1) % FR : kk;     // halo row 0 last: 1, ..., FR-1, 0
@@ -867,9 +876,14 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             } else {
                 if constexpr (BAR_LATE) __syncthreads();   // every warp has published its r row of it - 1
                 // slot of parity pb: written in iteration it - 1 (still 1/2 at it = 0)
-                if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
-                if constexpr (NBAR) { if (w > 0 && it > 0) bar_sync2(NW + w - 1); }   // r row of warp w - 1
-                row_ld_s(up_slot + pb * PS, lane, rup);
+                if (PRE && up_local) {
+                    #pragma unroll
+                    for (int c2 = 0; c2 < 4; ++c2) rup[c2] = rpre[c2];
+                } else {
+                    if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
+                    if constexpr (NBAR) { if (w > 0 && it > 0) bar_sync2(NW + w - 1); }   // r row of warp w - 1
+                    row_ld_s(up_slot + pb * PS, lane, rup);
+                }
             }
             float sl = __shfl_up_sync(0xffffffffu, s[k][3].y, 1);
             if (lane == 0) sl = 0.5f;
@@ -899,6 +913,9 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         // last row first and publish it
         const float beta = c_fgp_beta[it];
         const float2 beta2 = f2s(beta);
+        const bool dn_local = !(w == NW - 1 && has_dn);
+        float2 zpre[4];
+        if constexpr (PRE) { if (dn_local) row_ld_s(dn_slot + cb * PS, lane, zpre); }
         #pragma unroll
         for (int kk = 0; kk < FR; ++kk) {
             const int k = FGP_HALO_LAST ? kk : (kk + FR - 1) % FR;   // halo row FR-1 last: 0, ..., FR-1
@@ -908,9 +925,14 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 for (int c2 = 0; c2 < 4; ++c2) zb[c2] = z[k + 1][c2];
             } else {
                 if constexpr (BAR_LATE) __syncthreads();   // every warp has published its z row of it
-                if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
-                if constexpr (NBAR) { if (w < NW - 1) bar_sync2(w + 1); }     // z row of warp w + 1
-                row_ld_s(dn_slot + cb * PS, lane, zb);
+                if (PRE && dn_local) {
+                    #pragma unroll
+                    for (int c2 = 0; c2 < 4; ++c2) zb[c2] = zpre[c2];
+                } else {
+                    if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
+                    if constexpr (NBAR) { if (w < NW - 1) bar_sync2(w + 1); }     // z row of warp w + 1
+                    row_ld_s(dn_slot + cb * PS, lane, zb);
+                }
             }
             const float zr = __shfl_down_sync(0xffffffffu, z[k][0].x, 1);   // lane 31: masked by gq
             const float gpk = gp[k];
