@@ -245,7 +245,9 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
     const int nsx = (t.T + BP_SUB - 1) / BP_SUB;
     const long long ctas64 = e.blist ? nblist : (long long)nsx * nsx * t.ntiles;
     ScopedTimer tm(e.blist ? TC_XS : TC_BP, st);   // block-listed launches: the global x_s backprojection
-    if (!e.blist && ctas64 < 2LL * 3 * p.num_sms) {
+    static int sub_env = -1;
+    if (sub_env < 0) { const char* v = getenv("LT_BP_SUB"); sub_env = v ? atoi(v) : 0; }
+    if (!e.blist && (sub_env == 32 || (sub_env != 64 && ctas64 < 2LL * 3 * p.num_sms))) {
         const int nsx32 = (t.T + 31) / 32;
         k_bp<NS, MODE, 32><<<dim3(nsx32 * nsx32, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
     } else {
