@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(128) k_fp(Geo g, Tiles t, FpArgs f) {
     }
 }
 
-constexpr int FP_GA = 8;     // angles per CTA of the ROI forward projector (one warp per angle)
+constexpr int FP_APW = 2;    // angles per warp of the ROI forward projector
+constexpr int FP_GA = 8 * FP_APW;   // angles per CTA (they share each staged band)
 constexpr int FP_U = 12;     // rays per lane: window width <= 32 * FP_U
 
 // keeps ptxas from re-materialising a folded address bias (a mov it cannot see through)
@@ -222,7 +223,6 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
     const int r = blockIdx.y, grp = blockIdx.x;
     const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a = groups[grp * FP_GA + warp];                     // this warp's angle (-1: idle warp)
     const int a0 = groups[grp * FP_GA];
     const int col = g.ang[a0].col;
     const TileT ti = t.tile[r];
@@ -230,18 +230,7 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
     const int pv0 = col ? ti.vr0 : ti.vc0, pv1 = col ? ti.vr1 : ti.vc1;
     const double Lc = 0.5 * (T - 1);
     const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
-    double A = 0.0, B = 0.0, tauc = 0.0;
-    int d0 = 0;
-    if (a >= 0) {
-        A = g.A64[a]; B = g.B64[a];
-        tauc = t.tauc[r * na + a];
-        d0 = __ldg(t.d0 + r * na + a);
-    }
-    const float Bf = (float)B;
-    float* acc = sacc + warp * (32 * FP_U);
     for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += 256) sacc[e] = 0.f;
-    // rays with a detector bin: w in [wv0, wv1)
-    const int wv0 = max(0, -d0), wv1 = min(Wwin, g.nd - d0);
 
     // staging map (no division): thread = (line tid / 16, chunks c4 = tid % 16 + 16 u)
     const int q4 = TP / 4;                        // float4 chunks per raw line
@@ -281,7 +270,17 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
     for (int l0 = lbeg; l0 < lv1; l0 += FP2_BL) {
         const bool more = l0 + FP2_BL < lv1;
         if (more) fetch(l0 + FP2_BL);
-        if (a >= 0) {
+        #pragma unroll 1
+        for (int j = 0; j < FP_APW; ++j) {
+            const int a = groups[grp * FP_GA + warp * FP_APW + j];    // this warp's angle j (-1: idle)
+            if (a < 0) continue;
+            const double A = g.A64[a], B = g.B64[a];
+            const double tauc = t.tauc[r * na + a];
+            const int d0 = __ldg(t.d0 + r * na + a);
+            const float Bf = (float)B;
+            float* acc = sacc + (warp * FP_APW + j) * (32 * FP_U);
+            // rays with a detector bin: w in [wv0, wv1)
+            const int wv0 = max(0, -d0), wv1 = min(Wwin, g.nd - d0);
             // rays meeting the valid pixels (pv0 - 1, pv1) on some line of the band
             const double P0 = Lc - tauc * A + ((double)l0 - Lc) * B;           // p(w, l0) = P0 + w A
             const double P1 = P0 + (double)(FP2_BL - 1) * B;                   // p(w, l0 + 15) = P1 + w A
@@ -321,7 +320,11 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
         if (more) transform();
         __syncthreads();
     }
-    if (a >= 0) {
+    for (int j = 0; j < FP_APW; ++j) {
+        const int a = groups[grp * FP_GA + warp * FP_APW + j];
+        if (a < 0) continue;
+        const int d0 = __ldg(t.d0 + r * na + a);
+        const float* acc = sacc + (warp * FP_APW + j) * (32 * FP_U);
         const float sc = 0.5f * g.ang[a].invc;        // (S + g D) = 2 lerp
         for (int w = lane; w < Wwin; w += 32) {
             const int d = d0 + w;
