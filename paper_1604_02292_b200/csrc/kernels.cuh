@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(128) k_fp(Geo g, Tiles t, FpArgs f) {
     }
 }
 
-constexpr int FP_APW = 2;    // angles per warp of the ROI forward projector
-constexpr int FP_GA = 8 * FP_APW;   // angles per CTA (they share each staged band)
+constexpr int FP_APW_MAX = 2;          // angles per warp of the ROI forward projector (1 for small batches)
+constexpr int FP_GA = 8 * FP_APW_MAX;  // angles per CTA at the default 2 per warp (they share each staged band)
 constexpr int FP_U = 12;     // rays per lane: window width <= 32 * FP_U
 
 // keeps ptxas from re-materialising a folded address bias (a mov it cannot see through)
@@ -216,7 +216,9 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
     return acc;
 }
 
+template <int FP_APW>
 __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, const int* __restrict__ groups) {
+    constexpr int FP_GA = 8 * FP_APW;
     extern __shared__ float4 smf4[];
     float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][FP2_P] (S, D), entry 0 = pixel -PADL
     float* sacc = reinterpret_cast<float*>(sd + FP2_BL * FP2_P);  // [FP_GA][32 * FP_U] per-ray accumulators
@@ -385,8 +387,17 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     const int r = blockIdx.y;
     const int T = t.T, na = g.na;
     const int nsx = (T + SUB - 1) / SUB;
-    const int sub = e.blist ? __ldg(e.blist + blockIdx.x) : (int)blockIdx.x;
-    const int sty = sub / nsx, stx = sub - sty * nsx;
+    int sty, stx;
+    if (e.blist && SUB == 32) {     // block list in 64x64 units: four 32x32 CTAs per listed block
+        const int nsx64 = (T + 63) / 64;
+        const int b = __ldg(e.blist + (blockIdx.x >> 2));
+        const int by = b / nsx64, bx = b - by * nsx64;
+        sty = 2 * by + ((blockIdx.x >> 1) & 1);
+        stx = 2 * bx + (blockIdx.x & 1);
+    } else {
+        const int sub = e.blist ? __ldg(e.blist + blockIdx.x) : (int)blockIdx.x;
+        sty = sub / nsx; stx = sub - sty * nsx;
+    }
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int pj0 = stx * SUB + lane;                  // columns pj0, pj0 + 32
     const int pi0 = sty * SUB + wq * BP_PR;            // rows pi0 .. pi0 + BP_PR - 1

@@ -92,11 +92,12 @@ struct lt_plan {
     // tiled global forward projection: the grid cut into Tg x Tg tiles, each
     // projected by the ROI kernel onto its window, windows summed per bin
     int Tg = 0, TPg = 0, Wg = 0, NTg = 0;
-    std::vector<int> fpgroups;    // [ngroups][FP_GA] angle indices of one orientation, -1 padded
+    std::vector<int> fpgroups;    // [ngroups][16] angle indices of one orientation, -1 padded (2 per warp)
+    std::vector<int> fpgroups1;   // [ngroups1][8] the same, one angle per warp
     // BP_SUB^2 image blocks that the global x_s^k backprojection must cover: list 0 for
     // all local ROIs, lists 1 and 2 for the two pipelined ROI groups (halves)
     std::vector<int> xsblk[3];
-    int ngroups = 0;
+    int ngroups = 0, ngroups1 = 0;
     // workspace
     char* ws = nullptr;
     int64_t ws_bytes = 0;
@@ -130,7 +131,7 @@ struct lt_plan {
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t pev[2] = {nullptr, nullptr}, fev[2] = {nullptr, nullptr};
     struct {
-        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups;
+        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups, fpgroups1;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
@@ -198,12 +199,20 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
                   float* out, long long out_ts, cudaStream_t st) {
     if (t.TP > FP2_P || t.Wwin > 32 * FP_U)
         return launch_fp(p, 0, t, img, imgT, img_ts, out, out_ts, nullptr, nullptr, st);
-    const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)FP_GA * 32 * FP_U * sizeof(float);
-    LT_CUDA(cudaFuncSetAttribute(k_fp_roi2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    // 16 angles per CTA share each staged band; 8 when that would leave the
+    // SMs short of two waves (small ROI batches: C1-C3, T1, 8-GPU shards)
+    const bool one = (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
+    const int apw = one ? 1 : 2;
+    const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
-    dim3 grid(p.ngroups, t.ntiles);
     ScopedTimer tm(TC_FP, st);
-    k_fp_roi2<<<grid, 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
+    if (one) {
+        LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
+    } else {
+        LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        k_fp_roi2<2><<<dim3(p.ngroups, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
+    }
     LT_LAUNCHED();
     return LT_OK;
 }
@@ -237,7 +246,8 @@ int global_fp(const lt_plan& p, int mode, const float* img, const float* imgT, f
 
 // 64 x 64 sub-tiles per CTA; 32 x 32 when a batch would give fewer than about
 // two waves of 64 x 64 CTAs (small ROI counts: C2, C3, 8-GPU shards), so the
-// SMs stay busy (block lists are always in 64 x 64 units)
+// SMs stay busy (block lists are in 64 x 64 units: a listed block becomes four
+// 32 x 32 CTAs)
 template <int NS, int MODE>
 int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const SinoView& s2, const BpEpi& e,
                 cudaStream_t st, int nblist = 0) {
@@ -247,9 +257,9 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
     ScopedTimer tm(e.blist ? TC_XS : TC_BP, st);   // block-listed launches: the global x_s backprojection
     static int sub_env = -1;
     if (sub_env < 0) { const char* v = getenv("LT_BP_SUB"); sub_env = v ? atoi(v) : 0; }
-    if (!e.blist && (sub_env == 32 || (sub_env != 64 && ctas64 < 2LL * 3 * p.num_sms))) {
+    if (sub_env == 32 || (sub_env != 64 && ctas64 < 2LL * 3 * p.num_sms)) {
         const int nsx32 = (t.T + 31) / 32;
-        k_bp<NS, MODE, 32><<<dim3(nsx32 * nsx32, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
+        k_bp<NS, MODE, 32><<<dim3(e.blist ? 4 * nblist : nsx32 * nsx32, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
     } else {
         k_bp<NS, MODE, BP_SUB><<<dim3(e.blist ? nblist : nsx * nsx, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
     }
@@ -892,20 +902,24 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         // tile centre point (x, y) = (cc - N/2, N/2 - cr)
         tile_window(*p, cc - 0.5 * n, 0.5 * n - cr, p->Wwin, &p->d0[(size_t)q * n_angles], &p->tauc[(size_t)q * n_angles]);
     }
-    // forward-projection angle groups: one orientation per group
-    for (int o = 0; o < 2; ++o) {
-        std::vector<int> cur;
-        for (int a = 0; a < n_angles; ++a)
-            if (p->angf[a].col == o) {
-                cur.push_back(a);
-                if ((int)cur.size() == FP_GA) { p->fpgroups.insert(p->fpgroups.end(), cur.begin(), cur.end()); cur.clear(); }
+    // forward-projection angle groups (16 and 8 angles): one orientation per group
+    for (int ga : {16, 8}) {
+        std::vector<int>& grp = ga == 16 ? p->fpgroups : p->fpgroups1;
+        for (int o = 0; o < 2; ++o) {
+            std::vector<int> cur;
+            for (int a = 0; a < n_angles; ++a)
+                if (p->angf[a].col == o) {
+                    cur.push_back(a);
+                    if ((int)cur.size() == ga) { grp.insert(grp.end(), cur.begin(), cur.end()); cur.clear(); }
+                }
+            if (!cur.empty()) {
+                cur.resize(ga, -1);
+                grp.insert(grp.end(), cur.begin(), cur.end());
             }
-        if (!cur.empty()) {
-            cur.resize(FP_GA, -1);
-            p->fpgroups.insert(p->fpgroups.end(), cur.begin(), cur.end());
         }
     }
-    p->ngroups = (int)p->fpgroups.size() / FP_GA;
+    p->ngroups = (int)p->fpgroups.size() / 16;
+    p->ngroups1 = (int)p->fpgroups1.size() / 8;
     // x_s block lists: blocks meeting any valid extended rect
     {
         const int nbk = (n + BP_SUB - 1) / BP_SUB;
@@ -974,6 +988,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.tstack = take((size_t)p->NTg * p->Tg * p->TPg * fs); f.tstackT = take((size_t)p->NTg * p->Tg * p->TPg * fs);
     f.twin = take((size_t)p->NTg * n_angles * p->Wg * fs);
     f.fpgroups = take(p->fpgroups.size() * 4);
+    f.fpgroups1 = take(p->fpgroups1.size() * 4);
     f.bank = take((size_t)n_iter * ns * fs); f.conv = take((size_t)n_iter * ns * fs);
     f.pc = take(ns * fs); f.wd = take(ns * fs); f.wdsum = take(n_angles * 8); f.psum = take(n_angles * 8);
     f.discc64 = take(8); f.discc32 = take(4); f.err = take(4);
@@ -1053,6 +1068,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.tstack, 0, (size_t)p->NTg * p->Tg * p->TPg * sizeof(float), st));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.tstackT, 0, (size_t)p->NTg * p->Tg * p->TPg * sizeof(float), st));
     LT_CUDA(up(p->off.fpgroups, p->fpgroups.data(), p->fpgroups.size() * 4));
+    LT_CUDA(up(p->off.fpgroups1, p->fpgroups1.data(), p->fpgroups1.size() * 4));
     for (int l = 0; l < 3; ++l)
         if (!p->xsblk[l].empty()) LT_CUDA(up(p->off.xsblk[l], p->xsblk[l].data(), p->xsblk[l].size() * 4));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));
