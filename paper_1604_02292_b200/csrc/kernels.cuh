@@ -96,6 +96,9 @@ struct FpArgs {
     const float* aux_in;    // MODE 1: bank_{k-1} (nullable); MODE 2: p
     float* aux_out;         // MODE 1: bank_k
     float alpha;
+    // k_fp_roi2 band split (single ROIs): CTA z marches bands z, z + nsplit, ...
+    // and writes raw ray sums to part [z][tile][na][Wwin]; k_fp_join sums them
+    float* part; int nsplit;
 };
 
 template <int MODE>
@@ -265,13 +268,14 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
             }
         }
     };
-    const int lbeg = (lv0 / FP2_BL) * FP2_BL;
+    const int nsplit = f.nsplit > 1 ? f.nsplit : 1;
+    const int lbeg = (lv0 / FP2_BL) * FP2_BL + (int)blockIdx.z * FP2_BL, lstep = nsplit * FP2_BL;
     if (lbeg < lv1) { fetch(lbeg); transform(); }
     __syncthreads();
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd + PADL);     // entry of pixel 0
-    for (int l0 = lbeg; l0 < lv1; l0 += FP2_BL) {
-        const bool more = l0 + FP2_BL < lv1;
-        if (more) fetch(l0 + FP2_BL);
+    for (int l0 = lbeg; l0 < lv1; l0 += lstep) {
+        const bool more = l0 + lstep < lv1;
+        if (more) fetch(l0 + lstep);
         #pragma unroll 1
         for (int j = 0; j < FP_APW; ++j) {
             const int a = groups[grp * FP_GA + warp * FP_APW + j];    // this warp's angle j (-1: idle)
@@ -327,12 +331,28 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
         if (a < 0) continue;
         const int d0 = __ldg(t.d0 + r * na + a);
         const float* acc = sacc + (warp * FP_APW + j) * (32 * FP_U);
+        if (nsplit > 1) {
+            float* dst = f.part + (((long long)blockIdx.z * gridDim.y + r) * na + a) * Wwin;
+            for (int w = lane; w < Wwin; w += 32) dst[w] = acc[w];
+            continue;
+        }
         const float sc = 0.5f * g.ang[a].invc;        // (S + g D) = 2 lerp
         for (int w = lane; w < Wwin; w += 32) {
             const int d = d0 + w;
             f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = (d >= 0 && d < g.nd) ? acc[w] * sc : 0.f;
         }
     }
+}
+
+// the band-split partial ray sums of k_fp_roi2, summed in split order
+__global__ void k_fp_join(Geo g, Tiles t, FpArgs f) {
+    const int r = blockIdx.z, a = blockIdx.y, w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int na = g.na, Wwin = t.Wwin;
+    if (w >= Wwin) return;
+    float sum = 0.f;
+    for (int z = 0; z < f.nsplit; ++z) sum += f.part[(((long long)z * gridDim.z + r) * na + a) * Wwin + w];
+    const int d = __ldg(t.d0 + r * na + a) + w;
+    f.out[(long long)r * f.out_tstride + (long long)a * Wwin + w] = (d >= 0 && d < g.nd) ? sum * (0.5f * g.ang[a].invc) : 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -371,6 +391,10 @@ struct BpEpi {
     float* v; float* xs; long long p_tstride;              // plain [T][T] (TV)
     const float* discc; int use_disc;                      // disc gray value (device)
     float alpha, lo, hi; int last;
+    // angle split for small batches: stage 1 = CTA z gathers angles
+    // [z achunk, (z + 1) achunk) into part (CTA-local layout, no epilogue);
+    // stage 2 = the same grid sums the nsa partials in order, then the epilogue
+    float* part; int nsa, stage, achunk;
 };
 
 template <int NS, int MODE, int SUB = BP_SUB>
@@ -406,6 +430,10 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     const double dxc = stx * SUB + hs - Lc, dyc = sty * SUB + hs - Lc;
     const float dx = (float)lane - (float)hs, dy0 = (float)(wq * BP_PR) - (float)hs;
 
+    // angles this CTA gathers (all, or one chunk of an angle-split stage 1; none in stage 2)
+    const int az0 = e.stage == 1 ? (int)blockIdx.z * e.achunk : 0;
+    const int az1 = e.stage == 1 ? min(na, az0 + e.achunk) : na;
+    const bool gather = NS > 0 && e.stage != 2;
     float2 acc[COLS][BP_PR];                      // (left-tap, right-tap) partial sums per pixel
     #pragma unroll
     for (int h = 0; h < COLS; ++h)
@@ -421,7 +449,7 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
         return (int)floor(tc) - BP_SW / 2;                       // window bins sub0 .. sub0 + BP_SW
     };
     auto prefetch = [&](int a0n) {
-        const int can = min(BP_CA, na - a0n);
+        const int can = min(BP_CA, az1 - a0n);
         #pragma unroll
         for (int qq = 0; qq < RPW; ++qq) {
             const int q = wq + 8 * qq, a = a0n + q;
@@ -436,9 +464,9 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
             }
         }
     };
-    if (NS > 0) prefetch(0);
-    for (int a0 = 0; a0 < (NS > 0 ? na : 0); a0 += BP_CA) {
-        const int ca = min(BP_CA, na - a0);
+    if (gather && az0 < az1) prefetch(az0);
+    for (int a0 = az0; a0 < (gather ? az1 : az0); a0 += BP_CA) {
+        const int ca = min(BP_CA, az1 - a0);
         __syncthreads();
         #pragma unroll
         for (int qq = 0; qq < RPW; ++qq) {
@@ -461,7 +489,7 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
             }
         }
         __syncthreads();
-        if (a0 + BP_CA < na) prefetch(a0 + BP_CA);
+        if (a0 + BP_CA < az1) prefetch(a0 + BP_CA);
         // entry of bin m (relative to the window centre) at swbase + 8 (m + MAGIC bits)
         const unsigned swbase = opaque_u32((unsigned)__cvta_generic_to_shared(&sw[0][BP_SW / 2]) - 8u * (unsigned)MAGICI);
         #pragma unroll 1
@@ -504,6 +532,23 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     float g1[BP_PR];
     #pragma unroll
     for (int p = 0; p < BP_PR; ++p) g1[p] = acc[h][p].x + acc[h][p].y;
+    if (SUB == 32 && e.stage != 0) {   // angle split (32x32 launches only): partial sums per CTA-local pixel
+        const long long ctas = (long long)gridDim.x * gridDim.y;
+        const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+        const int loc = (wq * BP_PR) * SUB + lane + 32 * h;
+        if (e.stage == 1) {
+            float* dst = e.part + ((long long)blockIdx.z * ctas + cta) * (SUB * SUB) + loc;
+            #pragma unroll
+            for (int p = 0; p < BP_PR; ++p) dst[p * SUB] = g1[p];
+            continue;
+        }
+        #pragma unroll
+        for (int p = 0; p < BP_PR; ++p) {
+            float sum = 0.f;
+            for (int z = 0; z < e.nsa; ++z) sum += e.part[((long long)z * ctas + cta) * (SUB * SUB) + loc + p * SUB];
+            g1[p] = sum;
+        }
+    }
 
     // ---- epilogue ------------------------------------------------------------
     if (MODE == BP_BOX || MODE == BP_TV) {

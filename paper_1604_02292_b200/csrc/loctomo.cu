@@ -78,6 +78,8 @@ struct lt_plan {
     int T = 0, TP = 0, Wwin = 0, n_iter = 0, flags = 0, rank = 0, world = 1;
     int GT = 0, GTP = 0;          // global tile (whole image)
     int num_sms = 148;            // of the bound device (launch sizing)
+    long long bpart_cap = 0;      // floats of the angle-split backprojection partials (small batches)
+    long long fpart_cap = 0;      // floats of the band-split forward-projection partials
     double alpha = 0.0;
     std::vector<double> ang;
     std::vector<int> cen;         // [nroi_all][2]
@@ -131,7 +133,7 @@ struct lt_plan {
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t pev[2] = {nullptr, nullptr}, fev[2] = {nullptr, nullptr};
     struct {
-        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups, fpgroups1;
+        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups, fpgroups1, bpart, fpart;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
@@ -204,11 +206,23 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
     const bool one = (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
     const int apw = one ? 1 : 2;
     const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
-    FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha};
+    FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1};
     ScopedTimer tm(TC_FP, st);
     if (one) {
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
+        // at most one CTA per SM (single ROIs: T1): split the 16-line bands over
+        // nsplit CTAs per (tile, angle group), joined by k_fp_join in split order
+        const long long ctas = (long long)p.ngroups1 * t.ntiles;
+        const int nbands = (t.T + FP2_BL - 1) / FP2_BL;
+        int nsplit = ctas <= p.num_sms ? (int)std::min<long long>({8LL, (long long)nbands / 2, (2LL * 3 * p.num_sms + ctas - 1) / ctas}) : 1;
+        if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
+            f.part = p.P<float>(p.off.fpart); f.nsplit = nsplit;
+            k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles, nsplit), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
+            LT_LAUNCHED();
+            k_fp_join<<<dim3((t.Wwin + 127) / 128, p.na, t.ntiles), 128, 0, st>>>(p.geo(), t, f);
+        } else {
+            k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
+        }
     } else {
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
         k_fp_roi2<2><<<dim3(p.ngroups, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
@@ -259,7 +273,27 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
     if (sub_env < 0) { const char* v = getenv("LT_BP_SUB"); sub_env = v ? atoi(v) : 0; }
     if (sub_env == 32 || (sub_env != 64 && ctas64 < 2LL * 3 * p.num_sms)) {
         const int nsx32 = (t.T + 31) / 32;
-        k_bp<NS, MODE, 32><<<dim3(e.blist ? 4 * nblist : nsx32 * nsx32, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
+        const dim3 grid(e.blist ? 4 * nblist : nsx32 * nsx32, t.ntiles);
+        // at most one CTA per SM (single ROIs: T1, the x_s blocks of one ROI):
+        // split the angles over nsa CTAs per block (stage 1: partial sums;
+        // stage 2: their ordered sum + the epilogue).  Measured: T1 ROI BP 76 ->
+        // 36 us; with 2 CTAs per SM already (C2) the extra pass costs more than it gains
+        const long long ctas = (long long)grid.x * grid.y;
+        int nsa = NS > 0 && p.bpart_cap > 0 && ctas <= p.num_sms
+                      ? (int)std::min<long long>(8, (2LL * 3 * p.num_sms + ctas - 1) / ctas) : 1;
+        const int achunk = ((p.na + nsa - 1) / nsa + BP_CA - 1) / BP_CA * BP_CA;
+        nsa = (p.na + achunk - 1) / achunk;
+        if (nsa > 1 && (long long)nsa * ctas * 32 * 32 <= p.bpart_cap) {
+            BpEpi e1 = e;
+            e1.part = p.P<float>(p.off.bpart); e1.nsa = nsa; e1.achunk = achunk;
+            e1.stage = 1;
+            k_bp<NS, MODE, 32><<<dim3(grid.x, grid.y, nsa), 256, 0, st>>>(p.geo(), t, s1, s2, e1);
+            LT_LAUNCHED();
+            e1.stage = 2;
+            k_bp<NS, MODE, 32><<<grid, 256, 0, st>>>(p.geo(), t, s1, s2, e1);
+        } else {
+            k_bp<NS, MODE, 32><<<grid, 256, 0, st>>>(p.geo(), t, s1, s2, e);
+        }
     } else {
         k_bp<NS, MODE, BP_SUB><<<dim3(e.blist ? nblist : nsx * nsx, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
     }
@@ -989,6 +1023,12 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.twin = take((size_t)p->NTg * n_angles * p->Wg * fs);
     f.fpgroups = take(p->fpgroups.size() * 4);
     f.fpgroups1 = take(p->fpgroups1.size() * 4);
+    // angle-split BP partials: up to 8 chunks x two waves of 32x32 CTAs (<= 160 SMs x 3)
+    p->bpart_cap = 8LL * 2 * 3 * 160 * 32 * 32;
+    f.bpart = take((size_t)p->bpart_cap * fs);
+    // band-split FP partials: up to 8 splits x one wave of 8-angle CTAs (<= 160 SMs)
+    p->fpart_cap = 8LL * 160 * 8 * 32 * FP_U;
+    f.fpart = take((size_t)p->fpart_cap * fs);
     f.bank = take((size_t)n_iter * ns * fs); f.conv = take((size_t)n_iter * ns * fs);
     f.pc = take(ns * fs); f.wd = take(ns * fs); f.wdsum = take(n_angles * 8); f.psum = take(n_angles * 8);
     f.discc64 = take(8); f.discc32 = take(4); f.err = take(4);

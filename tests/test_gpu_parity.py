@@ -179,6 +179,24 @@ def test_sirt_solve_C1(lt, orc):
     assert cores.min() >= 0.0
 
 
+def test_single_roi_split_launches(lt, orc):
+    """One 256x256 extended ROI with 192 angles (the T1 shape at fewer angles and
+    iterations): fewer CTAs than SMs, so the ROI forward projector splits its
+    bands and the backprojections their angles (two-pass, ordered sums)."""
+    cfg = synth.Config(22, "single-split", 384, 192, math.pi, 545, "poisson", 1e4, 1, 96, 32, "centre", 6,
+                       "tv", 0.05, 20, 5, 0)
+    inp = synth.make_inputs(cfg)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    cores = cpu(plan.sirt_solve(gpu(inp.sino), 0.0, math.inf))
+    ref, _ = _oracle_solve(orc, inp, cfg, cfg.n_iter, "box")
+    assert relerr(cores, ref) <= 1e-3
+    cores = cpu(plan.tv_solve(gpu(inp.sino), cfg.lam, cfg.n_fgp))
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, inp.centres, cfg.radius, cfg.margin,
+                       cfg.n_iter, mode="tv", lam=cfg.lam, n_fgp=cfg.n_fgp)
+    assert relerr(cores[0], ref[0]) <= 1e-3
+
+
 def test_tv_solve_small(lt, orc):
     cfg = synth.Config(20, "tvsmall", 128, 24, math.pi, 181, "poisson", 1e4, 5, 16, 16, "seeded", 12, "tv",
                        0.05, 50, 6, 0)
