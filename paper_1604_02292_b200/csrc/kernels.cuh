@@ -792,7 +792,7 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 // BSM: b (read once per iteration) lives in shared memory instead of registers,
 // so the kernel fits 128 registers and two CTAs (two tiles) share an SM: one
 // tile's halo latency is hidden behind the other tile's arithmetic.
-template <int MODE, int FR, int NW, int SYNC, bool BSM>
+template <int MODE, int FR, int NW, bool BSM>
 __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpArgs A) {
     using SM = Fgp2Smem<FR, NW>;
     extern __shared__ __align__(16) float sm[];

@@ -343,13 +343,13 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
 // k_fgp2 (paired-FP32 layout): NW warps of FR full rows per CTA, K CTAs per
 // cluster.  LT_FGP2_CFG = "4x8" (default, 8-CTA clusters for 256-row tiles),
 // "2x8" (16-CTA clusters), "2x8b" (b in shared memory, two CTAs per SM).
-template <int MODE, int FR, int NW, int SYNC, bool BSM = false>
+template <int MODE, int FR, int NW, bool BSM = false>
 int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
     const size_t smem = (size_t)((BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) +
                                  (MODE == 1 ? Fgp2Smem<FR, NW>::xin_floats : 0)) * sizeof(float);
-    auto kern = k_fgp2<MODE, FR, NW, SYNC, BSM>;
+    auto kern = k_fgp2<MODE, FR, NW, BSM>;
     LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg;
@@ -385,10 +385,10 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     int nsm = 148;
     { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
     const bool small = ntiles * ((rows + 31) / 32) < nsm && rows > 16;
-    if (cfgv == 1 || (cfgv == 0 && small && (rows + 15) / 16 <= 16)) return launch_fgp2_t<MODE, 2, 8, 0>(A, rows, ntiles, st);
-    if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, 0, true>(A, rows, ntiles, st);
-    if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, 0, true>(A, rows, ntiles, st);
-    return launch_fgp2_t<MODE, 4, 8, 0>(A, rows, ntiles, st);
+    if (cfgv == 1 || (cfgv == 0 && small && (rows + 15) / 16 <= 16)) return launch_fgp2_t<MODE, 2, 8>(A, rows, ntiles, st);
+    if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, true>(A, rows, ntiles, st);
+    if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, true>(A, rows, ntiles, st);
+    return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
 }
 
 dim3 grid2d(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }

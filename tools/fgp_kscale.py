@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, '.')
 import torch
 import paper_1604_02292_b200 as lt
-tag = f"cfg={os.environ.get('LT_FGP2_CFG', '-')} sync={os.environ.get('LT_FGP2_SYNC', '0')}"
+tag = f"cfg={os.environ.get('LT_FGP2_CFG', '-')}"
 for H in (32, 64, 128, 256):
     x = torch.rand(256 * 256 // H, H, 256, device='cuda')
     for _ in range(2): lt.fgp_batch(x, 0.05, 100)

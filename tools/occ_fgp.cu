@@ -5,7 +5,7 @@
 using namespace lt;
 template <int FR, int NW, bool BSM>
 void q(int K) {
-    auto kern = k_fgp2<1, FR, NW, 0, BSM>;
+    auto kern = k_fgp2<1, FR, NW, BSM>;
     const size_t smem = (size_t)(BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) * sizeof(float);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
