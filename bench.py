@@ -50,6 +50,10 @@ def parse():
                          "exterior: NEXT-4(ii) exterior-subtraction box-SIRT (the prior art) for comparison")
     ap.add_argument("--combine", default="peer", choices=["peer", "nccl"],
                     help="N > 1: stitch reading the peers' cores over NVLink (CUDA IPC, one kernel) or NCCL all-gather + stitch")
+    ap.add_argument("--bank", default="local", choices=["local", "split"],
+                    help="N > 1: every rank computes the whole filter bank (no communication), or the "
+                         "angle-split cold bank (rank g owns N_theta/N angles, NCCL all-reduce of the N x N "
+                         "partial image per Alg. 1 step, all-gather of the bank rows); reported as bank_ms")
     ap.add_argument("--xs-exact", action="store_true",
                     help="NEXT-4(i): x_s^k from the global SIRT iterate instead of the filtered backprojection")
     return ap.parse_args()
@@ -174,7 +178,11 @@ def run_ours(args, cfg):
     # per-geometry precompute (outside the timed region)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    plan.filter_bank()
+    if args.bank == "split" and world > 1:
+        from paper_1604_02292_b200 import dist as ltd
+        ltd.filter_bank_split(plan)
+    else:
+        plan.filter_bank()
     torch.cuda.synchronize()
     bank_ms = (time.perf_counter() - t0) * 1e3
 
@@ -397,6 +405,8 @@ def run_ours(args, cfg):
         "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
         "fgp_gpix_it_s": round(fgp_pi / (ms_per_step / 1e3) / 1e9, 2),
         "bank_ms": round(bank_ms, 2),
+        "bank_mode": ("angle-split (NCCL all-reduce per Alg. 1 step)" if args.bank == "split" and world > 1
+                      else "local (every rank computes the whole bank)"),
         "kernels": kshare,
         "gpu_launches": int(n_launch),
         "e2e": {"value": round(cfg.n_roi / (e2e_ms / 1e3), 3), "unit": UNIT,

@@ -94,6 +94,26 @@ int lt_filter_bank(lt_plan* plan, void* stream);
 
 /* Copy a filter bank [n_iter][N_theta][N_d] fp32 (device) into / out of the
  * plan (per-geometry reuse). */
+/* Angle-split Alg. 1 for a cold bank on G ranks (P:L489-503 with
+ * W = [W_0; ...; W_{G-1}] split by angle rows): rank g owns angles [a0, a1).
+ *   lt_bank_split_begin: c = e_c (the centred impulse, reading A5) in the plan's
+ *     global image; records [a0, a1).  Errors: 2 if the range is empty or
+ *     outside [0, n_angles).
+ *   lt_bank_split_step(k): v_g = W_g c; bank rows u_k[a] = u_{k-1}[a] + alpha v_g[a]
+ *     for a in [a0, a1) (rows of other angles untouched); for k < n_iter - 1 also
+ *     d_partial = W_g^T v_g, a plain row-major N x N device image (caller-owned).
+ *     Errors: 2 if begin was not called, k outside [0, n_iter), d_partial null
+ *     when needed, or the geometry needs the single-pass projector (tiles wider
+ *     than the tiled projector's band).
+ *   lt_bank_split_apply: c <- c - alpha d_reduced, d_reduced = sum over ranks of
+ *     the partials (the caller's all-reduce, N x N device image).
+ * Steps must be issued in order k = 0, 1, ... with apply between steps.  After
+ * step n_iter - 1 the plan holds its own rows of every u_k (lt_get_bank returns
+ * them, the other rows unspecified); the caller gathers the other ranks' rows
+ * and installs the full bank with lt_set_bank. */
+int lt_bank_split_begin(lt_plan* plan, int32_t a0, int32_t a1, void* stream);
+int lt_bank_split_step(lt_plan* plan, int32_t k, float* d_partial, void* stream);
+int lt_bank_split_apply(lt_plan* plan, const float* d_reduced, void* stream);
 int lt_set_bank(lt_plan* plan, const float* d_bank, void* stream);
 int lt_get_bank(const lt_plan* plan, float* d_bank, void* stream);
 

@@ -44,6 +44,9 @@ _SIGS = {
     "lt_plan_tables": ([_P, _P, _P, _P], _I),
     "lt_filter_bank": ([_P, _P], _I),
     "lt_set_bank": ([_P, _P, _P], _I),
+    "lt_bank_split_begin": ([_P, _I, _I, _P], _I),
+    "lt_bank_split_step": ([_P, _I, _P, _P], _I),
+    "lt_bank_split_apply": ([_P, _P, _P], _I),
     "lt_get_bank": ([_P, _P, _P], _I),
     "lt_project": ([_P, _I, _P, _P, _P], _I),
     "lt_backproject": ([_P, _I, _P, _P, _P], _I),
@@ -199,6 +202,23 @@ class Plan:
         assert bank.numel() == self.n_iter * self.n_angles * self.n_det
         _chk(_lib.lt_set_bank(self._p, bank.data_ptr(), _stream(self.device)), "lt_set_bank")
         self._keep = bank
+
+    # angle-split Alg. 1 (lt_bank_split_*; the all-reduce is the caller's, dist.filter_bank_split)
+    def bank_split_begin(self, a0: int, a1: int) -> None:
+        _chk(_lib.lt_bank_split_begin(self._p, a0, a1, _stream(self.device)), "lt_bank_split_begin")
+
+    def bank_split_step(self, k: int, partial: torch.Tensor = None) -> None:
+        ptr = None
+        if partial is not None:
+            assert partial.is_cuda and partial.dtype == torch.float32 and partial.is_contiguous()
+            assert partial.numel() == self.n * self.n
+            ptr = partial.data_ptr()
+        _chk(_lib.lt_bank_split_step(self._p, k, ptr, _stream(self.device)), "lt_bank_split_step")
+
+    def bank_split_apply(self, reduced: torch.Tensor) -> None:
+        reduced = _cuda_f32(reduced, "reduced")
+        assert reduced.numel() == self.n * self.n
+        _chk(_lib.lt_bank_split_apply(self._p, reduced.data_ptr(), _stream(self.device)), "lt_bank_split_apply")
 
     def get_bank(self) -> torch.Tensor:
         out = self._empty(self.n_iter, self.n_angles, self.n_det)

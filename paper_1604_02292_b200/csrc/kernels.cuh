@@ -99,6 +99,7 @@ struct FpArgs {
     // k_fp_roi2 band split (single ROIs): CTA z marches bands z, z + nsplit, ...
     // and writes raw ray sums to part [z][tile][na][Wwin]; k_fp_join sums them
     float* part; int nsplit;
+    int a_lo, a_hi;         // k_fp_roi2: only angles [a_lo, a_hi) (a_hi <= 0: all; angle-split filter bank)
 };
 
 template <int MODE>
@@ -229,6 +230,12 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
     const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a0 = groups[grp * FP_GA];
+    auto in_range = [&](int a) { return a >= 0 && (f.a_hi <= 0 || (a >= f.a_lo && a < f.a_hi)); };
+    {   // a group with no angle in the requested range has nothing to do
+        bool any = false;
+        for (int q = 0; q < FP_GA; ++q) any |= in_range(groups[grp * FP_GA + q]);
+        if (!any) return;
+    }
     const int col = g.ang[a0].col;
     const TileT ti = t.tile[r];
     const int lv0 = col ? ti.vc0 : ti.vr0, lv1 = col ? ti.vc1 : ti.vr1;
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
         #pragma unroll 1
         for (int j = 0; j < FP_APW; ++j) {
             const int a = groups[grp * FP_GA + warp * FP_APW + j];    // this warp's angle j (-1: idle)
-            if (a < 0) continue;
+            if (!in_range(a)) continue;
             const double A = g.A64[a], B = g.B64[a];
             const double tauc = t.tauc[r * na + a];
             const int d0 = __ldg(t.d0 + r * na + a);
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
     }
     for (int j = 0; j < FP_APW; ++j) {
         const int a = groups[grp * FP_GA + warp * FP_APW + j];
-        if (a < 0) continue;
+        if (!in_range(a)) continue;
         const int d0 = __ldg(t.d0 + r * na + a);
         const float* acc = sacc + (warp * FP_APW + j) * (32 * FP_U);
         if (nsplit > 1) {
@@ -395,6 +402,7 @@ struct BpEpi {
     // [z achunk, (z + 1) achunk) into part (CTA-local layout, no epilogue);
     // stage 2 = the same grid sums the nsa partials in order, then the epilogue
     float* part; int nsa, stage, achunk;
+    int a_lo, a_hi;        // only angles [a_lo, a_hi) (a_hi <= 0: all; angle-split filter bank)
 };
 
 template <int NS, int MODE, int SUB = BP_SUB>
@@ -431,8 +439,9 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     const float dx = (float)lane - (float)hs, dy0 = (float)(wq * BP_PR) - (float)hs;
 
     // angles this CTA gathers (all, or one chunk of an angle-split stage 1; none in stage 2)
-    const int az0 = e.stage == 1 ? (int)blockIdx.z * e.achunk : 0;
-    const int az1 = e.stage == 1 ? min(na, az0 + e.achunk) : na;
+    const int alo = e.a_hi > 0 ? e.a_lo : 0, ahi = e.a_hi > 0 ? min(e.a_hi, na) : na;
+    const int az0 = e.stage == 1 ? alo + (int)blockIdx.z * e.achunk : alo;
+    const int az1 = e.stage == 1 ? min(ahi, az0 + e.achunk) : ahi;
     const bool gather = NS > 0 && e.stage != 2;
     float2 acc[COLS][BP_PR];                      // (left-tap, right-tap) partial sums per pixel
     #pragma unroll
@@ -1539,9 +1548,9 @@ __global__ void k_dwin(int na, int nd, int Wwin, const int* __restrict__ d0, con
 // (mode 1: out = v, aux_out = aux_in + alpha v; mode 2: out = aux_in - v)
 __global__ void k_winsum(int mode, int na, int nd, int Wwin, int ntiles, const int* __restrict__ d0,
                          const float* __restrict__ win, float* __restrict__ out, const float* __restrict__ aux_in,
-                         float* __restrict__ aux_out, float alpha) {
+                         float* __restrict__ aux_out, float alpha, int a_off) {
     extern __shared__ int sd0[];
-    const int a = blockIdx.y;
+    const int a = blockIdx.y + a_off;
     for (int t = threadIdx.x; t < ntiles; t += blockDim.x) sd0[t] = d0[t * na + a];
     __syncthreads();
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1558,6 +1567,16 @@ __global__ void k_winsum(int mode, int na, int nd, int Wwin, int ntiles, const i
         out[o] = acc;
         if (mode == 1) aux_out[o] = fmaf(alpha, acc, aux_in ? aux_in[o] : 0.f);
     }
+}
+
+// angle-split Alg. 1: c <- c - alpha (sum over ranks of W_g^T v_g),
+// on the padded image and its transposed twin
+__global__ void k_alg1_apply(int n, int GTP, const float* __restrict__ red, float alpha, float* c, float* cT) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const float u = alpha * red[(long long)i * n + j];
+    c[(long long)i * GTP + PADL + j] -= u;
+    cT[(long long)j * GTP + PADL + i] -= u;
 }
 
 // window -> full sinogram (zero outside the window)

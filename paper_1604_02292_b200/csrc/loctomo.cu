@@ -79,6 +79,9 @@ struct lt_plan {
     int GT = 0, GTP = 0;          // global tile (whole image)
     int num_sms = 148;            // of the bound device (launch sizing)
     long long bpart_cap = 0;      // floats of the angle-split backprojection partials (small batches)
+    int a_lo = 0, a_hi = 0;       // global projections restricted to angles [a_lo, a_hi) (angle-split bank; 0: all)
+    int split_a0 = 0, split_a1 = 0;   // this rank's angles in the angle-split bank
+    bool split_rows_ready = false;    // all steps of the angle-split bank issued (own rows valid)
     long long fpart_cap = 0;      // floats of the band-split forward-projection partials
     double alpha = 0.0;
     std::vector<double> ang;
@@ -206,7 +209,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
     const bool one = (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
     const int apw = one ? 1 : 2;
     const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
-    FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1};
+    FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1, p.a_lo, p.a_hi};
     ScopedTimer tm(TC_FP, st);
     if (one) {
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
@@ -241,8 +244,10 @@ int global_fp(const lt_plan& p, int mode, const float* img, const float* imgT, f
               float* aux_out, cudaStream_t st) {
     static int direct = -1;
     if (direct < 0) { const char* e = getenv("LT_GFP"); direct = (e && !strcmp(e, "direct")) ? 1 : 0; }
-    if (direct || p.TPg > FP2_P || p.Wg > 32 * FP_U)
+    if (direct || p.TPg > FP2_P || p.Wg > 32 * FP_U) {
+        if (p.a_hi > 0) return fail(LT_ERR_INVALID, "angle-restricted projection needs the tiled global projector");
         return launch_fp(p, mode, p.glob_tiles(), img, imgT, 0, out, 0, aux_in, aux_out, st);
+    }
     const Tiles tt = p.tile_tiles();
     float* stack = p.P<float>(p.off.tstack);
     float* stackT = p.P<float>(p.off.tstackT);
@@ -252,8 +257,9 @@ int global_fp(const lt_plan& p, int mode, const float* img, const float* imgT, f
         p.Tg, p.TPg, tt.tile, img, p.GTP, stack, stackT, ts);
     LT_LAUNCHED();
     if (int rc = launch_fp_roi(p, tt, stack, stackT, ts, win, (long long)p.na * p.Wg, st)) return rc;
-    k_winsum<<<dim3((p.nd + 255) / 256, p.na), 256, p.NTg * sizeof(int), st>>>(
-        mode, p.na, p.nd, p.Wg, p.NTg, tt.d0, win, out, aux_in, aux_out, (float)p.alpha);
+    const int a_off = p.a_hi > 0 ? p.a_lo : 0, a_cnt = p.a_hi > 0 ? p.a_hi - p.a_lo : p.na;
+    k_winsum<<<dim3((p.nd + 255) / 256, a_cnt), 256, p.NTg * sizeof(int), st>>>(
+        mode, p.na, p.nd, p.Wg, p.NTg, tt.d0, win, out, aux_in, aux_out, (float)p.alpha, a_off);
     LT_LAUNCHED();
     return LT_OK;
 }
@@ -281,8 +287,9 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
         const long long ctas = (long long)grid.x * grid.y;
         int nsa = NS > 0 && p.bpart_cap > 0 && ctas <= p.num_sms
                       ? (int)std::min<long long>(8, (2LL * 3 * p.num_sms + ctas - 1) / ctas) : 1;
-        const int achunk = ((p.na + nsa - 1) / nsa + BP_CA - 1) / BP_CA * BP_CA;
-        nsa = (p.na + achunk - 1) / achunk;
+        const int nang = e.a_hi > 0 ? e.a_hi - e.a_lo : p.na;
+        const int achunk = ((nang + nsa - 1) / nsa + BP_CA - 1) / BP_CA * BP_CA;
+        nsa = (nang + achunk - 1) / achunk;
         if (nsa > 1 && (long long)nsa * ctas * 32 * 32 <= p.bpart_cap) {
             BpEpi e1 = e;
             e1.part = p.P<float>(p.off.bpart); e1.nsa = nsa; e1.achunk = achunk;
@@ -1189,6 +1196,63 @@ int lt_filter_bank(lt_plan* p, void* stream) {
     return LT_OK;
 }
 
+// ---- angle-split Alg. 1 (SURVEY §8(e) "cold bank"): rank g owns angles
+// [a0, a1); per step it projects c on its angles (its bank rows) and
+// backprojects them into a partial image; the caller all-reduces the partials
+// (NCCL) and applies the sum.  The bank rows of other ranks are gathered by the
+// caller afterwards (lt_get_bank / lt_set_bank).
+int lt_bank_split_begin(lt_plan* p, int32_t a0, int32_t a1, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (a0 < 0 || a1 <= a0 || a1 > p->na) return fail(LT_ERR_INVALID, "angle range [%d, %d) invalid for %d angles", a0, a1, p->na);
+    cudaStream_t st = (cudaStream_t)stream;
+    float* c = p->P<float>(p->off.gimg);
+    float* cT = p->P<float>(p->off.gimgT);
+    const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(c, 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(cT, 0, gbytes, st));
+    k_impulse<<<1, 32, 0, st>>>(p->n, p->GTP, c, cT);
+    LT_LAUNCHED();
+    p->split_a0 = a0; p->split_a1 = a1;
+    p->bank_ready = false;
+    p->split_rows_ready = false;
+    return LT_OK;
+}
+
+int lt_bank_split_step(lt_plan* p, int32_t k, float* d_partial, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (p->split_a1 <= 0) return fail(LT_ERR_INVALID, "lt_bank_split_begin not called");
+    if (k < 0 || k >= p->n_iter) return fail(LT_ERR_INVALID, "step %d out of range", k);
+    if (k + 1 < p->n_iter && !d_partial) return fail(LT_ERR_INVALID, "null partial image");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long ns = (long long)p->na * p->nd;
+    float* c = p->P<float>(p->off.gimg);
+    float* cT = p->P<float>(p->off.gimgT);
+    float* v = p->P<float>(p->off.gsino);
+    float* bk = p->P<float>(p->off.bank) + k * ns;
+    p->a_lo = p->split_a0; p->a_hi = p->split_a1;
+    int rc = global_fp(*p, 1, c, cT, v, k ? bk - ns : nullptr, bk, st);    // v_g = W_g c, u_k = u_{k-1} + alpha v_g
+    if (!rc && k + 1 < p->n_iter) {                                        // partial = W_g^T v_g
+        BpEpi e = epi0();
+        e.out = d_partial; e.out_pitch = p->n;
+        e.a_lo = p->split_a0; e.a_hi = p->split_a1;
+        const SinoView sv = view_full(v, p->nd);
+        rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(*p, p->glob_tiles(), sv, sv, e, st);
+    }
+    p->a_lo = 0; p->a_hi = 0;
+    if (!rc && k + 1 == p->n_iter) p->split_rows_ready = true;
+    return rc;
+}
+
+int lt_bank_split_apply(lt_plan* p, const float* d_reduced, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (p->split_a1 <= 0) return fail(LT_ERR_INVALID, "lt_bank_split_begin not called");
+    if (!d_reduced) return fail(LT_ERR_INVALID, "null reduced image");
+    k_alg1_apply<<<dim3((p->n + 31) / 32, (p->n + 7) / 8), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+        p->n, p->GTP, d_reduced, (float)p->alpha, p->P<float>(p->off.gimg), p->P<float>(p->off.gimgT));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
 int lt_set_bank(lt_plan* p, const float* d_bank, void* stream) {
     if (int rc = check_plan(p)) return rc;
     if (!d_bank) return fail(LT_ERR_INVALID, "null bank");
@@ -1201,7 +1265,7 @@ int lt_set_bank(lt_plan* p, const float* d_bank, void* stream) {
 
 int lt_get_bank(const lt_plan* p, float* d_bank, void* stream) {
     if (int rc = check_plan(p)) return rc;
-    if (!p->bank_ready) return fail(LT_ERR_INVALID, "bank not computed");
+    if (!p->bank_ready && !p->split_rows_ready) return fail(LT_ERR_INVALID, "bank not computed");
     LT_CUDA(cudaMemcpyAsync(d_bank, p->ws + p->off.bank, (size_t)p->n_iter * p->na * p->nd * sizeof(float),
                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     return LT_OK;

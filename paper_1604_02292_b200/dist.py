@@ -65,6 +65,51 @@ def setup_combine(plan, group=None) -> Tuple[int, np.ndarray]:
     return spr, slot_table(lists, spr)
 
 
+def angle_range(n_angles: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous angle rows [a0, a1) of one rank for the angle-split bank."""
+    return rank * n_angles // world, (rank + 1) * n_angles // world
+
+
+def filter_bank_split(plan, group=None, reduce=None, gather=None) -> None:
+    """Cold filter bank on all ranks by angle split:
+    each rank projects / backprojects its angle rows (lt_bank_split_step), the
+    per-step partial images are all-reduced (NCCL / gloo: the only exchange),
+    the sum is applied in the kernels (lt_bank_split_apply), and finally every
+    rank's bank rows are all-gathered and installed with lt_set_bank.
+    ``reduce(t)`` / ``gather(rows) -> list`` override the collectives (tests)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if reduce is None:
+        reduce = (lambda t: dist.all_reduce(t, group=group)) if world > 1 else (lambda t: None)
+    na, n, nd, nit = plan.n_angles, plan.n, plan.n_det, plan.n_iter
+    a0, a1 = angle_range(na, rank, world)
+    plan.bank_split_begin(a0, a1)
+    part = torch.empty(n * n, dtype=torch.float32, device=plan.device)
+    for k in range(nit):
+        last = k + 1 == nit
+        plan.bank_split_step(k, None if last else part)
+        if not last:
+            reduce(part)
+            plan.bank_split_apply(part)
+    bank = plan.get_bank()
+    mine = bank[:, a0:a1, :].contiguous()
+    if gather is None and world == 1:
+        rows = [mine]
+    elif gather is None:
+        # equal-size slots (the largest share), then each rank's rows cut out
+        sizes = [angle_range(na, g, world) for g in range(world)]
+        cap = max(b - a for a, b in sizes)
+        slot = torch.zeros((nit, cap, nd), dtype=torch.float32, device=plan.device)
+        slot[:, :a1 - a0] = mine
+        slots = [torch.empty_like(slot) for _ in range(world)]
+        dist.all_gather(slots, slot, group=group)
+        rows = [slots[g][:, :b - a] for g, (a, b) in enumerate(sizes)]
+    else:
+        rows = gather(mine)
+    plan.set_bank(torch.cat(rows, dim=1).contiguous())
+
+
 class PeerCombine:
     """Combine over NVLink peer memory (lt_combine_peers): every rank's core
     buffer [slots_per_rank, 2r, 2r] is mapped into every other rank with CUDA

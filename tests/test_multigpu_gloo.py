@@ -99,3 +99,16 @@ def test_slot_table_and_partition_balance():
         t = ltd.slot_table(lists, spr)
         assert sorted(t[t >= 0].tolist()) == list(range(len(cen)))
         assert max(len(l) for l in lists) <= spr
+
+
+@pytest.mark.parametrize("na", [1, 7, 64, 180, 256])
+def test_angle_split_ranges_partition(na):
+    """The angle-split bank's rank ranges are contiguous, disjoint, cover
+    [0, N_theta) and differ in size by at most one."""
+    from paper_1604_02292_b200.dist import angle_range
+    for world in range(1, 9):
+        rs = [angle_range(na, g, world) for g in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == na
+        assert all(rs[g][1] == rs[g + 1][0] for g in range(world - 1))
+        sizes = [b - a for a, b in rs]
+        assert max(sizes) - min(sizes) <= 1
