@@ -115,6 +115,22 @@ int lt_bank_split_begin(lt_plan* plan, int32_t a0, int32_t a1, void* stream);
 int lt_bank_split_step(lt_plan* plan, int32_t k, float* d_partial, void* stream);
 int lt_bank_split_apply(lt_plan* plan, const float* d_reduced, void* stream);
 int lt_set_bank(lt_plan* plan, const float* d_bank, void* stream);
+
+/* Angle-split GLOBAL box-SIRT on G ranks (SURVEY §8(e), P:L382-396 with W split
+ * by angle rows), the same pattern as the split bank:
+ *   lt_global_split_begin: x = 0 in the plan's global image; this rank owns
+ *     angles [a0, a1) (errors: 2 if empty or outside [0, n_angles)).
+ *   lt_global_split_step: r_g = p_g - W_g x on its angles (d_sino: the full
+ *     N_theta x N_d sinogram, device) and d_partial = W_g^T r_g, a row-major
+ *     N x N device image (caller-owned).
+ *   lt_global_split_apply: x <- clamp(x + alpha d_reduced, lo, hi), d_reduced =
+ *     the sum of all ranks' partials (the caller's all-reduce).
+ *   lt_global_split_result: d_img (N x N, device) = x.
+ * Errors: 2 if begin was not called, null pointers, lo > hi. */
+int lt_global_split_begin(lt_plan* plan, int32_t a0, int32_t a1, void* stream);
+int lt_global_split_step(lt_plan* plan, const float* d_sino, float* d_partial, void* stream);
+int lt_global_split_apply(lt_plan* plan, const float* d_reduced, float lo, float hi, void* stream);
+int lt_global_split_result(lt_plan* plan, float* d_img, void* stream);
 int lt_get_bank(const lt_plan* plan, float* d_bank, void* stream);
 
 /* Forward projection.  roi = -1: full grid, d_img N x N -> d_sino N_theta x N_d

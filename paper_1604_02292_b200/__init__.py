@@ -47,6 +47,10 @@ _SIGS = {
     "lt_bank_split_begin": ([_P, _I, _I, _P], _I),
     "lt_bank_split_step": ([_P, _I, _P, _P], _I),
     "lt_bank_split_apply": ([_P, _P, _P], _I),
+    "lt_global_split_begin": ([_P, _I, _I, _P], _I),
+    "lt_global_split_step": ([_P, _P, _P, _P], _I),
+    "lt_global_split_apply": ([_P, _P, _F, _F, _P], _I),
+    "lt_global_split_result": ([_P, _P, _P], _I),
     "lt_get_bank": ([_P, _P, _P], _I),
     "lt_project": ([_P, _I, _P, _P, _P], _I),
     "lt_backproject": ([_P, _I, _P, _P, _P], _I),
@@ -219,6 +223,28 @@ class Plan:
         reduced = _cuda_f32(reduced, "reduced")
         assert reduced.numel() == self.n * self.n
         _chk(_lib.lt_bank_split_apply(self._p, reduced.data_ptr(), _stream(self.device)), "lt_bank_split_apply")
+
+    # angle-split global box-SIRT (lt_global_split_*; dist.global_sirt_split)
+    def global_split_begin(self, a0: int, a1: int) -> None:
+        _chk(_lib.lt_global_split_begin(self._p, a0, a1, _stream(self.device)), "lt_global_split_begin")
+
+    def global_split_step(self, sino: torch.Tensor, partial: torch.Tensor) -> None:
+        sino = _cuda_f32(sino, "sino")
+        assert partial.is_cuda and partial.dtype == torch.float32 and partial.is_contiguous()
+        assert partial.numel() == self.n * self.n
+        _chk(_lib.lt_global_split_step(self._p, sino.data_ptr(), partial.data_ptr(), _stream(self.device)),
+             "lt_global_split_step")
+
+    def global_split_apply(self, reduced: torch.Tensor, lo: float, hi: float) -> None:
+        reduced = _cuda_f32(reduced, "reduced")
+        assert reduced.numel() == self.n * self.n
+        _chk(_lib.lt_global_split_apply(self._p, reduced.data_ptr(), float(lo), float(hi), _stream(self.device)),
+             "lt_global_split_apply")
+
+    def global_split_result(self) -> torch.Tensor:
+        out = self._empty(self.n, self.n)
+        _chk(_lib.lt_global_split_result(self._p, out.data_ptr(), _stream(self.device)), "lt_global_split_result")
+        return out
 
     def get_bank(self) -> torch.Tensor:
         out = self._empty(self.n_iter, self.n_angles, self.n_det)

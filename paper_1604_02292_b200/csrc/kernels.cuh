@@ -1579,6 +1579,17 @@ __global__ void k_alg1_apply(int n, int GTP, const float* __restrict__ red, floa
     cT[(long long)j * GTP + PADL + i] -= u;
 }
 
+// angle-split global box-SIRT: x <- clamp(x + alpha sum_g W_g^T r_g, lo, hi)
+__global__ void k_gsirt_apply(int n, int GTP, const float* __restrict__ red, float alpha, float lo, float hi,
+                              float* x, float* xT) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= n || j >= n) return;
+    const long long o = (long long)i * GTP + PADL + j;
+    const float v = fminf(fmaxf(fmaf(alpha, red[(long long)i * n + j], x[o]), lo), hi);
+    x[o] = v;
+    xT[(long long)j * GTP + PADL + i] = v;
+}
+
 // window -> full sinogram (zero outside the window)
 __global__ void k_scatter_win(int na, int nd, int Wwin, const int* __restrict__ d0,
                               const float* __restrict__ win, float* __restrict__ sino) {

@@ -82,6 +82,7 @@ struct lt_plan {
     int a_lo = 0, a_hi = 0;       // global projections restricted to angles [a_lo, a_hi) (angle-split bank; 0: all)
     int split_a0 = 0, split_a1 = 0;   // this rank's angles in the angle-split bank
     bool split_rows_ready = false;    // all steps of the angle-split bank issued (own rows valid)
+    int gsplit_a0 = 0, gsplit_a1 = 0; // this rank's angles in the angle-split global SIRT
     long long fpart_cap = 0;      // floats of the band-split forward-projection partials
     double alpha = 0.0;
     std::vector<double> ang;
@@ -1447,6 +1448,61 @@ int lt_global_sirt(lt_plan* p, const float* d_sino, int32_t n_iter, float lo, fl
         if (int rc = launch_bp_t<1, BP_GSIRT>(*p, gt, sv, sv, e, st)) return rc;
     }
     k_unpack<<<grid2d(p->n, p->n), dim3(32, 8), 0, st>>>(p->n, p->GTP, x, d_img);
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+// ---- angle-split global box-SIRT ("the same pattern serves
+// GLOBAL-mode solves"): rank g owns angles [a0, a1); per iteration it forms its
+// residual rows r_g = p_g - W_g x and the partial image W_g^T r_g; the caller
+// all-reduces the partials and applies the sum with the box clamp.
+int lt_global_split_begin(lt_plan* p, int32_t a0, int32_t a1, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (a0 < 0 || a1 <= a0 || a1 > p->na) return fail(LT_ERR_INVALID, "angle range [%d, %d) invalid for %d angles", a0, a1, p->na);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t gbytes = (size_t)p->GT * p->GTP * sizeof(float);
+    LT_CUDA(cudaMemsetAsync(p->P<float>(p->off.gimg), 0, gbytes, st));
+    LT_CUDA(cudaMemsetAsync(p->P<float>(p->off.gimgT), 0, gbytes, st));
+    p->gsplit_a0 = a0; p->gsplit_a1 = a1;
+    return LT_OK;
+}
+
+int lt_global_split_step(lt_plan* p, const float* d_sino, float* d_partial, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (p->gsplit_a1 <= 0) return fail(LT_ERR_INVALID, "lt_global_split_begin not called");
+    if (!d_sino || !d_partial) return fail(LT_ERR_INVALID, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    float* x = p->P<float>(p->off.gimg);
+    float* xT = p->P<float>(p->off.gimgT);
+    float* r = p->P<float>(p->off.gsino);
+    p->a_lo = p->gsplit_a0; p->a_hi = p->gsplit_a1;
+    int rc = global_fp(*p, 2, x, xT, r, d_sino, nullptr, st);               // r_g = p_g - W_g x
+    if (!rc) {                                                             // partial = W_g^T r_g
+        BpEpi e = epi0();
+        e.out = d_partial; e.out_pitch = p->n;
+        e.a_lo = p->gsplit_a0; e.a_hi = p->gsplit_a1;
+        const SinoView sv = view_full(r, p->nd);
+        rc = launch_bp_t<1, BP_PLAIN_GLOBAL>(*p, p->glob_tiles(), sv, sv, e, st);
+    }
+    p->a_lo = 0; p->a_hi = 0;
+    return rc;
+}
+
+int lt_global_split_apply(lt_plan* p, const float* d_reduced, float lo, float hi, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (p->gsplit_a1 <= 0) return fail(LT_ERR_INVALID, "lt_global_split_begin not called");
+    if (!d_reduced || !(lo <= hi)) return fail(LT_ERR_INVALID, "bad arguments");
+    k_gsirt_apply<<<grid2d(p->n, p->n), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+        p->n, p->GTP, d_reduced, (float)p->alpha, lo, hi, p->P<float>(p->off.gimg), p->P<float>(p->off.gimgT));
+    LT_LAUNCHED();
+    return LT_OK;
+}
+
+int lt_global_split_result(lt_plan* p, float* d_img, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (p->gsplit_a1 <= 0) return fail(LT_ERR_INVALID, "lt_global_split_begin not called");
+    if (!d_img) return fail(LT_ERR_INVALID, "null pointer");
+    k_unpack<<<grid2d(p->n, p->n), dim3(32, 8), 0, (cudaStream_t)stream>>>(p->n, p->GTP, p->P<float>(p->off.gimg), d_img);
     LT_LAUNCHED();
     return LT_OK;
 }

@@ -110,6 +110,28 @@ def filter_bank_split(plan, group=None, reduce=None, gather=None) -> None:
     plan.set_bank(torch.cat(rows, dim=1).contiguous())
 
 
+def global_sirt_split(plan, sino: torch.Tensor, n_iter: int, lo: float = 0.0, hi: float = float("inf"),
+                      group=None, reduce=None) -> torch.Tensor:
+    """GLOBAL box-SIRT on all ranks by angle split: per iteration
+    each rank forms its residual rows and partial backprojection
+    (lt_global_split_step), the N x N partials are all-reduced, and the clamped
+    update is applied in a kernel (lt_global_split_apply).  Every rank ends with
+    the same image.  ``reduce(t)`` overrides the all-reduce (tests)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if reduce is None:
+        reduce = (lambda t: dist.all_reduce(t, group=group)) if world > 1 else (lambda t: None)
+    a0, a1 = angle_range(plan.n_angles, rank, world)
+    plan.global_split_begin(a0, a1)
+    part = torch.empty(plan.n * plan.n, dtype=torch.float32, device=plan.device)
+    for _ in range(n_iter):
+        plan.global_split_step(sino, part)
+        reduce(part)
+        plan.global_split_apply(part, lo, hi)
+    return plan.global_split_result()
+
+
 class PeerCombine:
     """Combine over NVLink peer memory (lt_combine_peers): every rank's core
     buffer [slots_per_rank, 2r, 2r] is mapped into every other rank with CUDA

@@ -127,3 +127,41 @@ def test_bank_split_two_processes():
     for p in procs: p.join(timeout=60)
     assert set(res) == {0, 1}
     assert max(res.values()) <= 1e-5, res
+
+
+@pytest.mark.parametrize("world,lo,hi", [(2, 0.0, math.inf), (3, -math.inf, math.inf), (4, 0.0, 0.02)])
+def test_global_sirt_split_in_one_process(lt, world, lo, hi):
+    """Angle-split GLOBAL box-SIRT: G plans standing
+    in for the ranks, partials summed by the harness, equals lt_global_sirt."""
+    cfg, inp, ref_plan = _plan(lt)
+    sino = torch.from_numpy(inp.sino).cuda()
+    n_iter = 8
+    ref = ref_plan.global_sirt(sino, n_iter, lo, hi).cpu().numpy()
+    from paper_1604_02292_b200 import dist as ltd
+    plans = [_plan(lt)[2] for _ in range(world)]
+    n = ref_plan.n
+    for g, p in enumerate(plans):
+        p.global_split_begin(*ltd.angle_range(p.n_angles, g, world))
+    parts = [torch.empty(n * n, device="cuda") for _ in range(world)]
+    for _ in range(n_iter):
+        for p, t in zip(plans, parts):
+            p.global_split_step(sino, t)
+        red = torch.stack(parts).sum(0)
+        for p in plans:
+            p.global_split_apply(red, lo, hi)
+    outs = [p.global_split_result().cpu().numpy() for p in plans]
+    for o in outs:
+        assert relerr(o, ref) <= 1e-5
+        assert np.array_equal(o, outs[0])              # every rank holds the same image
+    if lo == 0.0:
+        assert outs[0].min() >= 0.0
+
+
+def test_global_sirt_split_single_rank_helper(lt):
+    """dist.global_sirt_split without a process group (world 1) = lt_global_sirt."""
+    from paper_1604_02292_b200 import dist as ltd
+    cfg, inp, plan = _plan(lt)
+    sino = torch.from_numpy(inp.sino).cuda()
+    a = ltd.global_sirt_split(plan, sino, 5).cpu().numpy()
+    b = plan.global_sirt(sino, 5).cpu().numpy()
+    assert relerr(a, b) <= 1e-6
