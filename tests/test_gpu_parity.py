@@ -153,6 +153,20 @@ def test_fgp_batch(lt, orc, h, w):
         assert relerr(got[q], ref) <= 1e-5, (h, w, q)
 
 
+@pytest.mark.parametrize("cnt", [17, 32])
+def test_fgp_batch_split_tail(lt, orc, cnt):
+    """256-row tiles in batches with a ragged last wave of 8-CTA clusters
+    (17 = 15 + 2, 32 = 2 x 15 + 2 co-resident clusters on B200): the first and
+    last tiles against the oracle."""
+    rng = np.random.default_rng(4000 + cnt)
+    b = rng.random((cnt, 256, 240))
+    lam, nf = 0.05, 30
+    got = cpu(lt.fgp_batch(gpu(b), lam, nf))
+    for q in list(range(3)) + list(range(cnt - 3, cnt)):
+        ref = orc.fgp(b[q].astype(np.float32).astype(np.float64), lam, nf)
+        assert relerr(got[q], ref) <= 1e-5, q
+
+
 def test_fgp_lambda_zero_identity(lt):
     x = torch.rand(2, 30, 30, device="cuda")
     assert torch.equal(lt.fgp_batch(x, 0.0, 10), x)
