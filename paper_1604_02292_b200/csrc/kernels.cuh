@@ -838,17 +838,30 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         }
     };
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)vr0 * A.b_pitch + vc0;
+    // 16-byte loads when the rows are 16-byte aligned and the lane's 8 columns are valid
+    const bool vec_b = ((reinterpret_cast<uintptr_t>(bsrc) | ((uintptr_t)A.b_pitch << 2)) & 15) == 0 && x0 + 8 <= Wv;
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
         float2 bv[4];
+        const float* brow = bsrc + (long long)i * A.b_pitch + x0;
+        if (vec_b && i < Hv) {
+            const float4 u0 = __ldg(reinterpret_cast<const float4*>(brow));
+            const float4 u1 = __ldg(reinterpret_cast<const float4*>(brow) + 1);
+            bv[0] = make_float2(u0.x, u0.y); bv[1] = make_float2(u0.z, u0.w);
+            bv[2] = make_float2(u1.x, u1.y); bv[3] = make_float2(u1.z, u1.w);
+        } else {
+            #pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) {
+                const int x = x0 + 2 * c2;
+                const bool rv = i < Hv;
+                bv[c2] = make_float2((rv && x < Wv) ? __ldg(brow + 2 * c2) : 0.f,
+                                     (rv && x + 1 < Wv) ? __ldg(brow + 2 * c2 + 1) : 0.f);
+            }
+        }
         #pragma unroll
         for (int c2 = 0; c2 < 4; ++c2) {
-            const int x = x0 + 2 * c2;
-            const bool rv = i < Hv;
-            const float bx = (rv && x < Wv) ? __ldg(bsrc + (long long)i * A.b_pitch + x) : 0.f;
-            const float by = (rv && x + 1 < Wv) ? __ldg(bsrc + (long long)i * A.b_pitch + x + 1) : 0.f;
-            if constexpr (!BSM) breg[k][c2] = make_float2(bx, by); else bv[c2] = make_float2(bx, by);
+            if constexpr (!BSM) breg[k][c2] = bv[c2];
             r[k][c2] = f2s(0.5f); s[k][c2] = f2s(0.5f); p[k][c2] = f2s(0.5f); q[k][c2] = f2s(0.5f);
         }
         if constexpr (BSM) row_st(bs + k * FGP2_ROW, lane, bv);
