@@ -152,19 +152,36 @@ class PeerCombine:
             return
         # the IPC handle names the whole cudaMalloc segment of torch's caching
         # allocator: torch reports the storage's offset inside it (_share_cuda_);
-        # add the tensor's offset inside the storage
-        seg_off = int(cores.untyped_storage()._share_cuda_()[3])
-        info = (lt.ipc_handle(cores), seg_off + cores.storage_offset() * cores.element_size())
+        # add the tensor's offset inside the storage.  Every step that can fail
+        # is followed by a collective agreement, so either every rank uses the
+        # peer path or every rank raises (and the caller falls back together).
+        try:
+            seg_off = int(cores.untyped_storage()._share_cuda_()[3])
+            info = (lt.ipc_handle(cores), seg_off + cores.storage_offset() * cores.element_size())
+        except Exception:
+            info = None
         infos: List = [None] * self.world
         dist.all_gather_object(infos, info, group=group)
+        if any(i is None for i in infos):
+            raise RuntimeError("CUDA IPC handle unavailable on some rank")
         self.ptrs = []
-        for g, (h, off) in enumerate(infos):
+        ok = True
+        for g, i in enumerate(infos):
             if g == self.rank:
                 self.ptrs.append(cores.data_ptr())
-            else:
-                p = lt.ipc_open(h)
+                continue
+            try:
+                p = lt.ipc_open(i[0])
                 self._opened.append(p)
-                self.ptrs.append(p + off)
+                self.ptrs.append(p + i[1])
+            except Exception:
+                ok = False
+                break
+        flags: List = [None] * self.world
+        dist.all_gather_object(flags, ok, group=group)
+        if not all(flags):
+            self.close()
+            raise RuntimeError("CUDA IPC mapping failed on some rank")
 
     def combine(self, out: torch.Tensor) -> torch.Tensor:
         import torch.distributed as dist
