@@ -713,10 +713,16 @@ int crop_cores(lt_plan& p, float* d_cores, cudaStream_t st) {
 // Haar momentum, sinogram pointer) and replayed afterwards; every input of the
 // loop lives in the workspace, so a replay sees the new data.  Off under
 // per-kernel timing (the timing events would not repeat) and with two ROI
-// streams; LT_GRAPH=0 disables it.
+// streams; by default only for small batches (see below), LT_GRAPH=1 / 0
+// forces it on / off.
 int run_local(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, const float* d_sino, cudaStream_t st) {
-    static int use = -1;
-    if (use < 0) { const char* e = getenv("LT_GRAPH"); use = !(e && atoi(e) == 0); }
+    static int env = -2;
+    if (env == -2) { const char* e = getenv("LT_GRAPH"); env = e ? atoi(e) : -1; }   // 1 on, 0 off, unset: auto
+    // auto: only launch-bound batches gain from the replay (C1 e2e 502 -> 634,
+    // C2 565 -> 576 solves/s); with more work per iteration the eagerly issued
+    // streams overlap better (C3 614 vs 591, T1 36 vs 34, C4 319 vs 309)
+    const double work = (double)p.R * p.T * p.T * p.na;    // pixel-angle updates of one A over the batch
+    const bool use = env == 1 || (env == -1 && work < 2.5e7);
     if (!use || g_timing || (p.nsplit > 1 && p.R >= 2)) return local_iterations(p, mode, lo, hi, lam, nfgp, d_sino, st);
     if (mode == 1)
         if (int rc = ensure_fgp_beta(nfgp, st)) return rc;   // (synchronous on first use: not inside a capture)

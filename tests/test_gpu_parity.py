@@ -6,6 +6,7 @@ convolution cache <= 1e-5 relative L2 (fp32); filter bank <= 1e-4; full solves
 <= 1e-3 per ROI core and on the stitched image; ROI indexing exact.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -585,3 +586,34 @@ def test_tv_solve_C3_subset(lt, orc):
                        mode="tv", lam=cfg.lam, n_fgp=n_fgp)
     for q in range(len(cen)):
         assert relerr(cores[q], ref[q]) <= 1e-3, q
+
+
+_GRAPH_SCRIPT = r"""
+import sys, math, numpy as np, torch
+sys.path.insert(0, '.')
+import synth, paper_1604_02292_b200 as lt
+cfg = synth.config("C1"); inp = synth.make_inputs("C1")
+plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter)
+plan.filter_bank()
+outs = []
+for k in range(3):                      # capture, then replays with new data
+    sino = torch.from_numpy(inp.sino * (1.0 + 0.1 * k)).float().cuda()
+    outs.append(plan.sirt_solve(sino, 0.0, math.inf).cpu().numpy())
+    outs.append(plan.tv_solve(sino, 0.05, 30).cpu().numpy())
+np.save(sys.argv[1], np.stack(outs))
+"""
+
+
+def test_graph_replay_matches_eager(lt, tmp_path):
+    """The CUDA-graph replay of the local iteration loop (forced on) gives the
+    same bits as eager launches (forced off), including replays with new data."""
+    import subprocess, sys as _sys
+    res = {}
+    for g in ("0", "1"):
+        f = tmp_path / f"g{g}.npy"
+        env = dict(os.environ, LT_GRAPH=g)
+        r = subprocess.run([_sys.executable, "-c", _GRAPH_SCRIPT, str(f)], env=env, capture_output=True, text=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[g] = np.load(f)
+    assert np.array_equal(res["0"], res["1"])
