@@ -218,7 +218,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         // nsplit CTAs per (tile, angle group), joined by k_fp_join in split order
         const long long ctas = (long long)p.ngroups1 * t.ntiles;
         const int nbands = (t.T + FP2_BL - 1) / FP2_BL;
-        int nsplit = ctas <= p.num_sms ? (int)std::min<long long>({8LL, (long long)nbands / 2, (2LL * 3 * p.num_sms + ctas - 1) / ctas}) : 1;
+        int nsplit = ctas <= p.num_sms && p.nsplit <= 1 ? (int)std::min<long long>({8LL, (long long)nbands / 2, (2LL * 3 * p.num_sms + ctas - 1) / ctas}) : 1;
         if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
             f.part = p.P<float>(p.off.fpart); f.nsplit = nsplit;
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles, nsplit), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
@@ -286,7 +286,8 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
         // stage 2: their ordered sum + the epilogue).  Measured: T1 ROI BP 76 ->
         // 36 us; with 2 CTAs per SM already (C2) the extra pass costs more than it gains
         const long long ctas = (long long)grid.x * grid.y;
-        int nsa = NS > 0 && p.bpart_cap > 0 && ctas <= p.num_sms
+        // (one partial buffer per plan: not with two concurrent ROI groups, LT_SPLIT)
+        int nsa = NS > 0 && p.bpart_cap > 0 && p.nsplit <= 1 && ctas <= p.num_sms
                       ? (int)std::min<long long>(8, (2LL * 3 * p.num_sms + ctas - 1) / ctas) : 1;
         const int nang = e.a_hi > 0 ? e.a_hi - e.a_lo : p.na;
         const int achunk = ((nang + nsa - 1) / nsa + BP_CA - 1) / BP_CA * BP_CA;
