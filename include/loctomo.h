@@ -26,6 +26,8 @@
  * (argument violates the contract; detected on the host before any launch,
  * no partial output).  lt_last_error() returns a thread-local message.
  * Results are deterministic: no atomics, fixed summation orders.
+ * A plan keeps the solve state in its workspace: calls on one plan must be
+ * stream-ordered (one stream at a time); different plans are independent.
  */
 #ifndef LOCTOMO_H
 #define LOCTOMO_H
@@ -58,8 +60,8 @@ typedef struct lt_plan lt_plan;
  *      corners); every core must lie inside the grid.
  *  radius (>= 1), margin (>= 0): core half-side r and padding m.
  *  n_iter (>= 1): outer iterations n; the filter bank holds u_1..u_n.
- *  rank, world: this process's share of the ROIs (longest-processing-time
- *      partition over valid-pixel counts); world = 1
+ *  rank, world: this process's share of the ROIs (the ROIs in raster order
+ *      cut into world contiguous runs of balanced cost); world = 1
  *      for a single GPU.
  *  out: receives the plan.  Returns LT_ERR_INVALID on any violation. */
 int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angles,
