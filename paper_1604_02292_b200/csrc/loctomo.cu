@@ -353,7 +353,7 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
 // cluster.  LT_FGP2_CFG = "4x8" (default, 8-CTA clusters for 256-row tiles),
 // "2x8" (16-CTA clusters), "2x8b" (b in shared memory, two CTAs per SM).
 template <int MODE, int FR, int NW, bool BSM = false>
-int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
+int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clusters = nullptr) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
     const size_t smem = (size_t)((BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) +
@@ -374,6 +374,11 @@ int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (max_clusters) {    // query only: how many clusters of this shape are co-resident
+        if (cudaOccupancyMaxActiveClusters(max_clusters, kern, &cfg) != cudaSuccess) *max_clusters = 0;
+        cudaGetLastError();
+        return LT_OK;
+    }
     ScopedTimer tm(TC_FGP, st);
     LT_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     LT_LAUNCHED();
@@ -387,14 +392,30 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     static int cfgv = -1;
     if (cfgv < 0) {
         const char* e = getenv("LT_FGP2_CFG");
-        cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : !strcmp(e, "2x16b") ? 3 : 0;
+        cfgv = !e ? 0 : !strcmp(e, "2x8") ? 1 : !strcmp(e, "2x8b") ? 2 : !strcmp(e, "2x16b") ? 3 : !strcmp(e, "4x8") ? 4 : 0;
     }
-    // small batches: 16-row CTAs (twice the CTAs per tile) while the 32-row
-    // layout would not fill one wave of SMs
-    int nsm = 148;
-    { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
-    const bool small = ntiles * ((rows + 31) / 32) < nsm && rows > 16;
-    if (cfgv == 1 || (cfgv == 0 && small && (rows + 15) / 16 <= 16)) return launch_fgp2_t<MODE, 2, 8>(A, rows, ntiles, st);
+    // 16-row CTAs (twice the CTAs per tile, shorter iteration latency) or
+    // 32-row CTAs (fewer SMs per tile): the shape with fewer waves x wave
+    // latency, from the co-resident cluster counts of both shapes (B200,
+    // 256-row tiles: 7 clusters of 16 / 15 of 8) and the measured single-wave
+    // latencies (52 / 73 us per 100 FGP iterations, tools/fgp_single.py)
+    bool use16 = false;
+    if (cfgv == 0 && rows > 16 && (rows + 15) / 16 <= 16) {
+        static int c2[17] = {}, c4[17] = {};                  // cache by rows / 16
+        const int key = (rows + 15) / 16;
+        if (!c2[key]) {
+            launch_fgp2_t<MODE, 2, 8>(A, rows, 1, st, &c2[key]);
+            launch_fgp2_t<MODE, 4, 8>(A, rows, 1, st, &c4[key]);
+            if (c2[key] <= 0) c2[key] = -1;
+            if (c4[key] <= 0) c4[key] = -1;
+        }
+        if (c2[key] > 0 && c4[key] > 0) {
+            const long long w2 = (ntiles + c2[key] - 1) / c2[key], w4 = (ntiles + c4[key] - 1) / c4[key];
+            use16 = w2 * 52 < w4 * 73;
+        }
+    }
+    if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
+    if (cfgv == 1 || use16) return launch_fgp2_t<MODE, 2, 8>(A, rows, ntiles, st);
     if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, true>(A, rows, ntiles, st);
     if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, true>(A, rows, ntiles, st);
     return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
