@@ -617,3 +617,25 @@ def test_graph_replay_matches_eager(lt, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         res[g] = np.load(f)
     assert np.array_equal(res["0"], res["1"])
+
+
+@pytest.mark.parametrize("n_iter,radius,margin", [(1, 8, 4), (2, 1, 0), (3, 1, 3), (1, 31, 0)])
+def test_degenerate_solves(lt, orc, n_iter, radius, margin):
+    """Edge cases of the method: one outer iteration (x_s^1 only, y^0 = 0), a
+    2x2 core with no margin, a margin wider than the core, a core touching the
+    grid edge; box-SIRT and FISTA-TV against the oracle."""
+    cfg = synth.Config(23, "degenerate", 64, 20, math.pi, 91, "gauss", 0.01, 1, radius, margin, "centre", n_iter,
+                       "tv", 0.05, 10, 3, 0)
+    inp = synth.make_inputs(cfg)
+    cen = np.array([[32, 32], [radius, 64 - radius]], dtype=np.int32)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, radius, margin, n_iter)
+    plan.filter_bank()
+    sino = gpu(inp.sino)
+    box = cpu(plan.sirt_solve(sino, 0.0, math.inf))
+    tv = cpu(plan.tv_solve(sino, cfg.lam, cfg.n_fgp))
+    ref_box = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, radius, margin, n_iter, mode="box")
+    ref_tv = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, radius, margin, n_iter, mode="tv",
+                          lam=cfg.lam, n_fgp=cfg.n_fgp)
+    for q in range(len(cen)):
+        assert relerr(box[q], ref_box[q]) <= 1e-3, ("box", q)
+        assert relerr(tv[q], ref_tv[q]) <= 1e-3, ("tv", q)
