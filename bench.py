@@ -390,6 +390,9 @@ def run_ours(args, cfg):
             traffic = float(tj["dram_bytes_per_launch"]) * (plan.R / float(tj.get("rois_per_launch", plan.R)))
             traffic_src = tj["source"]
         ent["achieved"] = round(ent["achieved"], 3)
+        # the HBM fraction (reported although the path is SM-bound)
+        hbm = float(pk.get("hbm_gbs") or 0.0)
+        ent["hbm_frac"] = round(traffic / (avg_ms / 1e3) / 1e9 / hbm, 4) if traffic and hbm > 0 else None
         ent.update({"kernel": kname, "frac": round(ent["achieved"] / ent["peak"], 4), "traffic": traffic,
                     "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                     "avg_launch_ms": round(avg_ms, 4), "launches": n,
