@@ -199,6 +199,31 @@ int launch_fp(const lt_plan& p, int mode, const Tiles& t, const float* img, cons
     return LT_OK;
 }
 
+// Split factor of a launch with `ctas` CTAs whose work divides into `units`
+// equal parts (bands, angle chunks): the s in [1, smax] minimising rounds x
+// units per CTA, rounds = ceil(ctas s / resident) (ties: the smaller s, less
+// joining).  `resident` = CTAs of the kernel co-resident on the device.
+int best_split(long long ctas, int units, long long resident, int smax) {
+    int best = 1;
+    long long best_cost = LLONG_MAX;
+    for (int sp = 1; sp <= std::max(1, std::min(smax, units)); ++sp) {
+        const long long rounds = (ctas * sp + resident - 1) / std::max(1LL, resident);
+        const long long cost = rounds * ((units + sp - 1) / sp);
+        if (cost < best_cost) { best_cost = cost; best = sp; }
+    }
+    return best;
+}
+
+template <typename Kern>
+long long resident_ctas(const lt_plan& p, Kern kern, int threads, size_t smem) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    return (long long)std::max(1, per_sm) * p.num_sms;
+}
+
 // ROI-batch forward projection (shared-memory staged k_fp_roi2; the
 // single-pass k_fp for tiles wider than its band)
 int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
@@ -218,7 +243,12 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         // nsplit CTAs per (tile, angle group), joined by k_fp_join in split order
         const long long ctas = (long long)p.ngroups1 * t.ntiles;
         const int nbands = (t.T + FP2_BL - 1) / FP2_BL;
-        int nsplit = ctas <= p.num_sms && p.nsplit <= 1 ? (int)std::min<long long>({8LL, (long long)nbands / 2, (2LL * 3 * p.num_sms + ctas - 1) / ctas}) : 1;
+        int nsplit = 1;
+        if (ctas <= p.num_sms && p.nsplit <= 1) {
+            static long long resident = 0;
+            if (!resident) resident = resident_ctas(p, k_fp_roi2<1>, 256, smem2);
+            nsplit = best_split(ctas, nbands, resident, 8);      // T1: 64 CTAs x 6 = one wave of 3 bands
+        }
         if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
             f.part = p.P<float>(p.off.fpart); f.nsplit = nsplit;
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles, nsplit), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
@@ -287,9 +317,13 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
         // 36 us; with 2 CTAs per SM already (C2) the extra pass costs more than it gains
         const long long ctas = (long long)grid.x * grid.y;
         // (one partial buffer per plan: not with two concurrent ROI groups, LT_SPLIT)
-        int nsa = NS > 0 && p.bpart_cap > 0 && p.nsplit <= 1 && ctas <= p.num_sms
-                      ? (int)std::min<long long>(8, (2LL * 3 * p.num_sms + ctas - 1) / ctas) : 1;
         const int nang = e.a_hi > 0 ? e.a_hi - e.a_lo : p.na;
+        int nsa = 1;
+        if (NS > 0 && p.bpart_cap > 0 && p.nsplit <= 1 && ctas <= p.num_sms) {
+            static long long resident = 0;
+            if (!resident) resident = resident_ctas(p, k_bp<NS, MODE, 32>, 256, 0);
+            nsa = best_split(ctas, (nang + BP_CA - 1) / BP_CA, resident, 8);
+        }
         const int achunk = ((nang + nsa - 1) / nsa + BP_CA - 1) / BP_CA * BP_CA;
         nsa = (nang + achunk - 1) / achunk;
         if (nsa > 1 && (long long)nsa * ctas * 32 * 32 <= p.bpart_cap) {
