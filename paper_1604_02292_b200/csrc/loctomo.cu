@@ -244,11 +244,10 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         const long long ctas = (long long)p.ngroups1 * t.ntiles;
         const int nbands = (t.T + FP2_BL - 1) / FP2_BL;
         int nsplit = 1;
-        if (ctas <= p.num_sms && p.nsplit <= 1) {
-            static long long resident = 0;
-            if (!resident) resident = resident_ctas(p, k_fp_roi2<1>, 256, smem2);
+        static long long resident = 0;
+        if (!resident) resident = resident_ctas(p, k_fp_roi2<1>, 256, smem2);
+        if (ctas < resident && p.nsplit <= 1)                    // less than one wave
             nsplit = best_split(ctas, nbands, resident, 8);      // T1: 64 CTAs x 6 = one wave of 3 bands
-        }
         if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
             f.part = p.P<float>(p.off.fpart); f.nsplit = nsplit;
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles, nsplit), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
@@ -1096,8 +1095,8 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     // angle-split BP partials: up to 8 chunks x two waves of 32x32 CTAs (<= 160 SMs x 3)
     p->bpart_cap = 8LL * 2 * 3 * 160 * 32 * 32;
     f.bpart = take((size_t)p->bpart_cap * fs);
-    // band-split FP partials: up to 8 splits x one wave of 8-angle CTAs (<= 160 SMs)
-    p->fpart_cap = 8LL * 160 * 8 * 32 * FP_U;
+    // band-split FP partials: up to 8 splits x one wave of 8-angle CTAs (<= 3 x 160 SMs)
+    p->fpart_cap = 8LL * 3 * 160 * 8 * 32 * FP_U;
     f.fpart = take((size_t)p->fpart_cap * fs);
     f.bank = take((size_t)n_iter * ns * fs); f.conv = take((size_t)n_iter * ns * fs);
     f.pc = take(ns * fs); f.wd = take(ns * fs); f.wdsum = take(n_angles * 8); f.psum = take(n_angles * 8);
