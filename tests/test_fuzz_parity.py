@@ -1,0 +1,75 @@
+"""Seeded random geometries against the fp64 oracle (GPU): grid sizes, angle
+counts and spans, detector counts, ROI radii / margins / positions (clipped or
+not, overlapping or not), iteration counts and priors drawn at random, so the
+launch-shape decisions (split launches, FGP cluster shapes, small-batch
+backprojection, tile widths) are exercised on shapes no config names."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lt():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1604_02292_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def orc():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def relerr(a, b):
+    a = np.asarray(a, dtype=np.float64); b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(24, 321))
+    na = int(rng.integers(3, 97))
+    span = math.pi if rng.random() < 0.7 else 2 * math.pi / 3
+    nd = int(math.ceil(math.sqrt(2) * n)) | 1
+    nd += 2 * int(rng.integers(0, 3))                       # wider detectors too (odd N_d)
+    radius = int(rng.integers(1, max(2, n // 4)))
+    margin = int(rng.integers(0, 33))
+    n_roi = int(rng.integers(1, 6))
+    cen = np.stack([rng.integers(radius, n - radius + 1, size=n_roi),
+                    rng.integers(radius, n - radius + 1, size=n_roi)], axis=1).astype(np.int32)
+    n_iter = int(rng.integers(1, 6))
+    mode = "tv" if rng.random() < 0.5 else "box"
+    cfg = synth.Config(40 + seed, f"fuzz{seed}", n, na, span, nd, "gauss", 0.01, n_roi, radius, margin, "seeded",
+                       n_iter, mode, 0.05, int(rng.integers(5, 31)), 4, 0)
+    return cfg, cen
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_geometry(lt, orc, seed):
+    cfg, cen = _case(seed)
+    inp = synth.make_inputs(cfg)
+    h = cfg.radius + cfg.margin
+    if 2 * h > 256 and cfg.solver == "tv":
+        pytest.skip("FGP tiles are limited to 256 x 256")
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    sino = torch.from_numpy(inp.sino).cuda()
+    if cfg.solver == "tv":
+        got = plan.tv_solve(sino, cfg.lam, cfg.n_fgp).cpu().numpy()
+        ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, cfg.n_iter,
+                           mode="tv", lam=cfg.lam, n_fgp=cfg.n_fgp)
+    else:
+        got = plan.sirt_solve(sino, 0.0, math.inf).cpu().numpy()
+        ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, cfg.n_iter,
+                           mode="box")
+    for q in range(len(cen)):
+        assert relerr(got[q], ref[q]) <= 1e-3, (cfg, q)
