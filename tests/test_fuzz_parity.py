@@ -73,3 +73,33 @@ def test_random_geometry(lt, orc, seed):
                            mode="box")
     for q in range(len(cen)):
         assert relerr(got[q], ref[q]) <= 1e-3, (cfg, q)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_geometry_large_batch(lt, orc, seed):
+    """Many ROIs (60-300) on random geometries: the large-batch launch shapes
+    (16 angles per FP CTA, 64x64 backprojection blocks, 8-CTA FGP clusters)
+    on 8 sampled ROIs against the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.integers(200, 513))
+    na = int(rng.integers(60, 181))
+    nd = int(math.ceil(math.sqrt(2) * n)) | 1
+    radius = int(rng.integers(8, 41))
+    margin = int(rng.integers(0, 49))
+    n_roi = int(rng.integers(60, 301))
+    cen = np.stack([rng.integers(radius, n - radius + 1, size=n_roi),
+                    rng.integers(radius, n - radius + 1, size=n_roi)], axis=1).astype(np.int32)
+    mode = "tv" if seed % 2 == 0 else "box"
+    cfg = synth.Config(80 + seed, f"fuzzL{seed}", n, na, math.pi, nd, "gauss", 0.01, n_roi, radius, margin, "seeded",
+                       int(rng.integers(1, 4)), mode, 0.05, 15, 6, 0)
+    inp = synth.make_inputs(cfg)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
+    plan.filter_bank()
+    sino = torch.from_numpy(inp.sino).cuda()
+    got = (plan.tv_solve(sino, cfg.lam, cfg.n_fgp) if mode == "tv" else plan.sirt_solve(sino, 0.0, math.inf)).cpu().numpy()
+    sample = np.unique(np.concatenate([[0, n_roi - 1], rng.integers(0, n_roi, size=6)]))
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen[sample], cfg.radius, cfg.margin, cfg.n_iter,
+                       mode=mode, lam=cfg.lam, n_fgp=cfg.n_fgp)
+    for k, g in enumerate(sample):
+        q = int(np.nonzero(plan.local_rois == g)[0][0])
+        assert relerr(got[q], ref[k]) <= 1e-3, (cfg, int(g))
