@@ -757,6 +757,9 @@ __device__ __forceinline__ void bar_sync2(int id) { asm volatile("bar.sync %0, 6
 #ifndef FGP_NAMED_BARS
 #define FGP_NAMED_BARS 0          // 1: named-barrier hand-over (measured slower: 1.35 vs 1.26 ms, C4 tiles)
 #endif
+#ifndef FGP_PAIR_SLEFT
+#define FGP_PAIR_SLEFT 0           // 1: paired left-neighbour term (measured: no gain)
+#endif
 #ifndef FGP_HALO_PREFETCH
 #define FGP_HALO_PREFETCH 0       // 1: halo rows loaded at the phase start (255 registers; measured slower: 1.59 ms)
 #endif
@@ -976,6 +979,16 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 t[c2] = f2fma(nl2, f2sub(r[k][c2], rup[c2]), bk[c2]);
                 t[c2] = f2fma(nl2, s[k][c2], t[c2]);
             }
+#if FGP_PAIR_SLEFT
+            // the left neighbours (s_{j-1}, s_j) as an aligned register pair (two
+            // moves) so the last term is one FFMA2 instead of two scalar FFMAs
+            {
+                const float2 l2 = f2s(lam2);
+                z[k][0] = f2fma(l2, make_float2(sl, s[k][0].x), t[0]);
+                #pragma unroll
+                for (int c2 = 1; c2 < 4; ++c2) z[k][c2] = f2fma(l2, make_float2(s[k][c2 - 1].y, s[k][c2].x), t[c2]);
+            }
+#else
             z[k][0].x = fmaf(lam2, sl, t[0].x);
             z[k][0].y = fmaf(lam2, s[k][0].x, t[0].y);
             #pragma unroll
@@ -983,6 +996,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 z[k][c2].x = fmaf(lam2, s[k][c2 - 1].y, t[c2].x);
                 z[k][c2].y = fmaf(lam2, s[k][c2].x, t[c2].y);
             }
+#endif
             if (k == 0) {
                 if (w == 0 && has_up) row_push(rem_rx_z + cb * PS, lane, z[0], rem_bar_z + cb * 8);
                 if (w > 0) row_st_s(my_z_slot + cb * PS, lane, z[0]);
