@@ -306,6 +306,9 @@ __global__ void k_fp_join(Geo g, Tiles t, FpArgs f) {
 // window centre (|.| <= 48 bins).
 // NS = 0: no gather (y = 0 at k = 1), NS = 1: one sinogram.
 // ---------------------------------------------------------------------------
+#ifndef BP_PAIR_WEIGHTS
+#define BP_PAIR_WEIGHTS 0   // 1: FFMA2 + lower clamp (FMNMX) weights (measured slower: BP 1.19 vs 0.96 ms avg)
+#endif
 constexpr int BP_CA = 32;   // angles per staged chunk
 constexpr int BP_SUB = 64;  // default sub-tile side (pixels); 32 for small ROI batches
 
@@ -455,8 +458,17 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
                     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(b1.x), "=f"(b1.y) : "r"(ad1));
                     // hat weights of the left / right bin: sat(K' -/+ gg / c) (FFMA.SAT, full-rate scalar FP32;
                     // an FFMA2 + FMNMX form measured slower: FMNMX runs at half rate on the ALU pipe)
+#if BP_PAIR_WEIGHTS
+                    // (K' - u, K' + u) as one FFMA2, clamped at 0 only (K' + |u| <= 1 exactly)
+                    const float2 icp = make_float2(-A4.w, A4.w), kk2 = make_float2(A4.z, A4.z);
+                    float2 w0 = __ffma2_rn(icp, make_float2(gg.x, gg.x), kk2);
+                    float2 w1 = __ffma2_rn(icp, make_float2(gg.y, gg.y), kk2);
+                    w0 = make_float2(fmaxf(w0.x, 0.f), fmaxf(w0.y, 0.f));
+                    w1 = make_float2(fmaxf(w1.x, 0.f), fmaxf(w1.y, 0.f));
+#else
                     const float2 w0 = make_float2(__saturatef(fmaf(-gg.x, A4.w, A4.z)), __saturatef(fmaf(gg.x, A4.w, A4.z)));
                     const float2 w1 = make_float2(__saturatef(fmaf(-gg.y, A4.w, A4.z)), __saturatef(fmaf(gg.y, A4.w, A4.z)));
+#endif
                     acc[h][p] = __ffma2_rn(w0, b0, acc[h][p]);
                     acc[h][p + 1] = __ffma2_rn(w1, b1, acc[h][p + 1]);
                 }
