@@ -307,7 +307,11 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
     ScopedTimer tm(e.blist ? TC_XS : TC_BP, st);   // block-listed launches: the global x_s backprojection
     static int sub_env = -1;
     if (sub_env < 0) { const char* v = getenv("LT_BP_SUB"); sub_env = v ? atoi(v) : 0; }
-    if (sub_env == 32 || (sub_env != 64 && ctas64 < 2LL * 3 * p.num_sms)) {
+    // 32x32 below two waves of 64x64 CTAs for the block-listed x_s, below one
+    // wave for the ROI backprojection (a C4 shard of 34 ROIs on 8 GPUs: 544
+    // CTAs of 64x64 take 0.18 ms, 2176 of 32x32 0.21 ms)
+    const long long lim32 = (e.blist ? 2LL : 1LL) * 3 * p.num_sms;
+    if (sub_env == 32 || (sub_env != 64 && ctas64 < lim32)) {
         const int nsx32 = (t.T + 31) / 32;
         const dim3 grid(e.blist ? 4 * nblist : nsx32 * nsx32, t.ntiles);
         // at most one CTA per SM (single ROIs: T1, the x_s blocks of one ROI):
