@@ -236,6 +236,9 @@ def run_ours(args, cfg):
         if sweep:
             scores["mse"], scores["ssim"] = lt.metrics(out, truth_cores)
             return
+        combine_step()
+
+    def combine_step():
         if peer is not None:
             peer.combine(image)                            # stitch reading the peers' cores over NVLink
         elif world > 1:
@@ -284,6 +287,23 @@ def run_ours(args, cfg):
     instr_ms = ei0.elapsed_time(ei1)
     ktimes = lt.timing_read()
     lt.timing_enable(False)
+    # the combine (a9 / e) alone, reported separately; part of every step above
+    combine_ms = None
+    if not sweep:
+        if dist:
+            dist.barrier()
+        ec0 = torch.cuda.Event(enable_timing=True)
+        ec1 = torch.cuda.Event(enable_timing=True)
+        ec0.record()
+        for _ in range(5):
+            combine_step()
+        ec1.record()
+        torch.cuda.synchronize()
+        combine_ms = ec0.elapsed_time(ec1) / 5
+        if dist:
+            t = torch.tensor([combine_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            combine_ms = float(t.item())
     clk = clocks.stop()
     if dist:
         t = torch.tensor([elapsed_ms, instr_ms], device="cuda")
@@ -421,6 +441,7 @@ def run_ours(args, cfg):
         "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
         "fgp_gpix_it_s": round(fgp_pi / (ms_per_step / 1e3) / 1e9, 2),
         "bank_ms": round(bank_ms, 2),
+        "combine_ms": None if combine_ms is None else round(combine_ms, 3),
         "bank_mode": ("angle-split (NCCL all-reduce per Alg. 1 step)" if args.bank == "split" and world > 1
                       else "local (every rank computes the whole bank)"),
         "kernels": kshare,
