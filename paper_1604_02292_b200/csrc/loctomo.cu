@@ -100,10 +100,11 @@ struct lt_plan {
     int Tg = 0, TPg = 0, Wg = 0, NTg = 0;
     std::vector<int> fpgroups;    // [ngroups][16] angle indices of one orientation, -1 padded (2 per warp)
     std::vector<int> fpgroups1;   // [ngroups1][8] the same, one angle per warp
+    std::vector<int> fpgroups24;  // [ngroups24][24] the same, 12 warps x 2 angles
     // BP_SUB^2 image blocks that the global x_s^k backprojection must cover: list 0 for
     // all local ROIs, lists 1 and 2 for the two pipelined ROI groups (halves)
     std::vector<int> xsblk[3];
-    int ngroups = 0, ngroups1 = 0;
+    int ngroups = 0, ngroups1 = 0, ngroups24 = 0;
     // workspace
     char* ws = nullptr;
     int64_t ws_bytes = 0;
@@ -137,7 +138,7 @@ struct lt_plan {
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t pev[2] = {nullptr, nullptr}, fev[2] = {nullptr, nullptr};
     struct {
-        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups, fpgroups1, bpart, fpart;
+        size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups, fpgroups1, fpgroups24, bpart, fpart;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
         size_t gimg, gimgT, gsino, gsino2, gplain, gr, gs, gpo, gqo, gz, gxprev;
         size_t y, yT, s, v, xs, xprev;
@@ -224,6 +225,12 @@ long long resident_ctas(const lt_plan& p, Kern kern, int threads, size_t smem) {
     return (long long)std::max(1, per_sm) * p.num_sms;
 }
 
+bool fp_wide() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("LT_FP_WIDE"); v = !(e && atoi(e) == 0); }
+    return v != 0;
+}
+
 // ROI-batch forward projection (shared-memory staged k_fp_roi2; the
 // single-pass k_fp for tiles wider than its band)
 int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
@@ -256,6 +263,11 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         } else {
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
         }
+    } else if (fp_wide() && (long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms) {
+        // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM)
+        const size_t smem3 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
+        LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+        k_fp_roi2<2, 12><<<dim3(p.ngroups24, t.ntiles), 384, smem3, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups24));
     } else {
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
         k_fp_roi2<2><<<dim3(p.ngroups, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups));
@@ -1010,8 +1022,8 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         tile_window(*p, cc - 0.5 * n, 0.5 * n - cr, p->Wwin, &p->d0[(size_t)q * n_angles], &p->tauc[(size_t)q * n_angles]);
     }
     // forward-projection angle groups (16 and 8 angles): one orientation per group
-    for (int ga : {16, 8}) {
-        std::vector<int>& grp = ga == 16 ? p->fpgroups : p->fpgroups1;
+    for (int ga : {16, 8, 24}) {
+        std::vector<int>& grp = ga == 16 ? p->fpgroups : ga == 8 ? p->fpgroups1 : p->fpgroups24;
         for (int o = 0; o < 2; ++o) {
             std::vector<int> cur;
             for (int a = 0; a < n_angles; ++a)
@@ -1027,6 +1039,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     }
     p->ngroups = (int)p->fpgroups.size() / 16;
     p->ngroups1 = (int)p->fpgroups1.size() / 8;
+    p->ngroups24 = (int)p->fpgroups24.size() / 24;
     // x_s block lists: blocks meeting any valid extended rect
     {
         const int nbk = (n + BP_SUB - 1) / BP_SUB;
@@ -1096,6 +1109,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.twin = take((size_t)p->NTg * n_angles * p->Wg * fs);
     f.fpgroups = take(p->fpgroups.size() * 4);
     f.fpgroups1 = take(p->fpgroups1.size() * 4);
+    f.fpgroups24 = take(p->fpgroups24.size() * 4);
     // angle-split BP partials: up to 8 chunks x two waves of 32x32 CTAs (<= 160 SMs x 3)
     p->bpart_cap = 8LL * 2 * 3 * 160 * 32 * 32;
     f.bpart = take((size_t)p->bpart_cap * fs);
@@ -1182,6 +1196,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.tstackT, 0, (size_t)p->NTg * p->Tg * p->TPg * sizeof(float), st));
     LT_CUDA(up(p->off.fpgroups, p->fpgroups.data(), p->fpgroups.size() * 4));
     LT_CUDA(up(p->off.fpgroups1, p->fpgroups1.data(), p->fpgroups1.size() * 4));
+    LT_CUDA(up(p->off.fpgroups24, p->fpgroups24.data(), p->fpgroups24.size() * 4));
     for (int l = 0; l < 3; ++l)
         if (!p->xsblk[l].empty()) LT_CUDA(up(p->off.xsblk[l], p->xsblk[l].data(), p->xsblk[l].size() * 4));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));

@@ -150,9 +150,10 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
     return acc;
 }
 
-template <int FP_APW>
-__global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, const int* __restrict__ groups) {
-    constexpr int FP_GA = 8 * FP_APW;
+template <int FP_APW, int NWARP = 8>
+__global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo g, Tiles t, FpArgs f,
+                                                                            const int* __restrict__ groups) {
+    constexpr int FP_GA = NWARP * FP_APW;       // angles per CTA (they share each staged band)
     extern __shared__ float4 smf4[];
     float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][FP2_P] (S, D), entry 0 = pixel -PADL
     float* sacc = reinterpret_cast<float*>(sd + FP2_BL * FP2_P);  // [FP_GA][32 * FP_U] per-ray accumulators
@@ -172,15 +173,16 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
     const int pv0 = col ? ti.vr0 : ti.vc0, pv1 = col ? ti.vr1 : ti.vc1;
     const double Lc = 0.5 * (T - 1);
     const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
-    for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += 256) sacc[e] = 0.f;
+    for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += NWARP * 32) sacc[e] = 0.f;
 
-    // staging map (no division): thread = (line tid / 16, chunks c4 = tid % 16 + 16 u)
+    // staging map (no division): thread = (line tid / 16, chunks c4 = tid % 16 + 16 u);
+    // threads 256.. of a 12-warp CTA do not stage
     const int q4 = TP / 4;                        // float4 chunks per raw line
     const int sline = threadIdx.x >> 4, sc0 = threadIdx.x & 15;
     float4 raw[FP2_CPT];
     float nxt[FP2_CPT];
     auto fetch = [&](int l0) {                    // raw lines l0.. of the band into registers
-        const bool lok = l0 + sline < T;
+        const bool lok = sline < FP2_BL && l0 + sline < T;
         const float* rp0 = src + (long long)(l0 + sline) * TP;
         #pragma unroll
         for (int u = 0; u < FP2_CPT; ++u) {
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(256, 3) k_fp_roi2(Geo g, Tiles t, FpArgs f, co
         #pragma unroll
         for (int u = 0; u < FP2_CPT; ++u) {
             const int c4 = sc0 + 16 * u;
-            if (c4 < q4) {
+            if (sline < FP2_BL && c4 < q4) {
                 const float4 v = raw[u];
                 float4* dst = reinterpret_cast<float4*>(sd + sline * FP2_P + c4 * 4);
                 dst[0] = make_float4(v.x + v.y, v.y - v.x, v.y + v.z, v.z - v.y);
