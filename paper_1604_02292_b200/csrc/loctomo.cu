@@ -263,8 +263,10 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         } else {
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
         }
-    } else if (fp_wide() && (long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms) {
-        // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM)
+    } else if (fp_wide() && (long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms &&
+               p.ngroups24 * 24 <= p.ngroups * 16) {
+        // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM),
+        // unless the 24-angle groups pad more (C5: 128 angles per orientation = 5 1/3 x 24)
         const size_t smem3 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
         k_fp_roi2<2, 12><<<dim3(p.ngroups24, t.ntiles), 384, smem3, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups24));
