@@ -253,7 +253,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         int nsplit = 1;
         static long long resident = 0;
         if (!resident) resident = resident_ctas(p, k_fp_roi2<1>, 256, smem2);
-        if (ctas < resident && p.nsplit <= 1)                    // less than one wave
+        if (ctas < resident && p.nsplit <= 1 && nbands >= 8)   // less than one wave; tiny tiles (C1: 3 bands) keep one launch
             nsplit = best_split(ctas, nbands, resident, 8);      // T1: 64 CTAs x 6 = one wave of 3 bands
         if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
             f.part = p.P<float>(p.off.fpart); f.nsplit = nsplit;
