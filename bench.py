@@ -405,15 +405,22 @@ def run_ours(args, cfg):
                    "work_per_unit": f"{JOSEPH_FLOPS_PER_UPDATE:g} FP32 flops per pixel-angle update",
                    "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)"}
         traffic, traffic_src = None, None
+        busy = None
         if kname in traffic_all:   # the capture's launches cover all R ROIs; scale to this run's launch size
             tj = traffic_all[kname]
             traffic = float(tj["dram_bytes_per_launch"]) * (plan.R / float(tj.get("rois_per_launch", plan.R)))
             traffic_src = tj["source"]
+            # how busy the binding unit itself is in the same capture (ncu): the
+            # shared-memory / L1 data path for the FP, the FP32 pipe for BP / FGP
+            if all(k_ in tj for k_ in ("issue_pct", "fma_pipe_pct", "l1tex_pct")):
+                busy = {"issue_pct": tj["issue_pct"], "fma_pipe_pct": tj["fma_pipe_pct"],
+                        "l1tex_pct": tj["l1tex_pct"], "source": tj["source"]}
         ent["achieved"] = round(ent["achieved"], 3)
         # the HBM fraction (reported although the path is SM-bound)
         hbm = float(pk.get("hbm_gbs") or 0.0)
         ent["hbm_frac"] = round(traffic / (avg_ms / 1e3) / 1e9 / hbm, 4) if traffic and hbm > 0 else None
         ent.update({"kernel": kname, "frac": round(ent["achieved"] / ent["peak"], 4), "traffic": traffic,
+                    "unit_busy_ncu": busy,
                     "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                     "avg_launch_ms": round(avg_ms, 4), "launches": n,
                     "share_of_step": round(ms / instr_ms, 3)})
