@@ -639,3 +639,18 @@ def test_degenerate_solves(lt, orc, n_iter, radius, margin):
     for q in range(len(cen)):
         assert relerr(box[q], ref_box[q]) <= 1e-3, ("box", q)
         assert relerr(tv[q], ref_tv[q]) <= 1e-3, ("tv", q)
+
+
+def test_determinism_full_size_c4(lt):
+    """Bitwise-identical repeated solves in bench.py's C4 launch configuration
+    (24-angle projector CTAs, 64x64 backprojection blocks, 8-CTA FGP clusters,
+    the side-stream x_s backprojection with its events), TV and box."""
+    cfg = synth.config("C4")
+    inp = synth.make_inputs("C4")
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, 4)
+    plan.filter_bank()
+    sino = gpu(inp.sino)
+    tv = [cpu(plan.tv_solve(sino, cfg.lam, 10)) for _ in range(3)]
+    box = [cpu(plan.sirt_solve(sino, 0.0, math.inf)) for _ in range(2)]
+    assert np.array_equal(tv[0], tv[1]) and np.array_equal(tv[0], tv[2])
+    assert np.array_equal(box[0], box[1])
