@@ -23,6 +23,7 @@ struct FgpArgs {
     const float* xs; float* xprev; long long p_tstride; int T;
     float* y; float* yT; long long y_tstride; int TP;
     float beta_o;
+    int ntiles;             // persistent launch: tiles blockIdx.y, + gridDim.y, ... < ntiles
 };
 
 __device__ __forceinline__ float clip1(float v) { return fminf(1.f, fmaxf(-1.f, v)); }
@@ -107,6 +108,13 @@ __device__ __forceinline__ void row_ld_s(unsigned row, int lane, float2 (&v)[4])
     v[0] = make_float2(a0, a1); v[1] = make_float2(a2, a3);
     v[2] = make_float2(b0, b1); v[3] = make_float2(b2, b3);
 }
+// a lane's 8 consecutive columns of a naturally laid out shared row
+__device__ __forceinline__ void row_ld_nat(const float* p, float2 (&v)[4]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0];
+    const float4 b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
+    v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+}
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -159,7 +167,12 @@ struct Fgp2Smem {
     // MODE 1: [NW][FR][2][256] xprev and x_s rows, fetched with cp.async at
     // kernel start (they are inputs the FGP loop never touches) and read by the epilogue
     static constexpr int xin_floats = NW * FR * 2 * FGP2_ROW;
+    // persistent launch: [NW][FR][256] b of the cluster's next tile (cp.async)
+    static constexpr int bnext_floats = NW * FR * FGP2_ROW;
 };
+__device__ __forceinline__ void mbar_inval(unsigned bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
@@ -173,14 +186,20 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 // BSM: b (read once per iteration) lives in shared memory instead of registers,
 // so the kernel fits 128 registers and two CTAs (two tiles) share an SM: one
 // tile's halo latency is hidden behind the other tile's arithmetic.
-template <int MODE, int FR, int NW, bool BSM>
+// PERSIST: the grid holds only as many clusters as are co-resident; each
+// cluster iterates over the tiles blockIdx.y, + gridDim.y, ... and fetches the
+// next tile's b, x_prev and x_s by cp.async while iterating the current one.
+template <int MODE, int FR, int NW, bool BSM, bool PERSIST = false>
 __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpArgs A) {
+    static_assert(!(PERSIST && BSM), "persistent launch keeps b in registers");
     using SM = Fgp2Smem<FR, NW>;
     extern __shared__ __align__(16) float sm[];
     cg::cluster_group cl = cg::this_cluster();
     const int K = (int)cl.num_blocks();
     const int kr = (int)cl.block_rank();
-    const int tile = blockIdx.y;
+    const int tile_end = PERSIST ? A.ntiles : (int)blockIdx.y + 1;
+    int tcount = 0;
+    for (int tile = blockIdx.y; tile < tile_end; tile += gridDim.y, ++tcount) {
     int vr0 = 0, vc0 = 0, Hv = A.H, Wv = A.W;
     if (A.tiles) {
         const TileT ti = A.tiles[tile];
@@ -195,7 +214,10 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     for (int e = threadIdx.x; e < SM::hp - SM::hr; e += NW * 32)
         sm[SM::hr + e] = SM::hr + e >= SM::hz ? 0.f : 0.5f;   // z halos start at 0, dual halos at the shifted zero 1/2
     if (threadIdx.x == 0) {
-        for (int q_ = 0; q_ < 4; ++q_) mbar_init(smem_u32(bars + q_), 1);
+        for (int q_ = 0; q_ < 4; ++q_) {
+            if (PERSIST && tcount > 0) mbar_inval(smem_u32(bars + q_));   // (every transfer of the last tile landed)
+            mbar_init(smem_u32(bars + q_), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
@@ -212,12 +234,16 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)vr0 * A.b_pitch + vc0;
     // 16-byte loads when the rows are 16-byte aligned and the lane's 8 columns are valid
     const bool vec_b = ((reinterpret_cast<uintptr_t>(bsrc) | ((uintptr_t)A.b_pitch << 2)) & 15) == 0 && x0 + 8 <= Wv;
+    float* bnext = sm + SM::total + 2 * SM::xin_floats + (w * FR) * FGP2_ROW;   // (PERSIST layout)
+    if (PERSIST && tcount > 0) cp_async_commit_wait_all();   // this tile's b, x_prev, x_s (prefetched)
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
         float2 bv[4];
         const float* brow = bsrc + (long long)i * A.b_pitch + x0;
-        if (vec_b && i < Hv) {
+        if (PERSIST && tcount > 0) {
+            row_ld_nat(bnext + k * FGP2_ROW + x0, bv);
+        } else if (vec_b && i < Hv) {
             const float4 u0 = __ldg(reinterpret_cast<const float4*>(brow));
             const float4 u1 = __ldg(reinterpret_cast<const float4*>(brow) + 1);
             bv[0] = make_float2(u0.x, u0.y); bv[1] = make_float2(u0.z, u0.w);
@@ -240,9 +266,10 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     }
     // FISTA state for the epilogue: asynchronous copies into shared memory now,
     // consumed after the FGP loop (each lane reads back only its own columns)
-    float* xin = sm + (BSM ? SM::total_bsm : SM::total) + (w * FR) * 2 * FGP2_ROW;
+    float* xin = sm + (BSM ? SM::total_bsm : SM::total) + (PERSIST ? (tcount & 1) * SM::xin_floats : 0) +
+                 (w * FR) * 2 * FGP2_ROW;
     const bool vec_p = ((vc0 | A.T) & 3) == 0;
-    if constexpr (MODE == 1) {
+    if (MODE == 1 && !(PERSIST && tcount > 0)) {
         #pragma unroll
         for (int k = 0; k < FR; ++k) {
             const int i = i0 + k;
@@ -276,6 +303,57 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     #pragma unroll
     for (int c2 = 0; c2 < 4; ++c2) gq2[c2] = make_float2(gq[2 * c2], gq[2 * c2 + 1]);
     cl.sync();
+    if constexpr (PERSIST) {   // the cluster's next tile: b, x_prev, x_s into shared memory now
+        const int tn = tile + (int)gridDim.y;
+        if (tn < tile_end) {
+            int nvr0 = 0, nvc0 = 0, nHv = A.H, nWv = A.W;
+            if (A.tiles) {
+                const TileT tn_ = A.tiles[tn];
+                nvr0 = tn_.vr0; nvc0 = tn_.vc0; nHv = tn_.vr1 - tn_.vr0; nWv = tn_.vc1 - tn_.vc0;
+            }
+            const float* nb = A.b + (long long)tn * A.b_tstride + (long long)nvr0 * A.b_pitch + nvc0;
+            const bool nvec_b = ((reinterpret_cast<uintptr_t>(nb) | ((uintptr_t)A.b_pitch << 2)) & 15) == 0;
+            float* nxin = sm + SM::total + ((tcount + 1) & 1) * SM::xin_floats + (w * FR) * 2 * FGP2_ROW;
+            const bool nvec_p = ((nvc0 | A.T) & 3) == 0;
+            #pragma unroll
+            for (int k = 0; k < FR; ++k) {
+                const int i = i0 + k;
+                float* db = bnext + k * FGP2_ROW + x0;
+                const float* brow = nb + (long long)i * A.b_pitch + x0;
+                #pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (i < nHv && nvec_b && x0 + 4 * h + 3 < nWv) {
+                        cp_async16(db + 4 * h, brow + 4 * h);
+                    } else {
+                        #pragma unroll
+                        for (int c = 4 * h; c < 4 * h + 4; ++c) {
+                            if (i < nHv && x0 + c < nWv) cp_async4(db + c, brow + c);
+                            else db[c] = 0.f;
+                        }
+                    }
+                }
+                if (MODE == 1 && i < nHv) {
+                    const long long prow = (long long)tn * A.p_tstride + (long long)(nvr0 + i) * A.T + nvc0 + x0;
+                    float* dx = nxin + k * 2 * FGP2_ROW + x0;
+                    #pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (nvec_p && x0 + 4 * h + 3 < nWv) {
+                            cp_async16(dx + 4 * h, A.xprev + prow + 4 * h);
+                            cp_async16(dx + FGP2_ROW + 4 * h, A.xs + prow + 4 * h);
+                        } else {
+                            #pragma unroll
+                            for (int c = 4 * h; c < 4 * h + 4; ++c)
+                                if (x0 + c < nWv) {
+                                    cp_async4(dx + c, A.xprev + prow + c);
+                                    cp_async4(dx + FGP2_ROW + c, A.xs + prow + c);
+                                }
+                        }
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    }
     const unsigned up_rank = has_up ? kr - 1 : kr, dn_rank = has_dn ? kr + 1 : kr;
     constexpr unsigned RB = FGP2_ROW * 4u;             // bytes per staged row
     constexpr unsigned PS = (NW + 1) * RB;             // bytes per parity of hr / hz
@@ -538,7 +616,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         }
     }
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-
+    }   // tile loop
 }
 
 }  // namespace lt

@@ -403,13 +403,15 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
 // k_fgp2 (paired-FP32 layout): NW warps of FR full rows per CTA, K CTAs per
 // cluster.  LT_FGP2_CFG = "4x8" (default, 8-CTA clusters for 256-row tiles),
 // "2x8" (16-CTA clusters), "2x8b" (b in shared memory, two CTAs per SM).
-template <int MODE, int FR, int NW, bool BSM = false>
+template <int MODE, int FR, int NW, bool BSM = false, bool PERSIST = false>
 int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clusters = nullptr) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
-    const size_t smem = (size_t)((BSM ? Fgp2Smem<FR, NW>::total_bsm : Fgp2Smem<FR, NW>::total) +
-                                 (MODE == 1 ? Fgp2Smem<FR, NW>::xin_floats : 0)) * sizeof(float);
-    auto kern = k_fgp2<MODE, FR, NW, BSM>;
+    using SMl = Fgp2Smem<FR, NW>;
+    const size_t smem = PERSIST ? (size_t)(SMl::total + 2 * SMl::xin_floats + SMl::bnext_floats) * sizeof(float)
+                                : (size_t)((BSM ? SMl::total_bsm : SMl::total) +
+                                           (MODE == 1 ? SMl::xin_floats : 0)) * sizeof(float);
+    auto kern = k_fgp2<MODE, FR, NW, BSM, PERSIST>;
     LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg;
@@ -425,10 +427,19 @@ int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clu
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    A.ntiles = ntiles;
     if (max_clusters) {    // query only: how many clusters of this shape are co-resident
         if (cudaOccupancyMaxActiveClusters(max_clusters, kern, &cfg) != cudaSuccess) *max_clusters = 0;
         cudaGetLastError();
         return LT_OK;
+    }
+    if (PERSIST) {   // only the co-resident clusters; each iterates over its tiles
+        static int cmax = 0;
+        if (!cmax) {
+            cfg.gridDim = dim3(K, 1024, 1);
+            if (cudaOccupancyMaxActiveClusters(&cmax, kern, &cfg) != cudaSuccess || cmax <= 0) { cudaGetLastError(); cmax = 1; }
+        }
+        cfg.gridDim = dim3(K, std::min(ntiles, cmax), 1);
     }
     ScopedTimer tm(TC_FGP, st);
     LT_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
@@ -451,6 +462,7 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     // 256-row tiles: 7 clusters of 16 / 15 of 8) and the measured single-wave
     // latencies (52 / 73 us per 100 FGP iterations, tools/fgp_single.py)
     bool use16 = false;
+    int clusters8 = 0;                                        // co-resident 32-row-CTA clusters
     if (cfgv == 0 && rows > 16 && (rows + 15) / 16 <= 16) {
         static int c2[17] = {}, c4[17] = {};                  // cache by rows / 16
         const int key = (rows + 15) / 16;
@@ -460,15 +472,25 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
             if (c2[key] <= 0) c2[key] = -1;
             if (c4[key] <= 0) c4[key] = -1;
         }
+        clusters8 = c4[key];
         if (c2[key] > 0 && c4[key] > 0) {
             const long long w2 = (ntiles + c2[key] - 1) / c2[key], w4 = (ntiles + c4[key] - 1) / c4[key];
             use16 = w2 * 52 < w4 * 73;
         }
     }
     if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
+    static int persist_env = -1;
+    if (persist_env < 0) { const char* e = getenv("LT_FGP_PERSIST"); persist_env = !(e && atoi(e) == 0); }
+    // persistent 8-CTA clusters (default): only the co-resident clusters are
+    // launched and each walks its tiles, prefetching the next tile's b, x_prev
+    // and x_s during the current one; the SMs the clusters cannot use stay free
+    // for the side-stream x_s backprojection for the whole FGP (C4 318 -> 331)
     if (cfgv == 1 || use16) return launch_fgp2_t<MODE, 2, 8>(A, rows, ntiles, st);
     if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, true>(A, rows, ntiles, st);
     if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, true>(A, rows, ntiles, st);
+    // (many waves only: at C3's 64 tiles = 2.8 waves the dynamic wave scheduling does as well)
+    if (persist_env && clusters8 > 0 && ntiles > 3 * clusters8)
+        return launch_fgp2_t<MODE, 4, 8, false, true>(A, rows, ntiles, st);
     return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
 }
 
