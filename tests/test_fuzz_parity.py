@@ -4,6 +4,7 @@ not, overlapping or not), iteration counts and priors drawn at random, so the
 launch-shape decisions (split launches, FGP cluster shapes, small-batch
 backprojection, tile widths) are exercised on shapes no config names."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -53,7 +54,8 @@ def _case(seed):
     return cfg, cen
 
 
-@pytest.mark.parametrize("seed", range(40))
+# LT_FUZZ_SEEDS widens the sweep for one-off stress runs (profiles/r01/fuzz_*.txt)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("LT_FUZZ_SEEDS", "40"))))
 def test_random_geometry(lt, orc, seed):
     cfg, cen = _case(seed)
     inp = synth.make_inputs(cfg)
