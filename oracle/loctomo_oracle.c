@@ -290,12 +290,18 @@ static void fgp(int h, int w, const double* b, double lam, int nit, double* x, d
     double* z = (double*)malloc(sizeof(double) * (size_t)h * w);
     const double g = 1.0 / (8.0 * lam);
     double t = 1.0;
+    /* (rows in parallel only for large images: every element is computed by one
+     * thread from the previous iterate, so the thread count changes nothing) */
+    const int par = (size_t)h * w >= 4096;
     for (int it = 0; it < nit; ++it) {
+#pragma omp parallel for schedule(static) if (par)
         for (int i = 0; i < h; ++i)
             for (int j = 0; j < w; ++j) z[(size_t)i * w + j] = b[(size_t)i * w + j] - lam * Lop(r, s, h, w, i, j);
+#pragma omp parallel for schedule(static) if (par)
         for (int i = 0; i < h - 1; ++i)
             for (int j = 0; j < w; ++j)
                 pn[(size_t)i * w + j] = clip1(r[(size_t)i * w + j] + g * (z[(size_t)i * w + j] - z[(size_t)(i + 1) * w + j]));
+#pragma omp parallel for schedule(static) if (par)
         for (int i = 0; i < h; ++i)
             for (int j = 0; j < w - 1; ++j)
                 qn[(size_t)i * (w - 1) + j] = clip1(s[(size_t)i * (w - 1) + j] + g * (z[(size_t)i * w + j] - z[(size_t)i * w + j + 1]));

@@ -612,3 +612,130 @@ def test_exterior_with_exact_exterior_is_local_sirt_of_the_roi_data(orc):
     for _ in range(10):
         x = x + alpha * M * orc.back(pl - orc.forward(M * x, ang, nd), ang, n)
     assert relerr(cores[0], x[rect[0]:rect[1], rect[2]:rect[3]]) < 1e-12
+
+
+# ------------------------------------------------------------------ eq. localmethod off the grid origin, FISTA beta
+
+def _fista_table():
+    """tests/golden/fista_tk.txt: k, t_k, beta_k (Beck & Teboulle 2009, written by make_fista_tk.py)."""
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "fista_tk.txt")) if l.strip() and not l.startswith("#")]
+    k = np.array([int(r[0]) for r in rows])
+    t = np.array([float(r[1]) for r in rows])
+    b = np.array([float(r[2]) for r in rows])
+    return k, t, b
+
+
+def test_fista_table_is_beck_teboulle():
+    """The golden FISTA sequence has the properties that define it (Beck & Teboulle
+    2009, cited at P:L660; Alg. 3 P:L679-680 corrected per A12): t_1 = 1, t_2 = the
+    golden ratio, t_{k+1}^2 - t_{k+1} = t_k^2 (the quadratic whose root the update
+    takes), t_k >= (k+1)/2 (their Lemma 4.3), beta_1 = 0, 0 < beta_k < 1 increasing."""
+    k, t, b = _fista_table()
+    assert k[0] == 1 and t[0] == 1.0 and b[0] == 0.0
+    assert abs(t[1] - (1.0 + math.sqrt(5.0)) / 2.0) < 1e-15
+    assert np.all(np.abs(t[1:] ** 2 - t[1:] - t[:-1] ** 2) <= 1e-13 * t[1:] ** 2)
+    assert np.all(t >= (k + 1) / 2.0 - 1e-15)
+    assert np.all(np.diff(b) > 0) and np.all(b[1:] > 0) and np.all(b < 1)
+    assert np.all(np.abs(b[:-1] * t[1:] - (t[:-1] - 1.0)) < 1e-13 * t[1:])
+
+
+@pytest.mark.parametrize("mode", ["box", "tv"])
+def test_local_recursion_off_origin_equals_masked_global_operators(orc, mode):
+    """eq. localmethod / Alg. 2 / Alg. 3 on a
+    CLIPPED, OFF-CENTRE extended ROI (rows start at the grid edge, columns at 11,
+    non-square) with noisy data and the disc term, written with the already-pinned
+    global operators and the mask M_{L'} (W_{L'} = W M_{L'}, W_{L'}^T = M_{L'} W^T,
+    P:L250-251, pin P12):
+        x_s^k = M W^T b_k + c M D                              (A7)
+        S     = x_s^k + y - alpha M W^T W M y
+        box:  x = clamp(S), y = x - x_s^k                      (P:L538-546)
+        TV:   x = FGP(S on L'), r = x + beta_k (x - x_prev), y = r - x_s^k
+              with beta_k from the golden Beck-Teboulle table (A12)
+    The oracle's windowless local solve must agree to 1e-12; a swapped row/column
+    offset of the y projection, or a wrong momentum sequence, fails here."""
+    n, nd, ang, p = _small_problem(n=24, na=14, seed=21)
+    nk, lam, nf = 9, 0.03, 25
+    pc, c, _, D = orc.disc(p, ang, n)
+    bank = orc.filter_bank(n, ang, nd, nk)
+    b = orc.conv_cache(bank, pc)
+    cen, r, m = [[5, 18]], 4, 3
+    rect = orc.roi_rects(n, cen, r, m)[0]
+    er0, er1, ec0, ec1 = (int(v) for v in rect[4:8])
+    assert (er0, er1, ec0, ec1) == (0, 12, 11, 24)        # clipped on two sides, off the origin, 12 x 13
+    R = (er0, er1, ec0, ec1)
+    M = np.zeros((n, n)); M[er0:er1, ec0:ec1] = 1.0
+    alpha = orc.alpha_for(len(ang), nd)
+    _, _, beta = _fista_table()
+    y = np.zeros((n, n)); xprev = np.zeros((n, n)); x = np.zeros((n, n))
+    for k in range(nk):
+        xs = orc.back(b[k], ang, n, R) + c * M * D
+        S = xs + y - alpha * orc.back(orc.forward(y, ang, nd, R), ang, n, R)
+        if mode == "box":
+            x = M * np.clip(S, 0.0, np.inf)
+            y = x - xs
+        else:
+            x = np.zeros((n, n))
+            x[er0:er1, ec0:ec1] = orc.fgp(S[er0:er1, ec0:ec1], lam, nf)
+            y = x + beta[k] * (x - xprev) - xs
+            xprev = x
+    cores = orc.local_solve(n, ang, nd, b, cen, r, m, mode=mode, lo=0.0, hi=np.inf, lam=lam, n_fgp=nf,
+                            disc_c=c, use_disc=True)
+    ref = x[rect[0]:rect[1], rect[2]:rect[3]]
+    assert relerr(cores[0], ref) < 1e-12
+    if mode == "box":
+        assert np.min(S) < 0.0                            # the clamp was active
+    assert np.max(np.abs(y * (1 - M))) == 0.0             # y stays inside L' (P:L603-605)
+
+
+def test_fista_momentum_follows_the_golden_sequence(orc):
+    """Alg. 3 with lambda = 0 (FGP = identity), a full-grid ROI and the exact SIRT
+    iterates as x_s is FISTA on 1/2||p - Wx||^2 with step alpha (split
+    exactness P9/P10): x^k = r^{k-1} + alpha W^T (p - W r^{k-1}),
+    r^k = x^k + beta_k (x^k - x^{k-1}), beta_k from tests/golden/fista_tk.txt.
+    Both the local solve and the global FISTA-TV of the oracle must follow it to
+    1e-12 (a beta of (t'-1)/(t'+1), or t_{k} in place of t_{k-1}, fails)."""
+    n, nd, ang, p = _small_problem(n=12, na=10, seed=5)
+    nk = 14
+    alpha = orc.alpha_for(len(ang), nd)
+    _, _, beta = _fista_table()
+    x = np.zeros((n, n)); r_ = np.zeros((n, n))
+    for k in range(nk):
+        xn = r_ + alpha * orc.back(p - orc.forward(r_, ang, nd), ang, n)
+        r_ = xn + beta[k] * (xn - x)
+        x = xn
+    _, xs = orc.global_box(p, ang, n, nk, lo=-np.inf, hi=np.inf, iterates=True)
+    cores = orc.local_solve(n, ang, nd, np.zeros((nk, len(ang), nd)), [[n // 2, n // 2]], n // 2, 0,
+                            mode="tv", lam=0.0, n_fgp=1, xs_exact=xs)
+    assert relerr(cores[0], x) < 1e-12
+    assert relerr(orc.global_tv(p, ang, n, nk, 0.0, 1), x) < 1e-12
+    assert relerr(x, xs[-1]) > 1e-3                       # momentum really changes the iterate
+
+
+def test_fgp_iterates_follow_beck_teboulle(orc):
+    """The FGP (Beck & Teboulle 2009, named at P:L661-663; reading A13) step by
+    step on a ragged 5 x 7 image: dual step 1/(8 lambda), projection onto [-1, 1],
+    momentum beta_k from the golden table, output b - lambda L(p, q); oracle
+    iterates for n_FGP = 1, 2, 3, 7, 20 agree to 1e-12 (the inner momentum is
+    otherwise pinned only by convergence, P11)."""
+    rng = np.random.default_rng(11)
+    bimg = rng.random((5, 7))
+    lam = 0.07
+    _, _, beta = _fista_table()
+    h, w = bimg.shape
+
+    def Lop(P, Q):
+        out = np.zeros((h, w))
+        out[:-1, :] += P; out[1:, :] -= P
+        out[:, :-1] += Q; out[:, 1:] -= Q
+        return out
+
+    for nit in (1, 2, 3, 7, 20):
+        P = np.zeros((h - 1, w)); Q = np.zeros((h, w - 1)); Rr = P.copy(); Ss = Q.copy()
+        for it in range(nit):
+            z = bimg - lam * Lop(Rr, Ss)
+            Pn = np.clip(Rr + (z[:-1, :] - z[1:, :]) / (8 * lam), -1, 1)
+            Qn = np.clip(Ss + (z[:, :-1] - z[:, 1:]) / (8 * lam), -1, 1)
+            Rr = Pn + beta[it] * (Pn - P); Ss = Qn + beta[it] * (Qn - Q)
+            P, Q = Pn, Qn
+        x = bimg - lam * Lop(P, Q)
+        assert relerr(orc.fgp(bimg, lam, nit), x) < 1e-12, nit
