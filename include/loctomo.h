@@ -94,8 +94,6 @@ int lt_plan_tables(const lt_plan* plan, int32_t* h_rects, int32_t* h_d0, int32_t
  * workspace; also caches W D for the disc correction.  Geometry-only. */
 int lt_filter_bank(lt_plan* plan, void* stream);
 
-/* Copy a filter bank [n_iter][N_theta][N_d] fp32 (device) into / out of the
- * plan (per-geometry reuse). */
 /* Angle-split Alg. 1 for a cold bank on G ranks (P:L489-503 with
  * W = [W_0; ...; W_{G-1}] split by angle rows): rank g owns angles [a0, a1).
  *   lt_bank_split_begin: c = e_c (the centred impulse, reading A5) in the plan's
@@ -116,7 +114,26 @@ int lt_filter_bank(lt_plan* plan, void* stream);
 int lt_bank_split_begin(lt_plan* plan, int32_t a0, int32_t a1, void* stream);
 int lt_bank_split_step(lt_plan* plan, int32_t k, float* d_partial, void* stream);
 int lt_bank_split_apply(lt_plan* plan, const float* d_reduced, void* stream);
-int lt_set_bank(lt_plan* plan, const float* d_bank, void* stream);
+
+/* Filter-bank reuse and persistence ("the needed filters ... can be precomputed
+ * for a certain projection geometry").
+ *  lt_bank_key: 64-bit key of what u_k depends on -- N, the angles (bits),
+ *    N_d, alpha, the projector and the impulse rule (readings V2, A5); NOT
+ *    n_iter (u_k does not depend on n).  0 for a null plan.
+ *  lt_set_bank: install a bank [n_iter][N_theta][N_d] fp32 (device, caller-owned,
+ *    copied on `stream`) computed for the geometry with key `key`.  Errors: 2 if
+ *    the key differs from lt_bank_key(plan), null pointers, unbound plan.
+ *  lt_get_bank: copy the plan's bank out (same layout).
+ *  lt_save_bank / lt_load_bank: the bank to / from a file (header: magic
+ *    "LTBANK01", key, N, N_theta, N_d, n_iter, alpha; then fp32 u_1..u_n).  Both
+ *    synchronous on `stream`; save writes `path`.tmp then renames.  load accepts
+ *    a file with n' >= n_iter filters (uses the first n_iter).  Errors: 2 for a
+ *    non-bank file, another geometry (key / sizes / alpha) or too few filters;
+ *    1 for I/O failures. */
+uint64_t lt_bank_key(const lt_plan* plan);
+int lt_set_bank(lt_plan* plan, const float* d_bank, uint64_t key, void* stream);
+int lt_save_bank(const lt_plan* plan, const char* path, void* stream);
+int lt_load_bank(lt_plan* plan, const char* path, void* stream);
 
 /* Angle-split GLOBAL box-SIRT on G ranks (SURVEY §8(e), P:L382-396 with W split
  * by angle rows), the same pattern as the split bank:
@@ -168,15 +185,50 @@ int lt_tv_solve(lt_plan* plan, const float* d_sino, float lambda, int32_t n_fgp,
  * part top-left aligned, zeros elsewhere (for stage-wise parity). */
 int lt_get_ext(const lt_plan* plan, float* d_ext, void* stream);
 
-/* Combine (A19): d_image (N x N) = mean of the cores
- * covering each pixel, in ascending global ROI order, 0 where uncovered.
- * d_cores_all: [n_slots][2r][2r] (e.g. the all-gather of every rank's
- * d_cores); h_slot_roi: host, the global ROI index of each slot (-1 = empty). */
-int lt_combine_rois(const lt_plan* plan, const float* d_cores_all, int32_t n_slots,
+/* Combine ("combined ... by tiling"; A19):
+ * d_image (N x N, device) = the mean of the cores covering each pixel, summed in
+ * ascending global ROI order, 0 where no core covers -- on EVERY rank.
+ *  d_cores: this rank's cores [local_count][2r][2r] (lt_sirt_solve / lt_tv_solve).
+ *  nccl_comm: an ncclComm_t of the plan's `world` ranks with this process at the
+ *    plan's `rank` (lt_nccl_comm_init); may be NULL when world == 1.
+ * For world > 1 the cores go into fixed slots of the largest local count
+ * (lt_plan_slot_table; the partition is the same on every rank, so no table is
+ * exchanged), one in-place ncclAllGather runs on `stream`, then the stitch
+ * kernel: the image is bitwise identical for every world size.  All ranks must
+ * call it (collective).  Errors: 2 null pointers, missing communicator for
+ * world > 1, communicator size / rank different from the plan's; 1 CUDA or
+ * NCCL failures (including NCCL not loadable). */
+int lt_combine_rois(const lt_plan* plan, const float* d_cores, float* d_image, void* nccl_comm, void* stream);
+
+/* NCCL communicator for lt_combine_rois (created with
+ * ncclCommInitRank after the unique id is exchanged, e.g. by
+ * torch.distributed.broadcast of the LT_NCCL_ID_BYTES bytes from rank 0).
+ * lt_nccl_comm_init binds the communicator to the CURRENT device (set it
+ * first).  The library resolves NCCL from libnccl.so.2 at first use. */
+#define LT_NCCL_ID_BYTES 128
+int lt_nccl_get_unique_id(void* h_id);
+int lt_nccl_comm_init(int32_t world, int32_t rank, const void* h_id, void** comm);
+int lt_nccl_comm_destroy(void* comm);
+
+/* The partition's slot table: h_slot_roi[world * spr] = the global ROI index of
+ * rank g's q-th local ROI at g * spr + q (-1 = empty); *h_spr = spr = the
+ * largest local count.  Either pointer may be NULL (query spr first). */
+int lt_plan_slot_table(const lt_plan* plan, int32_t* h_slot_roi, int32_t* h_spr);
+
+/* Stitch already-gathered cores (the stitch step of lt_combine_rois without the
+ * collective, e.g. after the caller's own all-gather): d_image (N x N) = mean of
+ * the cores covering each pixel in ascending global ROI order, 0 where uncovered.
+ * d_cores_all: [n_slots][2r][2r]; h_slot_roi: host, the global ROI index of each
+ * slot (-1 = empty). */
+int lt_stitch_slots(const lt_plan* plan, const float* d_cores_all, int32_t n_slots,
                     const int32_t* h_slot_roi, float* d_image, void* stream);
 
+/* Window width W(h) = 2 ceil((2h-1)/sqrt2) + 4 of an extended half-side h
+ * (V4): the detector bins every ROI window holds per angle. */
+int32_t lt_window_width(int32_t h);
+
 /* Combine over peer memory (the all-gather and the stitch in one
- * kernel): like lt_combine_rois, but slot s of the gathered layout is read in
+ * kernel): like lt_stitch_slots, but slot s of the gathered layout is read in
  * place from rank s / slots_per_rank's core buffer, h_peer_cores[rank]
  * (a host array of `world` <= 64 DEVICE pointers valid in this process: the
  * own buffer and the others' buffers mapped with lt_ipc_open_handle, read over
@@ -184,8 +236,9 @@ int lt_combine_rois(const lt_plan* plan, const float* d_cores_all, int32_t n_slo
  * h_slot_roi: the global ROI of each of the world * slots_per_rank slots
  * (-1 = empty).  The caller orders the peers' solves before this call (e.g. a
  * stream sync + process-group barrier) and this call before the peers
- * overwrite their buffers.  Same image, bitwise, as lt_combine_rois on the
- * all-gathered cores.  Errors (2): null pointers, world outside 1..64. */
+ * overwrite their buffers.  Same image, bitwise, as lt_stitch_slots on the
+ * all-gathered cores (the peer-memory counterpart of lt_combine_rois, used by
+ * bench.py for N > 1).  Errors (2): null pointers, world outside 1..64. */
 int lt_combine_peers(const lt_plan* plan, const float* const* h_peer_cores, int32_t world, int32_t slots_per_rank,
                      const int32_t* h_slot_roi, float* d_image, void* stream);
 

@@ -5,9 +5,12 @@
 #include "kernels.cuh"
 
 #include <cufft.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -47,6 +50,15 @@ int fail(int code, const char* fmt, ...) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int LT_MAX_PEERS = 64;
+constexpr int LT_MAX_DEV = 64;      // per-device caches (occupancy, __constant__ tables) are indexed by ordinal
+
+// the calling thread's current device (every launch goes to it); -1 on error
+int cur_dev() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= LT_MAX_DEV) { cudaGetLastError(); return -1; }
+    return d;
+}
+std::mutex g_dev_mu;                // guards the per-device __constant__ uploads
 
 // ---- optional per-kernel-class timing (CUDA events on the launch stream) ----
 enum { TC_FP = 0, TC_BP = 1, TC_FGP = 2, TC_CONV = 3, TC_XS = 4, TC_N = 5 };
@@ -71,6 +83,45 @@ struct ScopedTimer {
     }
 };
 
+// NCCL (lt_combine_rois): resolved from libnccl.so.2 on first use, so the
+// library loads without it; under PyTorch this is the NCCL torch already loaded
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*commUserRank)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+    static NcclApi a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { a.why = std::string("dlopen libnccl.so.2: ") + dlerror(); return; }
+        a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
+        a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+        a.commCount = (decltype(a.commCount))dlsym(h, "ncclCommCount");
+        a.commUserRank = (decltype(a.commUserRank))dlsym(h, "ncclCommUserRank");
+        a.allGather = (decltype(a.allGather))dlsym(h, "ncclAllGather");
+        a.errStr = (decltype(a.errStr))dlsym(h, "ncclGetErrorString");
+        a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.commCount && a.commUserRank && a.allGather &&
+               a.errStr;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+    });
+    return a;
+}
+
+#define LT_NCCL(call)                                                                     \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess) return fail(LT_ERR_RUNTIME, "%s: %s", #call, nccl_api().errStr(r_)); \
+    } while (0)
+
 }  // namespace
 
 struct lt_plan {
@@ -89,6 +140,10 @@ struct lt_plan {
     std::vector<int> cen;         // [nroi_all][2]
     std::vector<int> local;       // global ROI indices on this rank (ascending)
     int R = 0;
+    // the whole partition (every rank computes the same one): slots_per_rank =
+    // the largest local count; slot_all[g * spr + q] = rank g's q-th ROI (-1 empty)
+    int spr = 1;
+    std::vector<int> slot_all;
     // host tables
     std::vector<AngF> angf;
     std::vector<double> cs64, sn64, A64, B64;
@@ -130,6 +185,9 @@ struct lt_plan {
     cudaStream_t xst = nullptr;
     cudaEvent_t xev_bp = nullptr, xev_xs = nullptr;
     int stitch_cap = 0;           // max list entries
+    // the stitch tables last uploaded to the workspace, keyed by the slot table
+    // (and the peer pointers): repeated combines of the same layout skip the upload
+    mutable std::vector<long long> st_key;
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
     int nsplit = 1;
@@ -147,7 +205,7 @@ struct lt_plan {
         size_t cp_sd, cp_tau, cp_yd, dwin, peers;
         size_t ttiles, td0, ttauc, tstack, tstackT, twin;
         size_t tt, ttT, tw;
-        size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg;
+        size_t st_off, st_lst, st_r0, st_c0, cores, hsino, himg, gather;
         size_t total;
     } off{};
 
@@ -251,8 +309,10 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         const long long ctas = (long long)p.ngroups1 * t.ntiles;
         const int nbands = (t.T + FP2_BL - 1) / FP2_BL;
         int nsplit = 1;
-        static long long resident = 0;
-        if (!resident) resident = resident_ctas(p, k_fp_roi2<1>, 256, smem2);
+        static long long resident_dev[LT_MAX_DEV] = {};
+        const int dv = std::max(0, cur_dev());
+        if (!resident_dev[dv]) resident_dev[dv] = resident_ctas(p, k_fp_roi2<1>, 256, smem2);
+        const long long resident = resident_dev[dv];
         if (ctas < resident && p.nsplit <= 1 && nbands >= 8)   // less than one wave; tiny tiles (C1: 3 bands) keep one launch
             nsplit = best_split(ctas, nbands, resident, 8);      // T1: 64 CTAs x 6 = one wave of 3 bands
         if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
@@ -337,8 +397,10 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
         const int nang = e.a_hi > 0 ? e.a_hi - e.a_lo : p.na;
         int nsa = 1;
         if (NS > 0 && p.bpart_cap > 0 && p.nsplit <= 1 && ctas <= p.num_sms) {
-            static long long resident = 0;
-            if (!resident) resident = resident_ctas(p, k_bp<NS, MODE, 32>, 256, 0);
+            static long long resident_dev[LT_MAX_DEV] = {};
+            const int dv = std::max(0, cur_dev());
+            if (!resident_dev[dv]) resident_dev[dv] = resident_ctas(p, k_bp<NS, MODE, 32>, 256, 0);
+            const long long resident = resident_dev[dv];
             nsa = best_split(ctas, (nang + BP_CA - 1) / BP_CA, resident, 8);
         }
         const int achunk = ((nang + nsa - 1) / nsa + BP_CA - 1) / BP_CA * BP_CA;
@@ -383,11 +445,17 @@ int fgp_check(int rows, int cols) {
     return LT_OK;
 }
 
-// host-computed FGP momentum table in constant memory (uploaded when n_FGP grows)
+// host-computed FGP momentum table (Beck-Teboulle t_k, reading A12) in __constant__
+// memory.  __constant__ symbols exist once PER DEVICE, so the upload is tracked
+// per device ordinal: a second device in the same process gets its own copy.
 int ensure_fgp_beta(int nfgp, cudaStream_t st) {
-    static int have = 0;
+    (void)nfgp;                         // the whole FGP_MAX_IT table is uploaded once per device
+    static uint64_t have_mask = 0;
     static float tab[FGP_MAX_IT];
-    if (nfgp <= have) return LT_OK;
+    const int dv = cur_dev();
+    if (dv < 0) return fail(LT_ERR_RUNTIME, "cudaGetDevice failed or device ordinal >= %d", LT_MAX_DEV);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (have_mask >> dv & 1) return LT_OK;
     double t = 1.0;
     for (int k = 0; k < FGP_MAX_IT; ++k) {
         const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
@@ -396,7 +464,7 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
     }
     LT_CUDA(cudaMemcpyToSymbolAsync(c_fgp_beta, tab, sizeof tab, 0, cudaMemcpyHostToDevice, st));
     LT_CUDA(cudaStreamSynchronize(st));
-    have = FGP_MAX_IT;
+    have_mask |= 1ull << dv;
     return LT_OK;
 }
 
@@ -434,7 +502,9 @@ int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clu
         return LT_OK;
     }
     if (PERSIST) {   // only the co-resident clusters; each iterates over its tiles
-        static int cmax = 0;
+        // (cached per device and cluster size K: the shape changes with the tile rows)
+        static int cmax_dev[LT_MAX_DEV][17] = {};
+        int& cmax = cmax_dev[std::max(0, cur_dev())][K];
         if (!cmax) {
             cfg.gridDim = dim3(K, 1024, 1);
             if (cudaOccupancyMaxActiveClusters(&cmax, kern, &cfg) != cudaSuccess || cmax <= 0) { cudaGetLastError(); cmax = 1; }
@@ -464,7 +534,10 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     bool use16 = false;
     int clusters8 = 0;                                        // co-resident 32-row-CTA clusters
     if (cfgv == 0 && rows > 16 && (rows + 15) / 16 <= 16) {
-        static int c2[17] = {}, c4[17] = {};                  // cache by rows / 16
+        static int c2_dev[LT_MAX_DEV][17] = {}, c4_dev[LT_MAX_DEV][17] = {};   // cache by device and rows / 16
+        const int dv = std::max(0, cur_dev());
+        int* c2 = c2_dev[dv];
+        int* c4 = c4_dev[dv];
         const int key = (rows + 15) / 16;
         if (!c2[key]) {
             launch_fgp2_t<MODE, 2, 8>(A, rows, 1, st, &c2[key]);
@@ -897,23 +970,31 @@ int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot
     }
     if ((int)lst.size() > p.stitch_cap || n_slots > p.nroi_all * std::max(1, p.world))
         return fail(LT_ERR_INVALID, "combine: %zu list entries / %d slots exceed the plan's capacity", lst.size(), n_slots);
-    // tables live in the workspace (stream-ordered upload from pageable host memory)
+    if (h_peers && (world < 1 || world > LT_MAX_PEERS || spr < 1 || (long long)world * spr < n_slots))
+        return fail(LT_ERR_INVALID, "combine_peers: bad world %d / slots per rank %d", world, spr);
+    // tables live in the workspace; uploaded (stream-ordered) only when the slot
+    // layout or the peer pointers differ from the last combine on this plan
     int* d_off = p.P<int>(p.off.st_off);
     int* d_lst = p.P<int>(p.off.st_lst);
     int* d_r0 = p.P<int>(p.off.st_r0);
     int* d_c0 = p.P<int>(p.off.st_c0);
-    LT_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (!lst.empty()) LT_CUDA(cudaMemcpyAsync(d_lst, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    LT_CUDA(cudaMemcpyAsync(d_r0, r0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
-    LT_CUDA(cudaMemcpyAsync(d_c0, c0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
-    const float* const* d_peers = nullptr;
-    if (h_peers) {
-        if (world < 1 || world > LT_MAX_PEERS || spr < 1 || (long long)world * spr < n_slots)
-            return fail(LT_ERR_INVALID, "combine_peers: bad world %d / slots per rank %d", world, spr);
-        const float** tab = p.P<const float*>(p.off.peers);
-        LT_CUDA(cudaMemcpyAsync(tab, h_peers, world * sizeof(float*), cudaMemcpyHostToDevice, st));
-        d_peers = tab;
+    std::vector<long long> key;
+    key.reserve((size_t)n_slots + 3 + (h_peers ? world : 0));
+    key.push_back(n_slots); key.push_back(h_peers ? world : 0); key.push_back(h_peers ? spr : 0);
+    for (int s = 0; s < n_slots; ++s) key.push_back(slot_roi[s]);
+    if (h_peers)
+        for (int g = 0; g < world; ++g) key.push_back((long long)(uintptr_t)h_peers[g]);
+    if (key != p.st_key) {
+        LT_CUDA(cudaMemcpyAsync(d_off, offs.data(), offs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        if (!lst.empty()) LT_CUDA(cudaMemcpyAsync(d_lst, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        LT_CUDA(cudaMemcpyAsync(d_r0, r0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
+        LT_CUDA(cudaMemcpyAsync(d_c0, c0.data(), n_slots * sizeof(int), cudaMemcpyHostToDevice, st));
+        if (h_peers)
+            LT_CUDA(cudaMemcpyAsync(p.P<const float*>(p.off.peers), h_peers, world * sizeof(float*),
+                                    cudaMemcpyHostToDevice, st));
+        p.st_key.swap(key);
     }
+    const float* const* d_peers = h_peers ? p.P<const float*>(p.off.peers) : nullptr;
     k_stitch<<<nb * nb, dim3(32, 8), 0, st>>>(p.n, side, nb, d_off, d_lst, d_r0, d_c0, d_cores, d_image, d_peers, spr);
     LT_LAUNCHED();
     // pageable copies above are staged synchronously by the driver before returning
@@ -1029,6 +1110,15 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     for (int r = 0; r < n_roi; ++r)
         if (owner[r] == rank) p->local.push_back(r);
     p->R = (int)p->local.size();
+    {
+        std::vector<std::vector<int>> per(world);
+        for (int r = 0; r < n_roi; ++r) per[owner[r]].push_back(r);
+        p->spr = 1;
+        for (auto& v : per) p->spr = std::max(p->spr, (int)v.size());
+        p->slot_all.assign((size_t)world * p->spr, -1);
+        for (int g = 0; g < world; ++g)
+            for (size_t q = 0; q < per[g].size(); ++q) p->slot_all[(size_t)g * p->spr + q] = per[g][q];
+    }
     // ROI tiles and windows
     p->tiles.resize(std::max(p->R, 1));
     p->d0.resize((size_t)std::max(p->R, 1) * n_angles);
@@ -1184,6 +1274,7 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     f.st_off = take(((size_t)nb * nb + 1) * 4); f.st_lst = take((size_t)p->stitch_cap * 4);
     f.st_r0 = take((size_t)n_roi * std::max(1, world) * 4 + 4); f.st_c0 = take((size_t)n_roi * std::max(1, world) * 4 + 4);
     f.cores = take(R * side * side * fs); f.hsino = take(ns * fs); f.himg = take(nn * fs);
+    f.gather = take((size_t)world * p->spr * side * side * fs);    // lt_combine_rois all-gather slots
     f.total = o;
     p->ws_bytes = (int64_t)o;
     *out = p;
@@ -1249,6 +1340,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
     }
     p->bound = true;
     p->bank_ready = p->wd_ready = p->spec_ready = false;
+    p->st_key.clear();
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
     return LT_OK;
 }
@@ -1364,11 +1456,97 @@ int lt_bank_split_apply(lt_plan* p, const float* d_reduced, void* stream) {
     return LT_OK;
 }
 
-int lt_set_bank(lt_plan* p, const float* d_bank, void* stream) {
+uint64_t lt_bank_key(const lt_plan* p) {
+    if (!p) return 0;
+    // FNV-1a over what the filters u_k depend on (Alg. 1): the grid N,
+    // the angles (bit patterns), N_d, alpha, the projector (Joseph, V2)
+    // and the impulse rule (reading A5); NOT n_iter: u_k does not depend on n
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* d, size_t len) {
+        const unsigned char* b = (const unsigned char*)d;
+        for (size_t i = 0; i < len; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+    };
+    const char tag[] = "loctomo-bank/joseph-v2/impulse-A5/alpha-1-over-NthetaNd";
+    mix(tag, sizeof tag);
+    mix(&p->n, sizeof p->n); mix(&p->na, sizeof p->na); mix(&p->nd, sizeof p->nd);
+    mix(p->ang.data(), p->ang.size() * sizeof(double));
+    mix(&p->alpha, sizeof p->alpha);
+    return h;
+}
+
+int lt_set_bank(lt_plan* p, const float* d_bank, uint64_t key, void* stream) {
     if (int rc = check_plan(p)) return rc;
     if (!d_bank) return fail(LT_ERR_INVALID, "null bank");
+    if (key != lt_bank_key(p))
+        return fail(LT_ERR_INVALID, "bank key %016llx does not match this plan's geometry (%016llx)",
+                    (unsigned long long)key, (unsigned long long)lt_bank_key(p));
     LT_CUDA(cudaMemcpyAsync(p->ws + p->off.bank, d_bank, (size_t)p->n_iter * p->na * p->nd * sizeof(float),
                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    p->bank_ready = true;
+    p->spec_ready = false;
+    return LT_OK;
+}
+
+// bank file: header (magic, key, n, n_angles, n_det, n_iter, alpha) + fp32 u_1..u_{n_iter}
+namespace {
+struct BankHeader {
+    char magic[8];
+    uint64_t key;
+    int32_t n, na, nd, n_iter;
+    double alpha;
+};
+const char kBankMagic[8] = {'L', 'T', 'B', 'A', 'N', 'K', '0', '1'};
+}  // namespace
+
+int lt_save_bank(const lt_plan* p, const char* path, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!path) return fail(LT_ERR_INVALID, "null path");
+    if (!p->bank_ready) return fail(LT_ERR_INVALID, "bank not computed");
+    const size_t cnt = (size_t)p->n_iter * p->na * p->nd;
+    std::vector<float> host(cnt);
+    LT_CUDA(cudaMemcpyAsync(host.data(), p->ws + p->off.bank, cnt * sizeof(float), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+    LT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    BankHeader hd;
+    memcpy(hd.magic, kBankMagic, 8);
+    hd.key = lt_bank_key(p); hd.n = p->n; hd.na = p->na; hd.nd = p->nd; hd.n_iter = p->n_iter; hd.alpha = p->alpha;
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE* f = fopen(tmp.c_str(), "wb");
+    if (!f) return fail(LT_ERR_RUNTIME, "cannot open %s for writing", tmp.c_str());
+    const bool ok = fwrite(&hd, sizeof hd, 1, f) == 1 && fwrite(host.data(), sizeof(float), cnt, f) == cnt;
+    if (fclose(f) != 0 || !ok) { remove(tmp.c_str()); return fail(LT_ERR_RUNTIME, "write to %s failed", tmp.c_str()); }
+    if (rename(tmp.c_str(), path) != 0) { remove(tmp.c_str()); return fail(LT_ERR_RUNTIME, "rename to %s failed", path); }
+    return LT_OK;
+}
+
+int lt_load_bank(lt_plan* p, const char* path, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!path) return fail(LT_ERR_INVALID, "null path");
+    FILE* f = fopen(path, "rb");
+    if (!f) return fail(LT_ERR_RUNTIME, "cannot open %s", path);
+    BankHeader hd;
+    if (fread(&hd, sizeof hd, 1, f) != 1 || memcmp(hd.magic, kBankMagic, 8) != 0) {
+        fclose(f);
+        return fail(LT_ERR_INVALID, "%s is not a bank file", path);
+    }
+    if (hd.key != lt_bank_key(p) || hd.n != p->n || hd.na != p->na || hd.nd != p->nd || hd.alpha != p->alpha) {
+        fclose(f);
+        return fail(LT_ERR_INVALID, "%s was computed for another geometry (key %016llx, plan %016llx)", path,
+                    (unsigned long long)hd.key, (unsigned long long)lt_bank_key(p));
+    }
+    if (hd.n_iter < p->n_iter) {
+        fclose(f);
+        return fail(LT_ERR_INVALID, "%s holds %d filters, the plan needs %d", path, hd.n_iter, p->n_iter);
+    }
+    // u_k does not depend on n: the first n_iter filters of a longer bank are this plan's
+    const size_t cnt = (size_t)p->n_iter * p->na * p->nd;
+    std::vector<float> host(cnt);
+    const bool ok = fread(host.data(), sizeof(float), cnt, f) == cnt;
+    fclose(f);
+    if (!ok) return fail(LT_ERR_RUNTIME, "%s is truncated", path);
+    LT_CUDA(cudaMemcpyAsync(p->ws + p->off.bank, host.data(), cnt * sizeof(float), cudaMemcpyHostToDevice,
+                            (cudaStream_t)stream));
+    LT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     p->bank_ready = true;
     p->spec_ready = false;
     return LT_OK;
@@ -1481,11 +1659,85 @@ int lt_get_ext(const lt_plan* p, float* d_ext, void* stream) {
     return LT_OK;
 }
 
-int lt_combine_rois(const lt_plan* p, const float* d_cores_all, int32_t n_slots, const int32_t* h_slot_roi,
+int lt_stitch_slots(const lt_plan* p, const float* d_cores_all, int32_t n_slots, const int32_t* h_slot_roi,
                     float* d_image, void* stream) {
     if (int rc = check_plan(p)) return rc;
     if (!d_image || n_slots < 0 || (n_slots > 0 && (!d_cores_all || !h_slot_roi))) return fail(LT_ERR_INVALID, "bad arguments");
     return combine(*p, d_cores_all, n_slots, h_slot_roi, d_image, (cudaStream_t)stream);
+}
+
+int32_t lt_window_width(int32_t h) { return h < 1 ? -1 : window_width(h); }
+
+int lt_plan_slot_table(const lt_plan* p, int32_t* h_slot_roi, int32_t* h_spr) {
+    if (!p) return fail(LT_ERR_INVALID, "null plan");
+    if (h_spr) *h_spr = p->spr;
+    if (h_slot_roi)
+        for (size_t s = 0; s < p->slot_all.size(); ++s) h_slot_roi[s] = p->slot_all[s];
+    return LT_OK;
+}
+
+int lt_nccl_get_unique_id(void* h_id) {
+    if (!h_id) return fail(LT_ERR_INVALID, "null id buffer");
+    NcclApi& a = nccl_api();
+    if (!a.ok) return fail(LT_ERR_RUNTIME, "NCCL unavailable: %s", a.why.c_str());
+    static_assert(sizeof(ncclUniqueId) == LT_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    LT_NCCL(a.getUniqueId(&id));
+    memcpy(h_id, &id, sizeof id);
+    return LT_OK;
+}
+
+int lt_nccl_comm_init(int32_t world, int32_t rank, const void* h_id, void** comm) {
+    if (!h_id || !comm || world < 1 || rank < 0 || rank >= world) return fail(LT_ERR_INVALID, "bad arguments");
+    NcclApi& a = nccl_api();
+    if (!a.ok) return fail(LT_ERR_RUNTIME, "NCCL unavailable: %s", a.why.c_str());
+    ncclUniqueId id;
+    memcpy(&id, h_id, sizeof id);
+    ncclComm_t c = nullptr;
+    LT_NCCL(a.commInitRank(&c, world, id, rank));
+    *comm = c;
+    return LT_OK;
+}
+
+int lt_nccl_comm_destroy(void* comm) {
+    if (!comm) return fail(LT_ERR_INVALID, "null communicator");
+    NcclApi& a = nccl_api();
+    if (!a.ok) return fail(LT_ERR_RUNTIME, "NCCL unavailable: %s", a.why.c_str());
+    LT_NCCL(a.commDestroy((ncclComm_t)comm));
+    return LT_OK;
+}
+
+int lt_combine_rois(const lt_plan* p, const float* d_cores, float* d_image, void* nccl_comm, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!d_image || (p->R > 0 && !d_cores)) return fail(LT_ERR_INVALID, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int side = 2 * p->radius;
+    const long long slot = (long long)side * side;
+    if (p->world == 1) {   // single rank: no collective, the local cores are the whole image's
+        if (nccl_comm) {
+            NcclApi& a = nccl_api();
+            int cnt = 0;
+            if (!a.ok) return fail(LT_ERR_RUNTIME, "NCCL unavailable: %s", a.why.c_str());
+            LT_NCCL(a.commCount((ncclComm_t)nccl_comm, &cnt));
+            if (cnt != 1) return fail(LT_ERR_INVALID, "communicator has %d ranks, the plan 1", cnt);
+        }
+        return combine(*p, d_cores, p->spr, p->slot_all.data(), d_image, st);
+    }
+    if (!nccl_comm) return fail(LT_ERR_INVALID, "plan of %d ranks needs a communicator", p->world);
+    NcclApi& a = nccl_api();
+    if (!a.ok) return fail(LT_ERR_RUNTIME, "NCCL unavailable: %s", a.why.c_str());
+    int cnt = 0, me = -1;
+    LT_NCCL(a.commCount((ncclComm_t)nccl_comm, &cnt));
+    LT_NCCL(a.commUserRank((ncclComm_t)nccl_comm, &me));
+    if (cnt != p->world || me != p->rank)
+        return fail(LT_ERR_INVALID, "communicator rank %d of %d, plan rank %d of %d", me, cnt, p->rank, p->world);
+    // own cores into this rank's slot block, then the in-place all-gather of the
+    // fixed-size blocks (rank-major), then the stitch in ascending ROI order
+    float* gbuf = p->P<float>(p->off.gather);
+    float* mine = gbuf + (long long)p->rank * p->spr * slot;
+    if (p->R > 0) LT_CUDA(cudaMemcpyAsync(mine, d_cores, (size_t)p->R * slot * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    LT_NCCL(a.allGather(mine, gbuf, (size_t)p->spr * slot, ncclFloat, (ncclComm_t)nccl_comm, st));
+    return combine(*p, gbuf, p->world * p->spr, p->slot_all.data(), d_image, st);
 }
 
 int lt_combine_peers(const lt_plan* p, const float* const* h_peer_cores, int32_t world, int32_t slots_per_rank,
@@ -1869,15 +2121,18 @@ int lt_metrics(const float* d_x, const float* d_ref, int32_t count, int32_t h, i
     if (count < 0 || h < 1 || w < 1) return fail(LT_ERR_INVALID, "count >= 0, h, w >= 1 required");
     if (count == 0) return LT_OK;
     if (!d_x || !d_ref || !d_mse || !d_ssim) return fail(LT_ERR_INVALID, "null pointer");
-    static bool have_w = false;
-    if (!have_w) {   // 11 x 11 Gaussian, sigma 1.5, normalised (fp64 on the host)
+    static uint64_t have_w = 0;       // per device: __constant__ memory is per device
+    const int dv = cur_dev();
+    if (dv < 0) return fail(LT_ERR_RUNTIME, "cudaGetDevice failed or device ordinal >= %d", LT_MAX_DEV);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!(have_w >> dv & 1)) {   // 11 x 11 Gaussian, sigma 1.5, normalised (fp64 on the host)
         double wt[121], s = 0.0;
         for (int a = 0; a < 11; ++a)
             for (int b = 0; b < 11; ++b) { wt[a * 11 + b] = std::exp(-((a - 5) * (a - 5) + (b - 5) * (b - 5)) / (2.0 * 1.5 * 1.5)); s += wt[a * 11 + b]; }
         float wf[121];
         for (int e = 0; e < 121; ++e) wf[e] = (float)(wt[e] / s);
         LT_CUDA(cudaMemcpyToSymbol(c_ssim_w, wf, sizeof wf));
-        have_w = true;
+        have_w |= 1ull << dv;
     }
     k_metrics<<<count, 256, 0, (cudaStream_t)stream>>>(h, w, d_x, d_ref, data_range, d_mse, d_ssim);
     LT_LAUNCHED();

@@ -1,8 +1,10 @@
 """Multi-GPU combine plumbing: ROIs are partitioned by
 ``lt_roi_setup(rank, world)``; each rank solves its ROIs, the cores are
 all-gathered into fixed slots (the largest local count of any rank, ROI-index
-ordered within a rank) and every rank stitches the same image with ``lt_combine_rois``
+ordered within a rank) and every rank stitches the same image with ``lt_stitch_slots``
 (ascending global ROI order => bitwise identical for every world size).
+``Plan.combine_rois`` + ``NcclComm`` do the same inside the library
+(lt_combine_rois: its own NCCL communicator and in-place all-gather).
 
 torch.distributed provides the collective (NCCL on GPUs; gloo works for the
 CPU tests of this host logic).  No arithmetic of the method lives here.
@@ -57,12 +59,19 @@ def gather_cores(cores_slots: torch.Tensor, group=None, out: torch.Tensor = None
 
 
 def setup_combine(plan, group=None) -> Tuple[int, np.ndarray]:
-    """(slots_per_rank, slot -> global ROI table) for a plan of this rank."""
+    """(slots_per_rank, slot -> global ROI table) for a plan of this rank: the
+    ranks' local lists are exchanged and must equal the partition the library
+    computed on every rank (lt_plan_slot_table)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     lists = exchange_local_lists(plan.local_rois, group) if world > 1 else [list(plan.local_rois)]
     spr = slots_per_rank(lists)
-    return spr, slot_table(lists, spr)
+    table = slot_table(lists, spr)
+    if getattr(plan, "world", world) == world:
+        spr_lib, table_lib = plan.slot_table()
+        if spr_lib != spr or not np.array_equal(table_lib, table):
+            raise RuntimeError("exchanged ROI lists differ from the library's partition")
+    return spr, table
 
 
 def angle_range(n_angles: int, rank: int, world: int) -> Tuple[int, int]:
@@ -107,7 +116,7 @@ def filter_bank_split(plan, group=None, reduce=None, gather=None) -> None:
         rows = [slots[g][:, :b - a] for g, (a, b) in enumerate(sizes)]
     else:
         rows = gather(mine)
-    plan.set_bank(torch.cat(rows, dim=1).contiguous())
+    plan.set_bank(torch.cat(rows, dim=1).contiguous(), key=plan.bank_key)
 
 
 def global_sirt_split(plan, sino: torch.Tensor, n_iter: int, lo: float = 0.0, hi: float = float("inf"),

@@ -176,3 +176,55 @@ def test_nelder_mead_validation(lt):
         lt.nelder_mead_1d(lambda t: t, 1.0, 1.0, 10)
     with pytest.raises(ValueError):
         lt.nelder_mead_1d(lambda t: t, 0.0, 1.0, 2)
+
+
+def test_bank_key_depends_on_geometry_only(lt):
+    """lt_bank_key: what Alg. 1's filters depend on (N, angles, N_d, alpha;
+    P:L489-503) changes the key; n_iter, the ROI list, radius and margin do not
+    (u_k does not depend on n or on the ROIs)."""
+    ang = synth.angles_for(16)
+    key = lambda **kw: lt.Plan(kw.get("n", 64), kw.get("ang", ang), kw.get("nd", 91), kw.get("cen", [[32, 32]]),
+                               kw.get("r", 12), kw.get("m", 8), kw.get("nit", 5), bind=False).bank_key
+    k0 = key()
+    assert k0 != 0
+    assert key(nit=50) == k0 and key(cen=[[20, 20], [40, 40]], r=8, m=2) == k0
+    assert key(n=65) != k0 and key(nd=93) != k0 and key(ang=synth.angles_for(17)) != k0
+    a2 = ang.copy(); a2[3] = np.nextafter(a2[3], 10.0)
+    assert key(ang=a2) != k0
+
+
+def test_unbound_plan_rejects_bank_calls(lt):
+    plan = lt.Plan(64, synth.angles_for(8), 91, [[32, 32]], 12, 8, 5, bind=False)
+    assert lt._lib.lt_set_bank(plan._p, None, plan.bank_key, None) == 2
+    assert lt._lib.lt_save_bank(plan._p, b"/tmp/x.bank", None) == 2
+    assert lt._lib.lt_load_bank(plan._p, b"/tmp/x.bank", None) == 2
+    assert lt._lib.lt_combine_rois(plan._p, None, None, None, None) == 2
+    assert lt.window_width(64) == 184 and lt.window_width(1) == 6        # 2 ceil((2h-1)/sqrt2) + 4
+    assert lt._lib.lt_window_width(0) == -1
+
+
+def test_output_buffer_checks_host_side():
+    import paper_1604_02292_b200 as m
+    import torch
+    with pytest.raises(TypeError):
+        m._out_f32(torch.empty(2, 2), (2, 2), torch.device("cuda", 0))     # host tensor
+    with pytest.raises(TypeError):
+        m._cuda_f32(torch.empty(2, 2, dtype=torch.float64), "x")
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_library_slot_table_matches_partition(lt, world):
+    """lt_plan_slot_table = the per-rank local lists of the partition, padded to
+    the largest count (the layout lt_combine_rois all-gathers)."""
+    c = synth.config("C4")
+    cen = synth.roi_centres(c)
+    ang = synth.angles_for(c.n_angles, c.span)
+    plans = [lt.Plan(c.n, ang, c.n_det, cen, c.radius, c.margin, 1, rank=g, world=world, bind=False)
+             for g in range(world)]
+    spr = max(p.R for p in plans)
+    for p in plans:
+        s, tab = p.slot_table()
+        assert s == spr and tab.shape == (world * spr,)
+        for g, q in enumerate(plans):
+            blk = tab[g * spr:(g + 1) * spr]
+            assert np.array_equal(blk[:q.R], q.local_rois) and np.all(blk[q.R:] == -1)
