@@ -11,8 +11,11 @@ timed region ("subsequent applications"); its time is
 reported as bank_ms.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
-Multi-GPU: launched by torchrun, one rank per GPU; ROIs are partitioned
-across ranks (strong scaling of one image), timing = max over ranks.
+Multi-GPU: one rank per GPU, either launched by torchrun (WORLD_SIZE set) or,
+for `--gpus N` without WORLD_SIZE, by this script itself (it re-executes
+under torch.distributed.run with N local ranks and rendezvous at 127.0.0.1);
+ROIs are partitioned across ranks (strong scaling of one image), timing = max
+over ranks, one JSON line from rank 0.
 """
 from __future__ import annotations
 
@@ -20,6 +23,8 @@ import argparse
 import json
 import math
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -56,7 +61,38 @@ def parse():
                          "partial image per Alg. 1 step, all-gather of the bank rows); reported as bank_ms")
     ap.add_argument("--xs-exact", action="store_true",
                     help="NEXT-4(i): x_s^k from the global SIRT iterate instead of the filtered backprojection")
+    ap.add_argument("--selftest", action="store_true",
+                    help="launcher self-test (no GPU): every rank joins a gloo group, rank 0 prints the world size")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`--gpus N` without WORLD_SIZE: run this script under torch.distributed.run
+    with N local ranks (one per GPU), rendezvous at 127.0.0.1; rank 0 prints
+    the JSON line, the launcher returns the ranks' exit status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1)))))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def selftest():
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    t = torch.tensor([float(rank)])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "rank_sum": float(t.item()),
+                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
+    dist.destroy_process_group()
 
 
 def peaks():
@@ -66,6 +102,20 @@ def peaks():
         return d, "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+MICRO_PEAKS = os.path.join("profiles", "r02", "peaks_micro.json")
+
+
+def sm_peaks():
+    """Measured SM-side ceilings (tools/peaks_micro.cu run on a B200, committed
+    under profiles/): shared-memory crossbar bytes/s of a conflict-free LDS.64
+    stream and FP32 FMA flops/s, over all SMs.  None when not measured."""
+    try:
+        with open(os.path.join(ROOT, MICRO_PEAKS)) as f:
+            return json.load(f)
+    except Exception:
+        return None
 
 
 # --------------------------------------------------------------------------- clocks
@@ -120,6 +170,23 @@ def algorithmic_counts(cfg, plan_rects, n_iter):
     updates = cfg.n_angles * Ptot * (1 + 3 * (n_iter - 1))
     fgp_px_it = Ptot * n_iter * cfg.n_fgp if "tv" in cfg.solver else 0.0
     return updates, fgp_px_it, Ptot
+
+
+def executed_updates(cfg, plan_rects, n_iter, block=64):
+    """Pixel-angle updates the kernels actually execute in one step: per
+    iteration 2..n one W_{L'} y and one W_{L'}^T s per ROI (valid pixels), and
+    per iteration 1..n ONE global x_s backprojection over the 64 x 64 image
+    blocks the extended ROIs meet (shared by overlapping ROIs)."""
+    P = float(sum((r[3] - r[2]) * (r[5] - r[4]) for r in plan_rects))
+    nb = (cfg.n + block - 1) // block
+    need = np.zeros((nb, nb), dtype=bool)
+    for row0, col0, vr0, vr1, vc0, vc1 in plan_rects:
+        r0, r1, c0, c1 = row0 + vr0, row0 + vr1, col0 + vc0, col0 + vc1
+        need[r0 // block:(r1 - 1) // block + 1, c0 // block:(c1 - 1) // block + 1] = True
+    xs_pix = 0.0
+    for by, bx in zip(*np.nonzero(need)):
+        xs_pix += (min(cfg.n, (by + 1) * block) - by * block) * (min(cfg.n, (bx + 1) * block) - bx * block)
+    return cfg.n_angles * (2.0 * P * (n_iter - 1) + xs_pix * n_iter)
 
 
 # FP32 operations per unit, DESIGN.md §Roofline (counted from the formulas, not the SASS)
@@ -348,12 +415,13 @@ def run_ours(args, cfg):
 
     # global counts
     upd_local, fgp_local, Ptot_local = algorithmic_counts(cfg, rects, n_iter)
+    exe_local = executed_updates(cfg, rects, n_iter) if not args.xs_exact and mode in ("tv", "sirt", "haar") else None
     if dist:
-        t = torch.tensor([upd_local, fgp_local], device="cuda", dtype=torch.float64)
+        t = torch.tensor([upd_local, fgp_local, exe_local or 0.0], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
-        upd, fgp_pi = float(t[0]), float(t[1])
+        upd, fgp_pi, exe = float(t[0]), float(t[1]), (float(t[2]) if exe_local is not None else None)
     else:
-        upd, fgp_pi = upd_local, fgp_local
+        upd, fgp_pi, exe = upd_local, fgp_local, exe_local
     ms_per_step = elapsed_ms / args.steps
     value = cfg.n_roi / (ms_per_step / 1e3)
     if rank != 0:
@@ -363,8 +431,20 @@ def run_ours(args, cfg):
 
     pk, pk_src = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    alu_peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # FP32 lanes x FMA, DESIGN.md §Roofline
-    smem_peak_gbs = 148 * 128 * sm_max * 1e6 / 1e9            # shared-memory crossbar, 128 B/clk/SM
+    alu_derived = 148 * 128 * 2 * sm_max * 1e6 / 1e12          # FP32 lanes x FMA, DESIGN.md §Roofline
+    smem_derived = 148 * 128 * sm_max * 1e6 / 1e9              # shared-memory crossbar, 128 B/clk/SM
+    mp = sm_peaks()
+    if mp:
+        alu_peak_tflops = max(float(mp["ffma_tflops"]), float(mp["ffma2_tflops"]))
+        smem_peak_gbs = float(mp["smem_lds64_gbs"])
+        alu_src = (f"measured: FP32 FMA stream over all SMs, {MICRO_PEAKS} (tools/peaks_micro.cu); "
+                   f"derived 148 x 128 lanes x 2 x {sm_max:.0f} MHz = {alu_derived:.1f}")
+        smem_src = (f"measured: conflict-free LDS.64 stream over all SMs, {MICRO_PEAKS} (tools/peaks_micro.cu); "
+                    f"derived 148 x 128 B/clk x {sm_max:.0f} MHz = {smem_derived:.0f}")
+    else:
+        alu_peak_tflops, smem_peak_gbs = alu_derived, smem_derived
+        alu_src = f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)"
+        smem_src = f"derived: 148 SM x 128 B/clk shared-memory crossbar x {sm_max:.0f} MHz ({pk_src} clock)"
     nA = cfg.n_angles * Ptot_local          # pixel-angle updates of one A or A^T over all local ROIs
     # Joseph ray-line steps of one W_{L'} over all local ROIs: per angle c_a P
     # (a line of w valid pixels is crossed by c_a w rays, c_a = max(|cos|, |sin|))
@@ -391,19 +471,19 @@ def run_ours(args, cfg):
             ent = {"bound": "alu", "peak": round(alu_peak_tflops, 1), "unit": "TFLOP/s",
                    "achieved": work / (avg_ms / 1e3) / 1e12,
                    "work_per_unit": f"{FGP_FLOPS_PER_PX_IT:g} FP32 flops per pixel-iteration",
-                   "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)"}
+                   "peak_source": alu_src}
         elif cls == "fp":        # one W_{L'} y per iteration 2..n; one (S, D) pair (8 B) per ray-line step
             work = FP_SMEM_BYTES_PER_STEP * fp_steps * (n_iter - 1) * args.steps / n
             ent = {"bound": "smem", "peak": round(smem_peak_gbs, 1), "unit": "GB/s",
                    "achieved": work / (avg_ms / 1e3) / 1e9,
                    "work_per_unit": f"{FP_SMEM_BYTES_PER_STEP:g} B of staged (S, D) pairs per Joseph ray-line step",
-                   "peak_source": f"derived: 148 SM x 128 B/clk shared-memory crossbar x {sm_max:.0f} MHz ({pk_src} clock)"}
+                   "peak_source": smem_src}
         else:                    # W_{L'}^T s of iterations 2..n (iteration 1 has s = 0: no gather)
             work = JOSEPH_FLOPS_PER_UPDATE * nA * (n_iter - 1) * args.steps / n
             ent = {"bound": "alu", "peak": round(alu_peak_tflops, 1), "unit": "TFLOP/s",
                    "achieved": work / (avg_ms / 1e3) / 1e12,
                    "work_per_unit": f"{JOSEPH_FLOPS_PER_UPDATE:g} FP32 flops per pixel-angle update",
-                   "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({pk_src} clock)"}
+                   "peak_source": alu_src}
         traffic, traffic_src = None, None
         busy = None
         if kname in traffic_all:   # the capture's launches cover all R ROIs; scale to this run's launch size
@@ -446,6 +526,9 @@ def run_ours(args, cfg):
         "combine": ("peer-memory stitch (CUDA IPC over NVLink, one kernel)" if peer is not None else
                     "NCCL all-gather + stitch" if world > 1 else "local stitch"),
         "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
+        "gray_s_note": "method-defined count: N_theta P (1 + 3 (n-1)) per ROI; gray_s_executed counts what the "
+                       "kernels execute (x_s once per 64x64 image block per iteration, shared by overlapping ROIs)",
+        "gray_s_executed": None if exe is None else round(exe / (ms_per_step / 1e3) / 1e9, 2),
         "fgp_gpix_it_s": round(fgp_pi / (ms_per_step / 1e3) / 1e9, 2),
         "bank_ms": round(bank_ms, 2),
         "combine_ms": None if combine_ms is None else round(combine_ms, 3),
@@ -473,10 +556,24 @@ def run_ours(args, cfg):
 
 
 # --------------------------------------------------------------------------- oracle (CPU)
-def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None, mode=None):
+def cpu_model() -> str:
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def oracle_sample(cfg, n_iter_sample=2, n_conv_k=1, n_rois=16, mode=None):
     """Time the fp64 oracle on a bounded sample of the same workload and
-    extrapolate to the full step: disc (whole) + conv cache (n_conv_k of n
-    filters, scaled) + one ROI for n_iter_sample of n iterations (scaled, x R)."""
+    extrapolate to the full step: disc (whole) + conv cache
+    (n_conv_k of the n filters, x n / n_conv_k) + a seeded sample of n_rois ROIs
+    for iterations 1..n_iter_sample, extrapolated linearly to n iterations and
+    to all ROIs by valid extended-pixel count (the oracle's per-ROI cost is
+    proportional to it).  Iteration 1 has y = 0 (its projection of y is
+    skipped by the oracle's zero test), so the extrapolation favours the oracle."""
     import oracle
     inp = synth.make_inputs(cfg)
     p = inp.sino.astype(np.float64)
@@ -489,26 +586,33 @@ def oracle_sample(cfg, n_iter_sample=4, n_conv_k=1, roi_index=None, mode=None):
     t0 = time.perf_counter()
     oracle.conv_cache(fake_bank, pc)
     t_conv = (time.perf_counter() - t0) * cfg.n_iter / n_conv_k
-    g = cfg.n_roi // 2 + cfg.n_roi // 32 if roi_index is None else roi_index
+    R = cfg.n_roi
+    pick = np.sort(synth.seeded_rng(cfg.cfg_id, 3).choice(R, size=min(n_rois, R), replace=False))
+    rects = oracle.roi_rects(n, inp.centres, cfg.radius, cfg.margin)
+    valid = (rects[:, 5] - rects[:, 4]).astype(np.float64) * (rects[:, 7] - rects[:, 6])
     bconv = rng.standard_normal((n_iter_sample, cfg.n_angles, cfg.n_det)) * 1e-3
     mode = {"sirt": "box", "tv": "tv", "haar": "haar", "exterior": "box",
             None: "tv" if "tv" in cfg.solver else "box"}[mode]
     t0 = time.perf_counter()
-    oracle.local_solve(n, inp.angles, cfg.n_det, bconv, inp.centres[g:g + 1], cfg.radius, cfg.margin, mode=mode,
+    oracle.local_solve(n, inp.angles, cfg.n_det, bconv, inp.centres[pick], cfg.radius, cfg.margin, mode=mode,
                        lam=HAAR_LAM if mode == "haar" else cfg.lam, n_fgp=cfg.n_fgp, disc_c=c, use_disc=True,
                        levels=HAAR_LEVELS)
-    t_roi = (time.perf_counter() - t0) * cfg.n_iter / n_iter_sample
-    total = t_disc + t_conv + t_roi * cfg.n_roi
-    sample = (f"disc (full) + conv cache {n_conv_k}/{cfg.n_iter} filters (x{cfg.n_iter / n_conv_k:g}) + ROI #{g} "
-              f"{n_iter_sample}/{cfg.n_iter} iterations (x{cfg.n_iter / n_iter_sample:g}, x{cfg.n_roi} ROIs); "
-              f"measured {t_disc:.2f}+{t_conv * n_conv_k / cfg.n_iter:.2f}+{t_roi * n_iter_sample / cfg.n_iter:.2f} s")
-    return cfg.n_roi / total, sample, oracle.get_threads()
+    t_rois = time.perf_counter() - t0
+    scale_iter = cfg.n_iter / n_iter_sample
+    scale_pix = float(valid.sum() / valid[pick].sum())
+    total = t_disc + t_conv + t_rois * scale_iter * scale_pix
+    sample = (f"disc (full) + conv cache {n_conv_k}/{cfg.n_iter} filters (x{cfg.n_iter / n_conv_k:g}) + "
+              f"{len(pick)} seeded ROIs {pick.tolist()[:16]} x iterations 1-{n_iter_sample} of {cfg.n_iter} "
+              f"(x{scale_iter:g} iterations, x{scale_pix:.2f} by valid extended pixels for all {R} ROIs); "
+              f"measured {t_disc:.2f}+{t_conv * n_conv_k / cfg.n_iter:.2f}+{t_rois:.2f} s")
+    return R / total, sample, oracle.get_threads()
 
 
 def cpu_baseline(cfg, budget_s=20.0, mode=None):
     try:
         v, sample, cores = oracle_sample(cfg, mode=mode)
-        return {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        return {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                "nproc": os.cpu_count(), "cpu_model": cpu_model()}
     except Exception as e:  # report, never fake
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
 
@@ -519,12 +623,12 @@ def run_reference(args, cfg):
         return None
     import oracle
     for _ in range(args.warmup):
-        oracle_sample(cfg, n_iter_sample=2, n_conv_k=1, mode=solve_mode(cfg, args))
+        oracle_sample(cfg, mode=solve_mode(cfg, args))
     vals = []
     t0 = time.perf_counter()
     sample = ""
     for _ in range(args.steps):
-        v, sample, cores = oracle_sample(cfg, n_iter_sample=2, n_conv_k=1, mode=solve_mode(cfg, args))
+        v, sample, cores = oracle_sample(cfg, mode=solve_mode(cfg, args))
         vals.append(v)
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
@@ -534,7 +638,7 @@ def run_reference(args, cfg):
             "config": dict(config_dict(cfg, args, 1),
                            reference="fp64 CPU oracle (the paper has no code), extrapolated from a bounded sample"),
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "nproc": os.cpu_count(), "cpu_model": cpu_model()},
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": round(wall, 1)}
     print(json.dumps(line), flush=True)
@@ -543,6 +647,11 @@ def run_reference(args, cfg):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if args.selftest:
+        selftest()
+        return
     cfg = synth.config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)

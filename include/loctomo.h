@@ -49,6 +49,8 @@ extern "C" {
                         * ROI covering the grid reproduces the global solve, pins P9/P10); the
                         * SIRT iterate is advanced once per iteration on the full grid (shared by
                         * all ROIs), no filter bank, conv cache or disc is used */
+#define LT_GUARD_BANDS 4 /* debug: a canary band after every workspace region (more workspace),
+                          * checked by lt_guard_check -- detects out-of-bounds device writes */
 
 typedef struct lt_plan lt_plan;
 
@@ -222,6 +224,13 @@ int lt_plan_slot_table(const lt_plan* plan, int32_t* h_slot_roi, int32_t* h_spr)
  * slot (-1 = empty). */
 int lt_stitch_slots(const lt_plan* plan, const float* d_cores_all, int32_t n_slots,
                     const int32_t* h_slot_roi, float* d_image, void* stream);
+
+/* LT_GUARD_BANDS plans only: synchronizes `stream`, then compares every canary
+ * band with its fill pattern: *h_damaged = the number of damaged bands (0 =
+ * every band intact), *h_bad_offset (nullable) = the workspace byte offset of
+ * the first damaged byte (-1 if none).  Errors: 2 for a plan without guard
+ * bands, unbound or a null h_damaged; 1 on a CUDA error. */
+int lt_guard_check(const lt_plan* plan, int32_t* h_damaged, int64_t* h_bad_offset, void* stream);
 
 /* Window width W(h) = 2 ceil((2h-1)/sqrt2) + 4 of an extended half-side h
  * (V4): the detector bins every ROI window holds per angle. */

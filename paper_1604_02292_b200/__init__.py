@@ -29,6 +29,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 LT_OK, LT_ERR_RUNTIME, LT_ERR_INVALID = 0, 1, 2
 LT_DISC_ON = 1
 LT_XS_EXACT = 2
+LT_GUARD_BANDS = 4
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int32
@@ -71,6 +72,7 @@ _SIGS = {
     "lt_nccl_comm_init": ([_I, _I, _P, _P], _I),
     "lt_nccl_comm_destroy": ([_P], _I),
     "lt_window_width": ([_I], _I),
+    "lt_guard_check": ([_P, _P, _P, _P], _I),
     "lt_solve_host": ([_P, _I, _P, _F, _F, _I, _P, _P], _I),
     "lt_global_sirt": ([_P, _P, _I, _F, _F, _P, _P], _I),
     "lt_global_tv": ([_P, _P, _I, _F, _I, _P, _P], _I),
@@ -180,7 +182,7 @@ class Plan:
 
     def __init__(self, n: int, angles, n_det: int, centres, radius: int, margin: int, n_iter: int,
                  disc: bool = True, rank: int = 0, world: int = 1, device=None, bind: bool = True,
-                 xs_exact: bool = False):
+                 xs_exact: bool = False, guard_bands: bool = False):
         """bind=False plans on the host only (tables, partition); no device memory.
         xs_exact: x_s^k from the global SIRT iterate (LT_XS_EXACT, NEXT-4(i))."""
         if bind:
@@ -198,7 +200,8 @@ class Plan:
         self._p = ctypes.c_void_p()
         _chk(_lib.lt_roi_setup(self.n, len(ang), self.n_det, ang.ctypes.data, len(cen), rows.ctypes.data,
                                cols.ctypes.data, self.radius, self.margin, self.n_iter,
-                               (LT_DISC_ON if disc else 0) | (LT_XS_EXACT if xs_exact else 0), rank, world,
+                               (LT_DISC_ON if disc else 0) | (LT_XS_EXACT if xs_exact else 0)
+                               | (LT_GUARD_BANDS if guard_bands else 0), rank, world,
                                ctypes.byref(self._p)), "lt_roi_setup")
         self.workspace_bytes = nbytes = int(_lib.lt_plan_workspace_bytes(self._p))
         if bind:
@@ -255,6 +258,15 @@ class Plan:
     def bank_key(self) -> int:
         """64-bit key of the geometry the filters depend on (lt_bank_key)."""
         return int(_lib.lt_bank_key(self._p))
+
+    def guard_check(self):
+        """(damaged canary bands, first damaged workspace offset or -1) of a
+        guard_bands=True plan (lt_guard_check; synchronizes the stream)."""
+        off = ctypes.c_int64(-1)
+        bad = ctypes.c_int32(0)
+        with self._dev():
+            _chk(_lib.lt_guard_check(self._p, ctypes.byref(bad), ctypes.byref(off), self._st()), "lt_guard_check")
+        return int(bad.value), int(off.value)
 
     def slot_table(self):
         """(slots_per_rank, slot -> global ROI table [world * spr]) of the partition (lt_plan_slot_table)."""

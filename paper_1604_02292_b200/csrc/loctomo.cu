@@ -51,6 +51,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int LT_MAX_PEERS = 64;
 constexpr int LT_MAX_DEV = 64;      // per-device caches (occupancy, __constant__ tables) are indexed by ordinal
+constexpr unsigned char kGuardByte = 0xA5;   // LT_GUARD_BANDS canary
 
 // the calling thread's current device (every launch goes to it); -1 on error
 int cur_dev() {
@@ -163,6 +164,7 @@ struct lt_plan {
     // workspace
     char* ws = nullptr;
     int64_t ws_bytes = 0;
+    std::vector<std::pair<size_t, size_t>> guards;   // LT_GUARD_BANDS: (offset, bytes) canary bands
     bool bound = false, bank_ready = false, wd_ready = false;
     int last_mode = -1;
     bool lam_array = false;       // tv solve with per-ROI lambda (lt_tv_solve_lambdas)
@@ -1211,7 +1213,21 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     const int nb = (n + 31) / 32;
     p->stitch_cap = n_roi * std::max(1, world) * ((side + 31) / 32 + 1) * ((side + 31) / 32 + 1);
     size_t o = 0;
-    auto take = [&](size_t bytes) { const size_t r = o; o = align256(o + bytes); return r; };
+    // LT_GUARD_BANDS: every region is followed by a canary band (from the first
+    // 16-byte boundary after its last byte to 256 bytes past its aligned end),
+    // filled at bind time and checked by lt_guard_check: any out-of-bounds write
+    // of a kernel into the workspace shows up as a changed canary
+    const bool guard = (flags & LT_GUARD_BANDS) != 0;
+    auto take = [&](size_t bytes) {
+        const size_t r = o;
+        o = align256(o + bytes);
+        if (guard) {
+            const size_t g0 = (r + bytes + 15) & ~size_t(15);
+            p->guards.push_back({g0, o + 256 - g0});
+            o += 256;
+        }
+        return r;
+    };
     auto& f = p->off;
     f.angf = take(n_angles * sizeof(AngF));
     f.cs64 = take(n_angles * 8); f.sn64 = take(n_angles * 8); f.A64 = take(n_angles * 8); f.B64 = take(n_angles * 8);
@@ -1322,6 +1338,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
         if (!p->xsblk[l].empty()) LT_CUDA(up(p->off.xsblk[l], p->xsblk[l].data(), p->xsblk[l].size() * 4));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.err, 0, 4, st));
     LT_CUDA(cudaMemsetAsync(p->ws + p->off.discc32, 0, 4, st));
+    for (auto& g : p->guards) LT_CUDA(cudaMemsetAsync(p->ws + g.first, kGuardByte, g.second, st));
     LT_CUDA(cudaStreamSynchronize(st));
     if (!p->gst[0]) {
         const char* e = getenv("LT_SPLIT");
@@ -1664,6 +1681,28 @@ int lt_stitch_slots(const lt_plan* p, const float* d_cores_all, int32_t n_slots,
     if (int rc = check_plan(p)) return rc;
     if (!d_image || n_slots < 0 || (n_slots > 0 && (!d_cores_all || !h_slot_roi))) return fail(LT_ERR_INVALID, "bad arguments");
     return combine(*p, d_cores_all, n_slots, h_slot_roi, d_image, (cudaStream_t)stream);
+}
+
+int lt_guard_check(const lt_plan* p, int32_t* h_damaged, int64_t* h_bad_offset, void* stream) {
+    if (int rc = check_plan(p)) return rc;
+    if (!h_damaged) return fail(LT_ERR_INVALID, "null output");
+    if (p->guards.empty()) return fail(LT_ERR_INVALID, "plan was set up without LT_GUARD_BANDS");
+    LT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    std::vector<unsigned char> buf;
+    int bad = 0;
+    if (h_bad_offset) *h_bad_offset = -1;
+    for (auto& g : p->guards) {
+        buf.resize(g.second);
+        LT_CUDA(cudaMemcpy(buf.data(), p->ws + g.first, g.second, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < g.second; ++i)
+            if (buf[i] != kGuardByte) {
+                if (!bad && h_bad_offset) *h_bad_offset = (int64_t)(g.first + i);
+                ++bad;
+                break;
+            }
+    }
+    *h_damaged = bad;
+    return LT_OK;
 }
 
 int32_t lt_window_width(int32_t h) { return h < 1 ? -1 : window_width(h); }
