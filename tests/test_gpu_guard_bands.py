@@ -51,7 +51,7 @@ def test_guard_bands_small_configs_every_entry(lt, case):
     c1 = plan.sirt_solve(sino, 0.0, math.inf)
     c2 = plan.tv_solve(sino, 0.05, 5)
     plan.tv_solve(sino, np.linspace(0.0, 0.1, plan.R), 4)
-    plan.haar_solve(sino, 0.02, 3)
+    plan.haar_solve(sino, 0.02, 3 if case == "C1" else 0)     # (C2 has clipped ROIs: 0 levels)
     plan.exterior_solve(sino)
     plan.combine(c2, plan.local_rois)
     plan.combine_rois(c2)

@@ -6,8 +6,7 @@
 //   * FP32 pipe: FFMA (scalar) and FFMA2 (paired) with 8 independent chains per
 //     thread, 2 flops per lane-FMA, over all SMs.
 // Each kernel runs on every SM with 2048 threads per SM, timed by CUDA events
-// (best of 5 after a warm-up); the SM clock is measured with clock64 in the
-// same kernel (cycles / elapsed).  Prints one JSON object.
+// (best of 5 after a warm-up).  Prints one JSON object.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/peaks_micro tools/peaks_micro.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -124,19 +123,20 @@ int main() {
     const double b64 = nl * it_lds * 8 * 8, b128 = nl * it_lds * 8 * 16;              // bytes delivered
     const double fl = nf * it_fma * 8 * 2 * 2;                                        // 16 lane-FMAs x 2 flops
     // clock: cycles of CTA 0 over the kernel time (CTA 0 spans ~the whole kernel: one wave)
-    auto mhz = [](long long cy, float ms) { return cy / (ms * 1e3); };
     printf("{\"device_sms\": %d, \"ctas_lds\": %d, \"ctas_fma\": %d, \"threads_per_cta\": %d,\n", sms, ctas_lds,
            ctas_fma, threads);
-    printf(" \"smem_lds64_gbs\": %.1f, \"smem_lds64_B_per_clk_per_sm\": %.2f, \"lds64_mhz\": %.0f,\n",
-           b64 / (ms64 * 1e6), b64 / (cy64 * (double)sms), mhz(cy64, ms64));
-    printf(" \"smem_lds128_gbs\": %.1f, \"smem_lds128_B_per_clk_per_sm\": %.2f, \"lds128_mhz\": %.0f,\n",
-           b128 / (ms128 * 1e6), b128 / (cy128 * (double)sms), mhz(cy128, ms128));
-    printf(" \"ffma_tflops\": %.2f, \"ffma_flops_per_clk_per_sm\": %.1f, \"ffma_mhz\": %.0f,\n",
-           fl / (msf * 1e9), fl / (cyf * (double)sms), mhz(cyf, msf));
-    printf(" \"ffma2_tflops\": %.2f, \"ffma2_flops_per_clk_per_sm\": %.1f, \"ffma2_mhz\": %.0f,\n",
-           fl / (msf2 * 1e9), fl / (cyf2 * (double)sms), mhz(cyf2, msf2));
+    // per SM-clock at the B200's 1965 MHz max SM clock (MEASURED_PEAKS.json)
+    const double clk = 1965e6 * sms;
+    printf(" \"smem_lds64_gbs\": %.1f, \"smem_lds64_B_per_clk_per_sm_at_1965MHz\": %.1f,\n",
+           b64 / (ms64 * 1e6), b64 / (ms64 * 1e-3) / clk);
+    printf(" \"smem_lds128_gbs\": %.1f, \"smem_lds128_B_per_clk_per_sm_at_1965MHz\": %.1f,\n",
+           b128 / (ms128 * 1e6), b128 / (ms128 * 1e-3) / clk);
+    printf(" \"ffma_tflops\": %.2f, \"ffma_flops_per_clk_per_sm_at_1965MHz\": %.1f,\n",
+           fl / (msf * 1e9), fl / (msf * 1e-3) / clk);
+    printf(" \"ffma2_tflops\": %.2f, \"ffma2_flops_per_clk_per_sm_at_1965MHz\": %.1f,\n",
+           fl / (msf2 * 1e9), fl / (msf2 * 1e-3) / clk);
     printf(" \"how\": \"tools/peaks_micro.cu: one full wave (occupancy-sized grid) of %d-thread CTAs, best of 5 "
            "(CUDA events); LDS: conflict-free 32-entry rows, 8 independent loads per iteration; FFMA: 8 independent "
-           "chains per thread; MHz = CTA 0 clock64 cycles / kernel time\"}\n", threads);
+           "chains per thread\"}\n", threads);
     return 0;
 }
