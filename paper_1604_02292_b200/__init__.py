@@ -19,6 +19,8 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_loctomo.so")
+if os.environ.get("LT_SO"):          # diagnostics only (tools/ab.sh): an alternative build of the same library
+    LIB_PATH = os.environ["LT_SO"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -123,6 +123,10 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 constexpr int FP2_BL = 16;       // lines per band
 constexpr int FP2_P = 272;       // (S, D) entries per staged line (>= T + PADL + PADR)
 constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16;  // float4 chunks per thread per band (16 threads per line)
+#ifndef FP_STAGE64
+#define FP_STAGE64 1   // staging by 8-byte pixel pairs: each STS.128 of a half-warp covers 256 contiguous bytes
+#endif
+constexpr int FP2_CPT2 = (FP2_P / 2 + 15) / 16; // float2 chunks per thread per band (FP_STAGE64)
 
 template <bool CLAMP>
 __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
@@ -150,6 +154,8 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
     return acc;
 }
 
+// (a double-buffered band -- one CTA barrier per band, the transform off the
+// critical path -- measured no faster: C4 FP 1.431 vs 1.425 ms; not kept)
 template <int FP_APW, int NWARP = 8>
 __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo g, Tiles t, FpArgs f,
                                                                             const int* __restrict__ groups) {
@@ -178,7 +184,39 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     // staging map (no division): thread = (line tid / 16, chunks c4 = tid % 16 + 16 u);
     // threads 256.. of a 12-warp CTA do not stage
     const int q4 = TP / 4;                        // float4 chunks per raw line
+    const int q2 = TP / 2;                        // float2 chunks per raw line
     const int sline = threadIdx.x >> 4, sc0 = threadIdx.x & 15;
+#if FP_STAGE64
+    // thread = (line tid / 16, pixel pairs c2 = tid % 16 + 16 u): entry pair (2 c2, 2 c2 + 1)
+    // is one 16-byte store and the 16 threads of a line write 256 contiguous bytes
+    float2 raw[FP2_CPT2];
+    float nxt[FP2_CPT2];
+    auto fetch = [&](int l0) {
+        const bool lok = sline < FP2_BL && l0 + sline < T;
+        const float* rp0 = src + (long long)(l0 + sline) * TP;
+        #pragma unroll
+        for (int u = 0; u < FP2_CPT2; ++u) {
+            const int c2 = sc0 + 16 * u;
+            raw[u] = make_float2(0.f, 0.f);
+            nxt[u] = 0.f;
+            if (lok && c2 < q2) {
+                raw[u] = __ldg(reinterpret_cast<const float2*>(rp0 + c2 * 2));
+                if (c2 + 1 < q2) nxt[u] = __ldg(rp0 + c2 * 2 + 2);
+            }
+        }
+    };
+    auto transform = [&]() {
+        #pragma unroll
+        for (int u = 0; u < FP2_CPT2; ++u) {
+            const int c2 = sc0 + 16 * u;
+            if (sline < FP2_BL && c2 < q2) {
+                const float2 v = raw[u];
+                *reinterpret_cast<float4*>(sd + sline * FP2_P + c2 * 2) =
+                    make_float4(v.x + v.y, v.y - v.x, v.y + nxt[u], nxt[u] - v.y);
+            }
+        }
+    };
+#else
     float4 raw[FP2_CPT];
     float nxt[FP2_CPT];
     auto fetch = [&](int l0) {                    // raw lines l0.. of the band into registers
@@ -207,6 +245,7 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
             }
         }
     };
+#endif
     const int nsplit = f.nsplit > 1 ? f.nsplit : 1;
     const int lbeg = (lv0 / FP2_BL) * FP2_BL + (int)blockIdx.z * FP2_BL, lstep = nsplit * FP2_BL;
     if (lbeg < lv1) { fetch(lbeg); transform(); }

@@ -8,7 +8,7 @@ import synth
 import paper_1604_02292_b200 as lt
 cfg = synth.config(sys.argv[1] if len(sys.argv) > 1 else "C4")
 inp = synth.make_inputs(cfg, noise=True)
-n_iter = 6
+n_iter = int(os.environ.get('KB_NITER', '6'))
 plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter)
 plan.filter_bank()
 sino = torch.from_numpy(inp.sino).cuda()
@@ -23,4 +23,5 @@ torch.cuda.synchronize()
 t = lt.timing_read()
 lt.timing_enable(False)
 print(f"solve {n_iter} it: {e0.elapsed_time(e1):.2f} ms;", {k: (round(v[0] / max(v[1], 1), 3), v[1]) for k, v in t.items()})
-torch.save(cores.cpu(), f"gpurun_out/cores_{os.environ.get('TAG', 'x')}.pt")
+os.makedirs("/tmp/lt_ab", exist_ok=True)
+torch.save(cores.cpu(), f"/tmp/lt_ab/cores_{os.environ.get('TAG', 'x')}.pt")
