@@ -60,60 +60,97 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "@!P bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
 }
 
+
 // ---------------------------------------------------------------------------
 // k_fgp2: the FGP TV prox + FISTA epilogue, laid out for the sm_100
 // paired FP32 datapath (FFMA2 / FADD2: two fp32 lanes per instruction).
 //
-// Warp w of CTA k owns FR full rows (rows (k*NW + w)*FR ...) of the tile, 256
-// columns wide; lane l owns the 8 consecutive columns 8l..8l+7 of each row, as
-// four column pairs.  Vertical neighbours are the same lane (aligned pairs ->
-// paired instructions); the horizontal neighbour across a lane boundary comes
-// by one warp shuffle per row and direction.  Rows crossing warps go through
-// shared memory, rows crossing CTAs through DSMEM (st.async + mbarrier), as in
-// k_fgp.  Per pixel-iteration ~8 issue slots (k_fgp: ~30).
+// Warp w of CTA k owns FR full rows (rows (k*NW + w)*FR ...) of the tile,
+// 64*CP columns wide; lane l owns the 2*CP consecutive columns 2CP*l .. of each
+// row, as CP column pairs (CP = 4: 256-wide tiles; CP = 5: 320-wide tiles,
+// the paper's 256^2 local parts with 1/8 padding).  Vertical
+// neighbours are the same lane (aligned pairs -> paired instructions); the
+// horizontal neighbour across a lane boundary comes by one warp shuffle per
+// row and direction.  Rows crossing warps go through shared memory, rows
+// crossing CTAs through DSMEM (st.async + mbarrier).
 //
 // Masks (A13, Neumann boundary on the valid rectangle H_v x W_v):
 // p exists for rows i < H_v - 1 (warp-uniform per row), q for columns
 // j < W_v - 1 (per-column step register).  Pixels outside the valid rectangle
 // carry finite garbage that no valid pixel reads.
+// (Measured slower in round 1 and removed: named-barrier hand-over between
+// warps, a paired left-neighbour term, halo prefetch at the phase start, a
+// barrier before each halo row.)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float2 f2sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
-// row storage in shared memory: column 8l + c of a 256-wide row at
-// (c >> 2) * 128 + 4l + (c & 3), so each lane moves its octet as two
-// conflict-free 128-bit accesses
-__device__ __forceinline__ void row_st(float* row, int lane, const float2 (&v)[4]) {
-    reinterpret_cast<float4*>(row)[lane] = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
-    reinterpret_cast<float4*>(row + 128)[lane] = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+
+// Staged row layout (shared memory), CP column pairs per lane: pairs 2h, 2h+1
+// of lane l as one float4 at h*128 + 4l (h < CP/2), an odd last pair as a
+// float2 at (CP/2)*128 + 2l -- every access of a warp is conflict free.
+template <int CP> struct RowL {
+    static constexpr int ROW = 64 * CP;            // floats per staged row
+    static constexpr int NQ = CP / 2;              // float4 chunks per lane
+    static constexpr bool ODD = (CP & 1) != 0;     // one float2 chunk
+};
+template <int CP>
+__device__ __forceinline__ void row_st(float* row, int lane, const float2 (&v)[CP]) {
+    #pragma unroll
+    for (int h = 0; h < CP / 2; ++h)
+        reinterpret_cast<float4*>(row + 128 * h)[lane] = make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
+    if constexpr (CP & 1) reinterpret_cast<float2*>(row + 128 * (CP / 2))[lane] = v[CP - 1];
 }
-__device__ __forceinline__ void row_ld(const float* row, int lane, float2 (&v)[4]) {
-    const float4 a = reinterpret_cast<const float4*>(row)[lane];
-    const float4 b = reinterpret_cast<const float4*>(row + 128)[lane];
-    v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
-    v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+template <int CP>
+__device__ __forceinline__ void row_ld(const float* row, int lane, float2 (&v)[CP]) {
+    #pragma unroll
+    for (int h = 0; h < CP / 2; ++h) {
+        const float4 a = reinterpret_cast<const float4*>(row + 128 * h)[lane];
+        v[2 * h] = make_float2(a.x, a.y); v[2 * h + 1] = make_float2(a.z, a.w);
+    }
+    if constexpr (CP & 1) v[CP - 1] = reinterpret_cast<const float2*>(row + 128 * (CP / 2))[lane];
 }
 // the same through 32-bit shared-window addresses (loop-invariant bases, no
 // generic-to-shared conversion inside the iteration loop)
-__device__ __forceinline__ void row_st_s(unsigned row, int lane, const float2 (&v)[4]) {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + 16u * lane),
-                 "f"(v[0].x), "f"(v[0].y), "f"(v[1].x), "f"(v[1].y) : "memory");
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + 512u + 16u * lane),
-                 "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y) : "memory");
+template <int CP>
+__device__ __forceinline__ void row_st_s(unsigned row, int lane, const float2 (&v)[CP]) {
+    #pragma unroll
+    for (int h = 0; h < CP / 2; ++h)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + 512u * h + 16u * lane),
+                     "f"(v[2 * h].x), "f"(v[2 * h].y), "f"(v[2 * h + 1].x), "f"(v[2 * h + 1].y) : "memory");
+    if constexpr (CP & 1)
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row + 512u * (CP / 2) + 8u * lane),
+                     "f"(v[CP - 1].x), "f"(v[CP - 1].y) : "memory");
 }
-__device__ __forceinline__ void row_ld_s(unsigned row, int lane, float2 (&v)[4]) {
-    float a0, a1, a2, a3, b0, b1, b2, b3;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3) : "r"(row + 16u * lane) : "memory");
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(row + 512u + 16u * lane) : "memory");
-    v[0] = make_float2(a0, a1); v[1] = make_float2(a2, a3);
-    v[2] = make_float2(b0, b1); v[3] = make_float2(b2, b3);
+template <int CP>
+__device__ __forceinline__ void row_ld_s(unsigned row, int lane, float2 (&v)[CP]) {
+    #pragma unroll
+    for (int h = 0; h < CP / 2; ++h) {
+        float a0, a1, a2, a3;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3)
+                     : "r"(row + 512u * h + 16u * lane) : "memory");
+        v[2 * h] = make_float2(a0, a1); v[2 * h + 1] = make_float2(a2, a3);
+    }
+    if constexpr (CP & 1) {
+        float a0, a1;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a0), "=f"(a1) : "r"(row + 512u * (CP / 2) + 8u * lane)
+                     : "memory");
+        v[CP - 1] = make_float2(a0, a1);
+    }
 }
-// a lane's 8 consecutive columns of a naturally laid out shared row
-__device__ __forceinline__ void row_ld_nat(const float* p, float2 (&v)[4]) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    const float4 b = reinterpret_cast<const float4*>(p)[1];
-    v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
-    v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+// a lane's 2*CP consecutive columns of a naturally laid out shared row (8-byte aligned)
+template <int CP>
+__device__ __forceinline__ void row_ld_nat(const float* p, float2 (&v)[CP]) {
+    if constexpr (CP % 2 == 0) {
+        #pragma unroll
+        for (int h = 0; h < CP / 2; ++h) {
+            const float4 a = reinterpret_cast<const float4*>(p)[h];
+            v[2 * h] = make_float2(a.x, a.y); v[2 * h + 1] = make_float2(a.z, a.w);
+        }
+    } else {
+        #pragma unroll
+        for (int c2 = 0; c2 < CP; ++c2) v[c2] = reinterpret_cast<const float2*>(p)[c2];
+    }
 }
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -122,34 +159,26 @@ __device__ __forceinline__ void st_async_v4(unsigned remote, float4 v, unsigned 
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
                  ::"r"(remote), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar) : "memory");
 }
-__device__ __forceinline__ void row_push(unsigned remote_row, int lane, const float2 (&v)[4], unsigned remote_bar) {
-    st_async_v4(remote_row + 16u * lane, make_float4(v[0].x, v[0].y, v[1].x, v[1].y), remote_bar);
-    st_async_v4(remote_row + 512u + 16u * lane, make_float4(v[2].x, v[2].y, v[3].x, v[3].y), remote_bar);
+__device__ __forceinline__ void st_async_v2(unsigned remote, float2 v, unsigned remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+                 ::"r"(remote), "f"(v.x), "f"(v.y), "r"(remote_bar) : "memory");
+}
+template <int CP>
+__device__ __forceinline__ void row_push(unsigned remote_row, int lane, const float2 (&v)[CP], unsigned remote_bar) {
+    #pragma unroll
+    for (int h = 0; h < CP / 2; ++h)
+        st_async_v4(remote_row + 512u * h + 16u * lane, make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y),
+                    remote_bar);
+    if constexpr (CP & 1) st_async_v2(remote_row + 512u * (CP / 2) + 8u * lane, v[CP - 1], remote_bar);
 }
 
-constexpr int FGP2_ROW = 256;     // columns per warp row (32 lanes x 8)
-// producer / consumer named barriers between two neighbouring warps (ids 1..15; 0 = __syncthreads)
-__device__ __forceinline__ void bar_arrive2(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void bar_sync2(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-#ifndef FGP_NAMED_BARS
-#define FGP_NAMED_BARS 0          // 1: named-barrier hand-over (measured slower: 1.35 vs 1.26 ms, C4 tiles)
-#endif
-#ifndef FGP_PAIR_SLEFT
-#define FGP_PAIR_SLEFT 0           // 1: paired left-neighbour term (measured: no gain)
-#endif
-#ifndef FGP_HALO_PREFETCH
-#define FGP_HALO_PREFETCH 0       // 1: halo rows loaded at the phase start (255 registers; measured slower: 1.59 ms)
-#endif
-#ifndef FGP_BAR_LATE
-#define FGP_BAR_LATE 0            // 1: barrier before each halo row (measured slower: 1.30 vs 1.26 ms)
-#endif
-#ifndef FGP_HALO_LAST
-#define FGP_HALO_LAST 1           // rows that read a halo are computed last in their phase
-#endif
+constexpr int FGP2_ROW = 256;     // columns per warp row of the CP = 4 kernel (32 lanes x 8)
+constexpr int FGP2_ROW_MAX = 320; // widest tile (CP = 5)
 template <int V> struct Parity { __device__ __forceinline__ operator int() const { return V; } };
 
-template <int FR, int NW>
+template <int FR, int NW, int CP = 4>
 struct Fgp2Smem {
+    static constexpr int ROW = RowL<CP>::ROW;
     // halo rows, one slot per warp and parity, so every warp reads its halo
     // from the same place whichever warp or CTA wrote it:
     //   hr[par][j]: the r row above warp j (j = 0: pushed by the CTA above over
@@ -158,17 +187,17 @@ struct Fgp2Smem {
     //               j = NW: pushed by the CTA below)
     // slots never written keep their initial value (r: the shifted zero 1/2, z: 0)
     static constexpr int bars = 0;                             // 4 x u64: r from above [2], z from below [2]
-    static constexpr int hr = 8;                               // [2][NW + 1][256]
-    static constexpr int hz = hr + 2 * (NW + 1) * FGP2_ROW;    // [2][NW + 1][256]
-    static constexpr int hp = hz + 2 * (NW + 1) * FGP2_ROW;    // [NW][256] last p row (epilogue)
-    static constexpr int bsm = hp + NW * FGP2_ROW;             // [NW][FR][256] b (BSM variant)
+    static constexpr int hr = 8;                               // [2][NW + 1][ROW]
+    static constexpr int hz = hr + 2 * (NW + 1) * ROW;         // [2][NW + 1][ROW]
+    static constexpr int hp = hz + 2 * (NW + 1) * ROW;         // [NW][ROW] last p row (epilogue)
+    static constexpr int bsm = hp + NW * ROW;                  // [NW][FR][ROW] b (BSM variant)
     static constexpr int total = bsm;
-    static constexpr int total_bsm = bsm + NW * FR * FGP2_ROW;
-    // MODE 1: [NW][FR][2][256] xprev and x_s rows, fetched with cp.async at
+    static constexpr int total_bsm = bsm + NW * FR * ROW;
+    // MODE 1: [NW][FR][2][ROW] xprev and x_s rows, fetched with cp.async at
     // kernel start (they are inputs the FGP loop never touches) and read by the epilogue
-    static constexpr int xin_floats = NW * FR * 2 * FGP2_ROW;
-    // persistent launch: [NW][FR][256] b of the cluster's next tile (cp.async)
-    static constexpr int bnext_floats = NW * FR * FGP2_ROW;
+    static constexpr int xin_floats = NW * FR * 2 * ROW;
+    // persistent launch: [NW][FR][ROW] b of the cluster's next tile (cp.async)
+    static constexpr int bnext_floats = NW * FR * ROW;
 };
 __device__ __forceinline__ void mbar_inval(unsigned bar) {
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
@@ -176,11 +205,70 @@ __device__ __forceinline__ void mbar_inval(unsigned bar) {
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+// a lane's 2*CP columns [x0, x0 + 2CP) of a global row into shared memory by
+// cp.async: 16-byte chunks (CP even, 16-byte aligned source), 8-byte chunks
+// (CP odd, 8-byte aligned), else per float; columns >= wv are not copied
+template <int CP>
+__device__ __forceinline__ void cp_async_cols(float* dst, const float* src, int x0, int wv, bool vec) {
+    if constexpr (CP % 2 == 0) {
+        #pragma unroll
+        for (int h = 0; h < CP / 2; ++h) {
+            if (vec && x0 + 4 * h + 3 < wv) {
+                cp_async16(dst + 4 * h, src + 4 * h);
+            } else {
+                #pragma unroll
+                for (int c = 4 * h; c < 4 * h + 4; ++c)
+                    if (x0 + c < wv) cp_async4(dst + c, src + c);
+            }
+        }
+    } else {
+        #pragma unroll
+        for (int c2 = 0; c2 < CP; ++c2) {
+            if (vec && x0 + 2 * c2 + 1 < wv) {
+                cp_async8(dst + 2 * c2, src + 2 * c2);
+            } else {
+                #pragma unroll
+                for (int c = 2 * c2; c < 2 * c2 + 2; ++c)
+                    if (x0 + c < wv) cp_async4(dst + c, src + c);
+            }
+        }
+    }
+}
+// store a lane's 2*CP values to a global row (16- / 8-byte stores when aligned)
+template <int CP>
+__device__ __forceinline__ void st_cols(float* dst, const float* v, int x0, int wv, bool vec) {
+    if constexpr (CP % 2 == 0) {
+        #pragma unroll
+        for (int h = 0; h < CP / 2; ++h) {
+            if (vec && x0 + 4 * h + 3 < wv) {
+                *reinterpret_cast<float4*>(dst + 4 * h) = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+            } else {
+                #pragma unroll
+                for (int c = 4 * h; c < 4 * h + 4; ++c)
+                    if (x0 + c < wv) dst[c] = v[c];
+            }
+        }
+    } else {
+        #pragma unroll
+        for (int c2 = 0; c2 < CP; ++c2) {
+            if (vec && x0 + 2 * c2 + 1 < wv) {
+                *reinterpret_cast<float2*>(dst + 2 * c2) = make_float2(v[2 * c2], v[2 * c2 + 1]);
+            } else {
+                #pragma unroll
+                for (int c = 2 * c2; c < 2 * c2 + 2; ++c)
+                    if (x0 + c < wv) dst[c] = v[c];
+            }
+        }
+    }
 }
 
 // BSM: b (read once per iteration) lives in shared memory instead of registers,
@@ -189,10 +277,13 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 // PERSIST: the grid holds only as many clusters as are co-resident; each
 // cluster iterates over the tiles blockIdx.y, + gridDim.y, ... and fetches the
 // next tile's b, x_prev and x_s by cp.async while iterating the current one.
-template <int MODE, int FR, int NW, bool BSM, bool PERSIST = false>
+template <int MODE, int FR, int NW, bool BSM, bool PERSIST = false, int CP = 4>
 __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpArgs A) {
     static_assert(!(PERSIST && BSM), "persistent launch keeps b in registers");
-    using SM = Fgp2Smem<FR, NW>;
+    static_assert(CP == 4 || CP == 5, "256- or 320-wide tiles");
+    using SM = Fgp2Smem<FR, NW, CP>;
+    constexpr int ROW = SM::ROW;
+    constexpr int NC = 2 * CP;                  // columns per lane
     extern __shared__ __align__(16) float sm[];
     cg::cluster_group cl = cg::this_cluster();
     const int K = (int)cl.num_blocks();
@@ -207,7 +298,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i0 = (kr * NW + w) * FR;          // first row of this warp (valid-rectangle coordinates)
-    const int x0 = lane * 8;                    // first column of this lane
+    const int x0 = lane * NC;                   // first column of this lane
     const bool has_up = kr > 0, has_dn = kr < K - 1;
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + SM::bars);
     float* hp = sm + SM::hp;
@@ -221,36 +312,44 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
-    float2 breg[BSM ? 1 : FR][4], r[FR][4], s[FR][4], p[FR][4], q[FR][4], z[FR][4];
-    float* bs = sm + SM::bsm + (w * FR) * FGP2_ROW;          // this warp's b rows (BSM)
-    auto bget = [&](int k, float2 (&v)[4]) {
+    float2 breg[BSM ? 1 : FR][CP], r[FR][CP], s[FR][CP], p[FR][CP], q[FR][CP], z[FR][CP];
+    float* bs = sm + SM::bsm + (w * FR) * ROW;               // this warp's b rows (BSM)
+    auto bget = [&](int k, float2 (&v)[CP]) {
         if constexpr (BSM) {
-            row_ld(bs + k * FGP2_ROW, lane, v);
+            row_ld<CP>(bs + k * ROW, lane, v);
         } else {
             #pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2) v[c2] = breg[k][c2];
+            for (int c2 = 0; c2 < CP; ++c2) v[c2] = breg[k][c2];
         }
     };
     const float* bsrc = A.b + (long long)tile * A.b_tstride + (long long)vr0 * A.b_pitch + vc0;
-    // 16-byte loads when the rows are 16-byte aligned and the lane's 8 columns are valid
-    const bool vec_b = ((reinterpret_cast<uintptr_t>(bsrc) | ((uintptr_t)A.b_pitch << 2)) & 15) == 0 && x0 + 8 <= Wv;
-    float* bnext = sm + SM::total + 2 * SM::xin_floats + (w * FR) * FGP2_ROW;   // (PERSIST layout)
+    // vector loads when the rows are aligned (16 bytes for CP = 4, 8 for CP = 5)
+    // and the lane's columns are valid
+    constexpr unsigned VAL = CP % 2 == 0 ? 15u : 7u;
+    const bool vec_b = ((reinterpret_cast<uintptr_t>(bsrc) | ((uintptr_t)A.b_pitch << 2)) & VAL) == 0 && x0 + NC <= Wv;
+    float* bnext = sm + SM::total + 2 * SM::xin_floats + (w * FR) * ROW;   // (PERSIST layout)
     if (PERSIST && tcount > 0) cp_async_commit_wait_all();   // this tile's b, x_prev, x_s (prefetched)
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
-        float2 bv[4];
+        float2 bv[CP];
         const float* brow = bsrc + (long long)i * A.b_pitch + x0;
         if (PERSIST && tcount > 0) {
-            row_ld_nat(bnext + k * FGP2_ROW + x0, bv);
+            row_ld_nat<CP>(bnext + k * ROW + x0, bv);
         } else if (vec_b && i < Hv) {
-            const float4 u0 = __ldg(reinterpret_cast<const float4*>(brow));
-            const float4 u1 = __ldg(reinterpret_cast<const float4*>(brow) + 1);
-            bv[0] = make_float2(u0.x, u0.y); bv[1] = make_float2(u0.z, u0.w);
-            bv[2] = make_float2(u1.x, u1.y); bv[3] = make_float2(u1.z, u1.w);
+            if constexpr (CP % 2 == 0) {
+                #pragma unroll
+                for (int h = 0; h < CP / 2; ++h) {
+                    const float4 u0 = __ldg(reinterpret_cast<const float4*>(brow) + h);
+                    bv[2 * h] = make_float2(u0.x, u0.y); bv[2 * h + 1] = make_float2(u0.z, u0.w);
+                }
+            } else {
+                #pragma unroll
+                for (int c2 = 0; c2 < CP; ++c2) bv[c2] = __ldg(reinterpret_cast<const float2*>(brow) + c2);
+            }
         } else {
             #pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2) {
+            for (int c2 = 0; c2 < CP; ++c2) {
                 const int x = x0 + 2 * c2;
                 const bool rv = i < Hv;
                 bv[c2] = make_float2((rv && x < Wv) ? __ldg(brow + 2 * c2) : 0.f,
@@ -258,50 +357,38 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             }
         }
         #pragma unroll
-        for (int c2 = 0; c2 < 4; ++c2) {
+        for (int c2 = 0; c2 < CP; ++c2) {
             if constexpr (!BSM) breg[k][c2] = bv[c2];
             r[k][c2] = f2s(0.5f); s[k][c2] = f2s(0.5f); p[k][c2] = f2s(0.5f); q[k][c2] = f2s(0.5f);
         }
-        if constexpr (BSM) row_st(bs + k * FGP2_ROW, lane, bv);
+        if constexpr (BSM) row_st<CP>(bs + k * ROW, lane, bv);
     }
     // FISTA state for the epilogue: asynchronous copies into shared memory now,
     // consumed after the FGP loop (each lane reads back only its own columns)
     float* xin = sm + (BSM ? SM::total_bsm : SM::total) + (PERSIST ? (tcount & 1) * SM::xin_floats : 0) +
-                 (w * FR) * 2 * FGP2_ROW;
-    const bool vec_p = ((vc0 | A.T) & 3) == 0;
+                 (w * FR) * 2 * ROW;
+    const bool vec_p = CP % 2 == 0 ? ((vc0 | A.T) & 3) == 0 : ((vc0 | A.T) & 1) == 0;
     if (MODE == 1 && !(PERSIST && tcount > 0)) {
         #pragma unroll
         for (int k = 0; k < FR; ++k) {
             const int i = i0 + k;
             if (i >= Hv) continue;
             const long long prow = (long long)tile * A.p_tstride + (long long)(vr0 + i) * A.T + vc0 + x0;
-            float* dx = xin + k * 2 * FGP2_ROW + x0;
-            #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (vec_p && x0 + 4 * h + 3 < Wv) {
-                    cp_async16(dx + 4 * h, A.xprev + prow + 4 * h);
-                    cp_async16(dx + FGP2_ROW + 4 * h, A.xs + prow + 4 * h);
-                } else {
-                    #pragma unroll
-                    for (int c = 4 * h; c < 4 * h + 4; ++c)
-                        if (x0 + c < Wv) {
-                            cp_async4(dx + c, A.xprev + prow + c);
-                            cp_async4(dx + FGP2_ROW + c, A.xs + prow + c);
-                        }
-                }
-            }
+            float* dx = xin + k * 2 * ROW + x0;
+            cp_async_cols<CP>(dx, A.xprev + prow, x0, Wv, vec_p);
+            cp_async_cols<CP>(dx + ROW, A.xs + prow, x0, Wv, vec_p);
         }
     }
     const float lam = A.lams ? __ldg(A.lams + tile) : A.lam;
     const float lam2 = 2.f * lam;               // L(p, q) = 2 L(p', q')
     const float gam = lam > 0.f ? 1.f / (16.f * lam) : 0.f;
     // q step per column (0 where q does not exist: j >= W_v - 1)
-    float gq[8];
+    float gq[NC];
     #pragma unroll
-    for (int c = 0; c < 8; ++c) gq[c] = (x0 + c < Wv - 1) ? gam : 0.f;
-    float2 gq2[4];
+    for (int c = 0; c < NC; ++c) gq[c] = (x0 + c < Wv - 1) ? gam : 0.f;
+    float2 gq2[CP];
     #pragma unroll
-    for (int c2 = 0; c2 < 4; ++c2) gq2[c2] = make_float2(gq[2 * c2], gq[2 * c2 + 1]);
+    for (int c2 = 0; c2 < CP; ++c2) gq2[c2] = make_float2(gq[2 * c2], gq[2 * c2 + 1]);
     cl.sync();
     if constexpr (PERSIST) {   // the cluster's next tile: b, x_prev, x_s into shared memory now
         const int tn = tile + (int)gridDim.y;
@@ -312,50 +399,35 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 nvr0 = tn_.vr0; nvc0 = tn_.vc0; nHv = tn_.vr1 - tn_.vr0; nWv = tn_.vc1 - tn_.vc0;
             }
             const float* nb = A.b + (long long)tn * A.b_tstride + (long long)nvr0 * A.b_pitch + nvc0;
-            const bool nvec_b = ((reinterpret_cast<uintptr_t>(nb) | ((uintptr_t)A.b_pitch << 2)) & 15) == 0;
-            float* nxin = sm + SM::total + ((tcount + 1) & 1) * SM::xin_floats + (w * FR) * 2 * FGP2_ROW;
-            const bool nvec_p = ((nvc0 | A.T) & 3) == 0;
+            const bool nvec_b = ((reinterpret_cast<uintptr_t>(nb) | ((uintptr_t)A.b_pitch << 2)) & VAL) == 0;
+            float* nxin = sm + SM::total + ((tcount + 1) & 1) * SM::xin_floats + (w * FR) * 2 * ROW;
+            const bool nvec_p = CP % 2 == 0 ? ((nvc0 | A.T) & 3) == 0 : ((nvc0 | A.T) & 1) == 0;
             #pragma unroll
             for (int k = 0; k < FR; ++k) {
                 const int i = i0 + k;
-                float* db = bnext + k * FGP2_ROW + x0;
+                float* db = bnext + k * ROW + x0;
                 const float* brow = nb + (long long)i * A.b_pitch + x0;
-                #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (i < nHv && nvec_b && x0 + 4 * h + 3 < nWv) {
-                        cp_async16(db + 4 * h, brow + 4 * h);
-                    } else {
-                        #pragma unroll
-                        for (int c = 4 * h; c < 4 * h + 4; ++c) {
-                            if (i < nHv && x0 + c < nWv) cp_async4(db + c, brow + c);
-                            else db[c] = 0.f;
-                        }
-                    }
+                if (i < nHv) {
+                    cp_async_cols<CP>(db, brow, x0, nWv, nvec_b);
+                    #pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        if (x0 + c >= nWv) db[c] = 0.f;
+                } else {
+                    #pragma unroll
+                    for (int c = 0; c < NC; ++c) db[c] = 0.f;
                 }
                 if (MODE == 1 && i < nHv) {
                     const long long prow = (long long)tn * A.p_tstride + (long long)(nvr0 + i) * A.T + nvc0 + x0;
-                    float* dx = nxin + k * 2 * FGP2_ROW + x0;
-                    #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (nvec_p && x0 + 4 * h + 3 < nWv) {
-                            cp_async16(dx + 4 * h, A.xprev + prow + 4 * h);
-                            cp_async16(dx + FGP2_ROW + 4 * h, A.xs + prow + 4 * h);
-                        } else {
-                            #pragma unroll
-                            for (int c = 4 * h; c < 4 * h + 4; ++c)
-                                if (x0 + c < nWv) {
-                                    cp_async4(dx + c, A.xprev + prow + c);
-                                    cp_async4(dx + FGP2_ROW + c, A.xs + prow + c);
-                                }
-                        }
-                    }
+                    float* dx = nxin + k * 2 * ROW + x0;
+                    cp_async_cols<CP>(dx, A.xprev + prow, x0, nWv, nvec_p);
+                    cp_async_cols<CP>(dx + ROW, A.xs + prow, x0, nWv, nvec_p);
                 }
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
     }
     const unsigned up_rank = has_up ? kr - 1 : kr, dn_rank = has_dn ? kr + 1 : kr;
-    constexpr unsigned RB = FGP2_ROW * 4u;             // bytes per staged row
+    constexpr unsigned RB = ROW * 4u;                  // bytes per staged row
     constexpr unsigned PS = (NW + 1) * RB;             // bytes per parity of hr / hz
     const unsigned s_hr = smem_u32(sm + SM::hr), s_hz = smem_u32(sm + SM::hz);
     // this warp's halo slots: r from above, z from below (read); r / z it publishes (written)
@@ -365,7 +437,7 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     const unsigned rem_rx_z = mapa(s_hz + NW * RB, up_rank);       // my first warp's z row -> slot NW of the CTA above
     const unsigned rem_bar_z = mapa(smem_u32(bars + 2), up_rank);
     const unsigned my_r_slot = s_hr + (w + 1) * RB, my_z_slot = s_hz + w * RB;
-    constexpr unsigned row_bytes = FGP2_ROW * 4;
+    constexpr unsigned row_bytes = ROW * 4;
     const int nit = lam > 0.f ? A.nfgp : 0;
     const unsigned bar0 = smem_u32(bars);
     const float2 nl2 = f2s(-lam2);
@@ -374,118 +446,76 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     #pragma unroll
     for (int k = 0; k < FR; ++k) gp[k] = (i0 + k < Hv - 1) ? gam : 0.f;
 
-    // Halo hand-over between the warps of the CTA: NBAR (NW <= 8, with the halo
-    // rows computed last): producer / consumer named barriers per warp pair,
-    // so a warp waits only for the neighbour whose row it reads, and only
-    // before that row; otherwise a CTA barrier after each phase.  Parity cb is
+    // Two CTA barriers per iteration (one after each phase); the rows that read
+    // a halo are computed last in their phase, so the halo's DSMEM transfer and
+    // the neighbour warps' work overlap the interior rows.  Parity cb is
     // compile-time, so every halo address is loop invariant.
-    constexpr bool NBAR = FGP_HALO_LAST && NW <= 8 && FGP_NAMED_BARS;
-    // BAR_LATE: the CTA barrier sits right before each phase's halo row instead
-    // of at the phase end (same count; the segments between barriers balance)
-    constexpr bool BAR_LATE = FGP_HALO_LAST && !NBAR && FGP_BAR_LATE;
     auto fgp_iter = [&](int it, auto cbv) {
         const int cb = cbv, pb = cb ^ 1;
         if (lane == 0) {   // the consuming warp arms its DSMEM receive buffers
             if (w == NW - 1 && has_dn) mbar_expect_tx(bar0 + 16 + 8 * cb, row_bytes);   // z row of it, from below
             if (w == 0 && has_up) mbar_expect_tx(bar0 + 8 * cb, row_bytes);             // r row of it, from above
         }
-        // ---- phase A: z = b - lam2 L(r, s); row 0 first (its upper neighbour
-        // may come from another warp or CTA) and publish it at once
-        // halo rows published before the last barrier: loaded now, used last
-        // (the DSMEM rows wait on their mbarrier first, at the halo row)
-        constexpr bool PRE = FGP_HALO_LAST && !NBAR && !BAR_LATE && FGP_HALO_PREFETCH;
-        const bool up_local = !(w == 0 && has_up);
-        float2 rpre[4];
-        if constexpr (PRE) { if (up_local) row_ld_s(up_slot + pb * PS, lane, rpre); }
+        // ---- phase A: z = b - lam2 L(r, s); halo row 0 last: 1, ..., FR-1, 0
         #pragma unroll
         for (int kk = 0; kk < FR; ++kk) {
-            const int k = FGP_HALO_LAST ? (kk + 1) % FR : kk;     // halo row 0 last: 1, ..., FR-1, 0
-            float2 rup[4];
+            const int k = (kk + 1) % FR;
+            float2 rup[CP];
             if (k > 0) {
                 #pragma unroll
-                for (int c2 = 0; c2 < 4; ++c2) rup[c2] = r[k - 1][c2];
+                for (int c2 = 0; c2 < CP; ++c2) rup[c2] = r[k - 1][c2];
             } else {
-                if constexpr (BAR_LATE) __syncthreads();   // every warp has published its r row of it - 1
                 // slot of parity pb: written in iteration it - 1 (still 1/2 at it = 0)
-                if (PRE && up_local) {
-                    #pragma unroll
-                    for (int c2 = 0; c2 < 4; ++c2) rup[c2] = rpre[c2];
-                } else {
-                    if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
-                    if constexpr (NBAR) { if (w > 0 && it > 0) bar_sync2(NW + w - 1); }   // r row of warp w - 1
-                    row_ld_s(up_slot + pb * PS, lane, rup);
-                }
+                if (w == 0 && has_up && it > 0) mbar_wait(bar0 + 8 * pb, ((it - 1) >> 1) & 1);
+                row_ld_s<CP>(up_slot + pb * PS, lane, rup);
             }
-            float sl = __shfl_up_sync(0xffffffffu, s[k][3].y, 1);
+            float sl = __shfl_up_sync(0xffffffffu, s[k][CP - 1].y, 1);
             if (lane == 0) sl = 0.5f;
             // z = b - lam2 (r - rup) - lam2 s + lam2 s_left
-            float2 t[4], bk[4];
+            float2 t[CP], bk[CP];
             bget(k, bk);
             #pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2) {
+            for (int c2 = 0; c2 < CP; ++c2) {
                 t[c2] = f2fma(nl2, f2sub(r[k][c2], rup[c2]), bk[c2]);
                 t[c2] = f2fma(nl2, s[k][c2], t[c2]);
             }
-#if FGP_PAIR_SLEFT
-            // the left neighbours (s_{j-1}, s_j) as an aligned register pair (two
-            // moves) so the last term is one FFMA2 instead of two scalar FFMAs
-            {
-                const float2 l2 = f2s(lam2);
-                z[k][0] = f2fma(l2, make_float2(sl, s[k][0].x), t[0]);
-                #pragma unroll
-                for (int c2 = 1; c2 < 4; ++c2) z[k][c2] = f2fma(l2, make_float2(s[k][c2 - 1].y, s[k][c2].x), t[c2]);
-            }
-#else
             z[k][0].x = fmaf(lam2, sl, t[0].x);
             z[k][0].y = fmaf(lam2, s[k][0].x, t[0].y);
             #pragma unroll
-            for (int c2 = 1; c2 < 4; ++c2) {
+            for (int c2 = 1; c2 < CP; ++c2) {
                 z[k][c2].x = fmaf(lam2, s[k][c2 - 1].y, t[c2].x);
                 z[k][c2].y = fmaf(lam2, s[k][c2].x, t[c2].y);
             }
-#endif
             if (k == 0) {
-                if (w == 0 && has_up) row_push(rem_rx_z + cb * PS, lane, z[0], rem_bar_z + cb * 8);
-                if (w > 0) row_st_s(my_z_slot + cb * PS, lane, z[0]);
-                if constexpr (NBAR) { if (w > 0) bar_arrive2(w); }           // z row -> warp w - 1
+                if (w == 0 && has_up) row_push<CP>(rem_rx_z + cb * PS, lane, z[0], rem_bar_z + cb * 8);
+                if (w > 0) row_st_s<CP>(my_z_slot + cb * PS, lane, z[0]);
             }
         }
-        if constexpr (!NBAR && !BAR_LATE) __syncthreads();
+        __syncthreads();
         // ---- phase B: dual ascent, projection on [0, 1] (shifted), FGP momentum;
-        // last row first and publish it
+        // halo row FR-1 last: 0, ..., FR-1
         const float beta = c_fgp_beta[it];
         const float2 beta2 = f2s(beta);
-        const bool dn_local = !(w == NW - 1 && has_dn);
-        float2 zpre[4];
-        if constexpr (PRE) { if (dn_local) row_ld_s(dn_slot + cb * PS, lane, zpre); }
         #pragma unroll
-        for (int kk = 0; kk < FR; ++kk) {
-            const int k = FGP_HALO_LAST ? kk : (kk + FR - 1) % FR;   // halo row FR-1 last: 0, ..., FR-1
-            float2 zb[4];
+        for (int k = 0; k < FR; ++k) {
+            float2 zb[CP];
             if (k < FR - 1) {
                 #pragma unroll
-                for (int c2 = 0; c2 < 4; ++c2) zb[c2] = z[k + 1][c2];
+                for (int c2 = 0; c2 < CP; ++c2) zb[c2] = z[k + 1][c2];
             } else {
-                if constexpr (BAR_LATE) __syncthreads();   // every warp has published its z row of it
-                if (PRE && dn_local) {
-                    #pragma unroll
-                    for (int c2 = 0; c2 < 4; ++c2) zb[c2] = zpre[c2];
-                } else {
-                    if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
-                    if constexpr (NBAR) { if (w < NW - 1) bar_sync2(w + 1); }     // z row of warp w + 1
-                    row_ld_s(dn_slot + cb * PS, lane, zb);
-                }
+                if (w == NW - 1 && has_dn) mbar_wait(bar0 + 16 + 8 * cb, (it >> 1) & 1);
+                row_ld_s<CP>(dn_slot + cb * PS, lane, zb);
             }
             const float zr = __shfl_down_sync(0xffffffffu, z[k][0].x, 1);   // lane 31: masked by gq
             const float gpk = gp[k];
             const float2 gp2 = f2s(gpk);
             #pragma unroll
-            for (int c2 = 0; c2 < 4; ++c2) {
+            for (int c2 = 0; c2 < CP; ++c2) {
                 // p' = sat(r + g (z - z_below)), q' = sat(s + g (z - z_right))
                 const float2 tp = f2fma(gp2, z[k][c2], r[k][c2]);
                 const float2 tq = f2fma(gq2[c2], z[k][c2], s[k][c2]);
                 const float zrx = z[k][c2].y;
-                const float zry = c2 < 3 ? z[k][c2 + 1].x : zr;
+                const float zry = c2 < CP - 1 ? z[k][c2 + 1].x : zr;
                 float2 pn, qn;
                 pn.x = __saturatef(fmaf(-gpk, zb[c2].x, tp.x));
                 pn.y = __saturatef(fmaf(-gpk, zb[c2].y, tp.y));
@@ -497,12 +527,11 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
                 q[k][c2] = qn;
             }
             if (k == FR - 1) {
-                if (w == NW - 1 && has_dn) row_push(rem_rx_r + cb * PS, lane, r[FR - 1], rem_bar_r + cb * 8);
-                if (w < NW - 1) row_st_s(my_r_slot + cb * PS, lane, r[FR - 1]);
-                if constexpr (NBAR) { if (w < NW - 1 && it + 1 < nit) bar_arrive2(NW + w); }   // r row -> warp w + 1
+                if (w == NW - 1 && has_dn) row_push<CP>(rem_rx_r + cb * PS, lane, r[FR - 1], rem_bar_r + cb * 8);
+                if (w < NW - 1) row_st_s<CP>(my_r_slot + cb * PS, lane, r[FR - 1]);
             }
         }
-        if constexpr (!NBAR && !BAR_LATE) __syncthreads();
+        __syncthreads();
     };
     {
         int it = 0;
@@ -514,31 +543,31 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     }
 
     // ---- x = b - lam2 L(p', q'), then the epilogue
-    row_st(hp + w * FGP2_ROW, lane, p[FR - 1]);
+    row_st<CP>(hp + w * ROW, lane, p[FR - 1]);
     cl.sync();
-    float2 pup0[4];
-    if (w > 0) row_ld(hp + (w - 1) * FGP2_ROW, lane, pup0);
-    else if (has_up) row_ld(cl.map_shared_rank(hp, kr - 1) + (NW - 1) * FGP2_ROW, lane, pup0);
+    float2 pup0[CP];
+    if (w > 0) row_ld<CP>(hp + (w - 1) * ROW, lane, pup0);
+    else if (has_up) row_ld<CP>(cl.map_shared_rank(hp, kr - 1) + (NW - 1) * ROW, lane, pup0);
     else {
         #pragma unroll
-        for (int c2 = 0; c2 < 4; ++c2) pup0[c2] = f2s(0.5f);
+        for (int c2 = 0; c2 < CP; ++c2) pup0[c2] = f2s(0.5f);
     }
     // the neighbour's halo row has been read: arrive now, wait at exit (keeps
     // shared memory alive until every neighbour has read its halo)
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     if constexpr (MODE == 1) cp_async_commit_wait_all();
-    const bool vec_y = (vc0 & 3) == 0;                  // y rows: PADL + vc0 + x0, TP % 4 == 0
+    const bool vec_y = CP % 2 == 0 ? (vc0 & 3) == 0 : (vc0 & 1) == 0;   // y rows: PADL + vc0 + x0, TP % 4 == 0
     const bool vec_yT = FR == 4 && (vr0 & 3) == 0;      // yT columns: PADL + vr0 + i0 + k
-    float xall[FR][8];
+    float xall[FR][NC];
     #pragma unroll
     for (int k = 0; k < FR; ++k) {
         const int i = i0 + k;
-        float ql = __shfl_up_sync(0xffffffffu, q[k][3].y, 1);
+        float ql = __shfl_up_sync(0xffffffffu, q[k][CP - 1].y, 1);
         if (lane == 0) ql = 0.5f;
-        float2 bk[4];
+        float2 bk[CP];
         bget(k, bk);
         #pragma unroll
-        for (int c2 = 0; c2 < 4; ++c2) {
+        for (int c2 = 0; c2 < CP; ++c2) {
             const float2 pu = k > 0 ? p[k - 1][c2] : pup0[c2];
             const float qlx = c2 > 0 ? q[k][c2 - 1].y : ql;
             xall[k][2 * c2] = bk[c2].x - lam2 * (p[k][c2].x + q[k][c2].x - pu.x - qlx);
@@ -547,52 +576,38 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
         if (i >= Hv) continue;
         if constexpr (MODE == 0) {
             #pragma unroll
-            for (int c = 0; c < 8; ++c)
+            for (int c = 0; c < NC; ++c)
                 if (x0 + c < Wv) A.out[(long long)tile * A.out_tstride + (long long)i * A.out_pitch + x0 + c] = xall[k][c];
         } else {
             const int ti_ = vr0 + i;
             const long long prow = (long long)tile * A.p_tstride + (long long)ti_ * A.T + vc0 + x0;
             float* yrow = A.y + (long long)tile * A.y_tstride + (long long)ti_ * A.TP + PADL + vc0 + x0;
-            const float* sx = xin + k * 2 * FGP2_ROW + x0;
-            float xp[8], xsv[8];
-            *reinterpret_cast<float4*>(xp) = *reinterpret_cast<const float4*>(sx);
-            *reinterpret_cast<float4*>(xp + 4) = *reinterpret_cast<const float4*>(sx + 4);
-            *reinterpret_cast<float4*>(xsv) = *reinterpret_cast<const float4*>(sx + FGP2_ROW);
-            *reinterpret_cast<float4*>(xsv + 4) = *reinterpret_cast<const float4*>(sx + FGP2_ROW + 4);
-            float yv[8];
+            const float* sx = xin + k * 2 * ROW + x0;
+            float xp[NC], xsv[NC];
             #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int c2 = 0; c2 < CP; ++c2) {
+                const float2 a = *reinterpret_cast<const float2*>(sx + 2 * c2);
+                const float2 b = *reinterpret_cast<const float2*>(sx + ROW + 2 * c2);
+                xp[2 * c2] = a.x; xp[2 * c2 + 1] = a.y; xsv[2 * c2] = b.x; xsv[2 * c2 + 1] = b.y;
+            }
+            float yv[NC];
+            #pragma unroll
+            for (int c = 0; c < NC; ++c) {
                 const float x = xall[k][c];
                 const float rr = x + A.beta_o * (x - xp[c]);          // FISTA extrapolation (A12)
                 yv[c] = rr - xsv[c];                                  // x_L^k = r - x_s^k
             }
-            #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (x0 + 4 * h + 3 < Wv && vec_p) {
-                    *reinterpret_cast<float4*>(A.xprev + prow + 4 * h) =
-                        make_float4(xall[k][4 * h], xall[k][4 * h + 1], xall[k][4 * h + 2], xall[k][4 * h + 3]);
-                } else {
-                    #pragma unroll
-                    for (int c = 4 * h; c < 4 * h + 4; ++c)
-                        if (x0 + c < Wv) A.xprev[prow + c] = xall[k][c];
-                }
-                if (x0 + 4 * h + 3 < Wv && vec_y) {
-                    *reinterpret_cast<float4*>(yrow + 4 * h) = make_float4(yv[4 * h], yv[4 * h + 1], yv[4 * h + 2], yv[4 * h + 3]);
-                } else {
-                    #pragma unroll
-                    for (int c = 4 * h; c < 4 * h + 4; ++c)
-                        if (x0 + c < Wv) yrow[c] = yv[c];
-                }
-            }
+            st_cols<CP>(A.xprev + prow, xall[k], x0, Wv, vec_p);
+            st_cols<CP>(yrow, yv, x0, Wv, vec_y);
             if (vec_yT) {
                 // the warp's FR = 4 rows are consecutive: the transposed copy of
                 // column c is one 16-byte store per lane, written after the last row
                 #pragma unroll
-                for (int c = 0; c < 8; ++c) xall[k][c] = yv[c];
+                for (int c = 0; c < NC; ++c) xall[k][c] = yv[c];
             } else {
                 float* ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + ti_;
                 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < NC; ++c)
                     if (x0 + c < Wv) ycol[(long long)c * A.TP] = yv[c];
             }
         }
@@ -602,13 +617,13 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
             float* ycol = A.yT + (long long)tile * A.y_tstride + (long long)(vc0 + x0) * A.TP + PADL + vr0 + i0;
             if (i0 + 3 < Hv) {
                 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < NC; ++c)
                     if (x0 + c < Wv)
                         *reinterpret_cast<float4*>(ycol + (long long)c * A.TP) =
                             make_float4(xall[0][c], xall[FR > 1 ? 1 : 0][c], xall[FR > 2 ? 2 : 0][c], xall[FR > 3 ? 3 : 0][c]);
             } else {
                 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < NC; ++c)
                     #pragma unroll
                     for (int k = 0; k < FR; ++k)
                         if (x0 + c < Wv && i0 + k < Hv) ycol[(long long)c * A.TP + k] = xall[k][c];

@@ -295,8 +295,35 @@ bool fp_wide() {
 // single-pass k_fp for tiles wider than its band)
 int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const float* imgT, long long img_ts,
                   float* out, long long out_ts, cudaStream_t st) {
-    if (t.TP > FP2_P || t.Wwin > 32 * FP_U)
+    if (t.TP > FP2_PW || t.Wwin > 32 * FP_UW)
         return launch_fp(p, 0, t, img, imgT, img_ts, out, out_ts, nullptr, nullptr, st);
+    if (t.TP > FP2_P || t.Wwin > 32 * FP_U) {
+        // wide tiles (up to 320: the paper's 256^2 parts with 1/8 padding): 8 warps x
+        // 1 angle, 336-entry staged lines, 15 rays per lane; bands split over CTAs
+        // when a launch is under one wave (as below)
+        const size_t smemw = (size_t)FP2_BL * FP2_PW * sizeof(float2) + (size_t)8 * 32 * FP_UW * sizeof(float);
+        auto kw = k_fp_roi2<1, 8, FP2_PW, FP_UW>;
+        LT_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemw));
+        FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1, p.a_lo, p.a_hi};
+        ScopedTimer tm(TC_FP, st);
+        const long long ctas = (long long)p.ngroups1 * t.ntiles;
+        const int nbands = (t.T + FP2_BL - 1) / FP2_BL;
+        static long long resident_dev[LT_MAX_DEV] = {};
+        const int dv = std::max(0, cur_dev());
+        if (!resident_dev[dv]) resident_dev[dv] = resident_ctas(p, kw, 256, smemw);
+        int nsplit = 1;
+        if (ctas < resident_dev[dv] && p.nsplit <= 1 && nbands >= 8) nsplit = best_split(ctas, nbands, resident_dev[dv], 8);
+        if (nsplit > 1 && (long long)nsplit * t.ntiles * p.na * t.Wwin <= p.fpart_cap) {
+            f.part = p.P<float>(p.off.fpart); f.nsplit = nsplit;
+            kw<<<dim3(p.ngroups1, t.ntiles, nsplit), 256, smemw, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
+            LT_LAUNCHED();
+            k_fp_join<<<dim3((t.Wwin + 127) / 128, p.na, t.ntiles), 128, 0, st>>>(p.geo(), t, f);
+        } else {
+            kw<<<dim3(p.ngroups1, t.ntiles), 256, smemw, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
+        }
+        LT_LAUNCHED();
+        return LT_OK;
+    }
     // 16 angles per CTA share each staged band; 8 when that would leave the
     // SMs short of two waves (small ROI batches: C1-C3, T1, 8-GPU shards)
     const bool one = (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
@@ -440,10 +467,11 @@ SinoView view_win(const float* base, int Wwin, int na) {
     return SinoView{base, (long long)na * Wwin, Wwin, 0, Wwin};
 }
 
-// the FGP kernel supports extended ROIs up to 256 x 256 (32 lanes x 8 columns)
+// the FGP kernels support extended ROIs up to 320 x 320 (32 lanes x 8 columns
+// up to 256, 32 lanes x 10 columns above: the paper's 256^2 parts padded by 1/8)
 int fgp_check(int rows, int cols) {
-    if (rows < 1 || cols < 1 || cols > 256 || rows > 256)
-        return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported (extended ROI side <= 256)", rows, cols);
+    if (rows < 1 || cols < 1 || cols > FGP2_ROW_MAX || rows > FGP2_ROW_MAX)
+        return fail(LT_ERR_INVALID, "FGP tile %dx%d unsupported (extended ROI side <= %d)", rows, cols, FGP2_ROW_MAX);
     return LT_OK;
 }
 
@@ -473,15 +501,16 @@ int ensure_fgp_beta(int nfgp, cudaStream_t st) {
 // k_fgp2 (paired-FP32 layout): NW warps of FR full rows per CTA, K CTAs per
 // cluster.  LT_FGP2_CFG = "4x8" (default, 8-CTA clusters for 256-row tiles),
 // "2x8" (16-CTA clusters), "2x8b" (b in shared memory, two CTAs per SM).
-template <int MODE, int FR, int NW, bool BSM = false, bool PERSIST = false>
+// CP = 5: tiles wider than 256 (up to 320) with 10 columns per lane (3 rows per warp).
+template <int MODE, int FR, int NW, bool BSM = false, bool PERSIST = false, int CP = 4>
 int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clusters = nullptr) {
     const int K = (rows + NW * FR - 1) / (NW * FR);
     if (K > 16) return fail(LT_ERR_INVALID, "FGP tile with %d rows needs a %d-CTA cluster (> 16)", rows, K);
-    using SMl = Fgp2Smem<FR, NW>;
+    using SMl = Fgp2Smem<FR, NW, CP>;
     const size_t smem = PERSIST ? (size_t)(SMl::total + 2 * SMl::xin_floats + SMl::bnext_floats) * sizeof(float)
                                 : (size_t)((BSM ? SMl::total_bsm : SMl::total) +
                                            (MODE == 1 ? SMl::xin_floats : 0)) * sizeof(float);
-    auto kern = k_fgp2<MODE, FR, NW, BSM, PERSIST>;
+    auto kern = k_fgp2<MODE, FR, NW, BSM, PERSIST, CP>;
     LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (K > 8) LT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg;
@@ -523,6 +552,9 @@ template <int MODE>
 int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     if (int rc = fgp_check(rows, cols)) return rc;
     if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
+    // wide tiles (257..320 columns or rows): 10 columns per lane, 3 rows per warp,
+    // 24-row CTAs (clusters of up to 14 CTAs)
+    if (rows > FGP2_ROW || cols > FGP2_ROW) return launch_fgp2_t<MODE, 3, 8, false, false, 5>(A, rows, ntiles, st);
     static int cfgv = -1;
     if (cfgv < 0) {
         const char* e = getenv("LT_FGP2_CFG");
@@ -2109,7 +2141,8 @@ int lt_global_cp(lt_plan* p, const float* d_sino, int32_t n_iter, float mu, floa
 
 int lt_fgp_batch(int32_t h, int32_t w, int32_t count, const float* d_in, float lambda, int32_t n_fgp, float* d_out,
                  void* stream) {
-    if (h < 1 || w < 1 || count < 0 || !(lambda >= 0.f) || n_fgp < 1 || n_fgp > 4096 || h > 256 || w > 256)
+    if (h < 1 || w < 1 || count < 0 || !(lambda >= 0.f) || n_fgp < 1 || n_fgp > 4096 || h > FGP2_ROW_MAX ||
+        w > FGP2_ROW_MAX)
         return fail(LT_ERR_INVALID, "bad FGP arguments");
     if (count == 0) return LT_OK;
     if (!d_in || !d_out) return fail(LT_ERR_INVALID, "null pointer");

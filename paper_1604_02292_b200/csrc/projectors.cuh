@@ -122,13 +122,15 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 // ---------------------------------------------------------------------------
 constexpr int FP2_BL = 16;       // lines per band
 constexpr int FP2_P = 272;       // (S, D) entries per staged line (>= T + PADL + PADR)
+constexpr int FP2_PW = 336;      // wide tiles (T <= 328 - PADL - PADR = 320): entries per staged line
+constexpr int FP_UW = 15;        // wide tiles: rays per lane (window W(160) = 456 <= 32 * 15)
 constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16;  // float4 chunks per thread per band (16 threads per line)
 #ifndef FP_STAGE64
 #define FP_STAGE64 1   // staging by 8-byte pixel pairs: each STS.128 of a half-warp covers 256 contiguous bytes
 #endif
 constexpr int FP2_CPT2 = (FP2_P / 2 + 15) / 16; // float2 chunks per thread per band (FP_STAGE64)
 
-template <bool CLAMP>
+template <bool CLAMP, int SP = FP2_P>
 __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
     const unsigned rowbase = __shfl_sync(0xffffffffu, rowbase_, threadIdx.x & 31);
     float acc = 0.f;
@@ -146,8 +148,8 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
         const unsigned a0 = rowbase + ((unsigned)__float_as_int(rm.x) << 3);
         const unsigned a1 = rowbase + ((unsigned)__float_as_int(rm.y) << 3);
         float s0, d0, s1, d1;
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s0), "=f"(d0) : "r"(a0 + (unsigned)(i * FP2_P * 8)));
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s1), "=f"(d1) : "r"(a1 + (unsigned)((i + 1) * FP2_P * 8)));
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s0), "=f"(d0) : "r"(a0 + (unsigned)(i * SP * 8)));
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s1), "=f"(d1) : "r"(a1 + (unsigned)((i + 1) * SP * 8)));
         acc = fmaf(g.x, d0, acc + s0);
         acc = fmaf(g.y, d1, acc + s1);
     }
@@ -156,10 +158,14 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
 
 // (a double-buffered band -- one CTA barrier per band, the transform off the
 // critical path -- measured no faster: C4 FP 1.431 vs 1.425 ms; not kept)
-template <int FP_APW, int NWARP = 8>
+// SP, SU: staged entries per line and rays per lane (FP2_P, FP_U; FP2_PW, FP_UW for
+// tiles wider than 256)
+template <int FP_APW, int NWARP = 8, int SP = FP2_P, int SU = FP_U>
 __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo g, Tiles t, FpArgs f,
                                                                             const int* __restrict__ groups) {
     constexpr int FP_GA = NWARP * FP_APW;       // angles per CTA (they share each staged band)
+    constexpr int FP2_P = SP, FP_U = SU;
+    constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16, FP2_CPT2 = (FP2_P / 2 + 15) / 16;
     extern __shared__ float4 smf4[];
     float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][FP2_P] (S, D), entry 0 = pixel -PADL
     float* sacc = reinterpret_cast<float*>(sd + FP2_BL * FP2_P);  // [FP_GA][32 * FP_U] per-ray accumulators
@@ -292,10 +298,10 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
                 const unsigned rowbase = sbase + 8u * (unsigned)(ib - MAGICI);
                 float v;
                 if (__all_sync(0xffffffffu, safe)) {
-                    v = fp2_band_ray<false>(rowbase, f0, Bu, 0.f, 0.f);
+                    v = fp2_band_ray<false, FP2_P>(rowbase, f0, Bu, 0.f, 0.f);
                 } else {
                     const float lo = (float)(-3 - ib) - 0.5f, hi = (float)(T + 2 - ib) - 0.5f;
-                    v = fp2_band_ray<true>(rowbase, f0, Bu, lo, hi);
+                    v = fp2_band_ray<true, FP2_P>(rowbase, f0, Bu, lo, hi);
                 }
                 if (ray) acc[w] += v;
             }

@@ -99,6 +99,16 @@ CONFIGS = {
     # ROI-lambda solves), scored by MSE and SSIM against the ground truth.
     "L1": Config(7, "L1", 512, 64, math.pi, 725, "poisson", 1e4, 64, 32, 32,
                  "sweep", 200, "tv", 0.05, 100, 16, 0),
+    # The paper's own local-part experiment (PAPER.md L845-849, L874-875,
+    # L796-798): 1024^2 grid, 1024 detector pixels (1025: odd, reading A3; the
+    # phantom lies inside the inscribed disc, so no data are truncated), 512
+    # angles on [0, pi), Poisson noise (I0 = 1e4: the paper varies it), one
+    # central 256^2 local part padded by 1/8 of its size on each side
+    # (margin 32, extended side 320), FISTA-TV, 200 x 100 FGP
+    # iterations; piecewise-constant ellipses and rectangles stand in for the
+    # motor phantom (not distributed).
+    "P1": Config(8, "P1", 1024, 512, math.pi, 1025, "poisson", 1e4, 1, 128, 32,
+                 "centre", 200, "tv", 0.05, 100, 25, 25),
 }
 
 SWEEP_ROIS, SWEEP_LAMBDAS = 4, 16

@@ -228,3 +228,14 @@ def test_library_slot_table_matches_partition(lt, world):
         for g, q in enumerate(plans):
             blk = tab[g * spr:(g + 1) * spr]
             assert np.array_equal(blk[:q.R], q.local_rois) and np.all(blk[q.R:] == -1)
+
+
+def test_tv_accepts_extended_sides_up_to_320(lt):
+    """The FGP kernels take extended ROIs up to 320 x 320 (the paper's 256^2 local
+    parts with 1/8 padding per side); wider is error 2 (host check)."""
+    ang = synth.angles_for(8)
+    ok = lt.Plan(1024, ang, 1449, [[512, 512]], 128, 32, 2, bind=False)
+    assert ok.h == 160
+    assert lt._lib.lt_fgp_batch(320, 320, 0, None, 0.1, 10, None, None) == 0
+    assert lt._lib.lt_fgp_batch(321, 320, 1, None, 0.1, 10, None, None) == 2
+    assert lt._lib.lt_fgp_batch(300, 321, 1, None, 0.1, 10, None, None) == 2
