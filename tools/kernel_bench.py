@@ -9,7 +9,8 @@ import paper_1604_02292_b200 as lt
 cfg = synth.config(sys.argv[1] if len(sys.argv) > 1 else "C4")
 inp = synth.make_inputs(cfg, noise=True)
 n_iter = int(os.environ.get('KB_NITER', '6'))
-plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter)
+plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter,
+               rank=int(os.environ.get('KB_RANK', '0')), world=int(os.environ.get('KB_WORLD', '1')))
 plan.filter_bank()
 sino = torch.from_numpy(inp.sino).cuda()
 plan.tv_solve(sino, cfg.lam, cfg.n_fgp)

@@ -9,10 +9,11 @@ import torch
 import synth
 import paper_1604_02292_b200 as lt
 cfg = synth.config(sys.argv[1] if len(sys.argv) > 1 else "C4")
+worlds = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 4, 8]
 inp = synth.make_inputs(cfg)
 sino = torch.from_numpy(inp.sino).cuda()
 bank = None
-for world in (1, 2, 4, 8):
+for world in worlds:
     times = []
     for rank in range(world):
         plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, cfg.n_iter,
