@@ -451,11 +451,13 @@ def run_ours(args, cfg):
     c_sum = float(np.sum(np.maximum(np.abs(np.cos(inp.angles)), np.abs(np.sin(inp.angles)))))
     fp_steps = c_sum * Ptot_local
     traffic_all = {}
-    try:   # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            traffic_all = json.load(f)
-    except Exception:
-        traffic_all = {}
+    for rnd in ("r02", "r01"):   # dram__bytes_read.sum + dram__bytes_write.sum per launch, latest committed ncu capture
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                traffic_all = json.load(f)
+            break
+        except Exception:
+            traffic_all = {}
 
     def roofline_of(cls):
         """Roofline entry of one main-stream kernel class."""

@@ -326,7 +326,9 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
     }
     // 16 angles per CTA share each staged band; 8 when that would leave the
     // SMs short of two waves (small ROI batches: C1-C3, T1, 8-GPU shards)
-    const bool one = (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
+    static int one_env = -2;
+    if (one_env == -2) { const char* e = getenv("LT_FP_ONE"); one_env = e ? atoi(e) : -1; }   // diagnostics: 0 / 1 force
+    const bool one = one_env >= 0 ? one_env == 1 : (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
     const int apw = one ? 1 : 2;
     const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1, p.a_lo, p.a_hi};
@@ -352,7 +354,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         } else {
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
         }
-    } else if (fp_wide() && (long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms &&
+    } else if (fp_wide() && ((long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms || one_env == 0) &&
                p.ngroups24 * 24 <= p.ngroups * 16) {
         // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM),
         // unless the 24-angle groups pad more (C5: 128 angles per orientation = 5 1/3 x 24)

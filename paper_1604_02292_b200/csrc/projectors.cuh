@@ -130,12 +130,14 @@ constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16;  // float4 chunks per thread per 
 #endif
 constexpr int FP2_CPT2 = (FP2_P / 2 + 15) / 16; // float2 chunks per thread per band (FP_STAGE64)
 
+#ifndef FP_PIPE
+#define FP_PIPE 1      // the loads of the next line pair issued before the current pair is consumed
+#endif                 // (C4 FP 1.427 -> 1.417 ms, bitwise identical; ray addresses by mad.lo: no change)
 template <bool CLAMP, int SP = FP2_P>
 __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
     const unsigned rowbase = __shfl_sync(0xffffffffu, rowbase_, threadIdx.x & 31);
     float acc = 0.f;
-    #pragma unroll
-    for (int i = 0; i < FP2_BL; i += 2) {
+    auto addr_g = [&](int i, unsigned& a0, unsigned& a1, float2& g) {
         float2 tt = make_float2(fmaf((float)i, Bf, f0), fmaf((float)(i + 1), Bf, f0));   // immediates
         if (CLAMP) {
             tt.x = fminf(fmaxf(tt.x, lo), hi);
@@ -143,16 +145,44 @@ __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float
         }
         const float2 rm = __fadd2_rn(tt, make_float2(MAGICF, MAGICF));           // round(tt) in the low bits
         const float2 k2 = __ffma2_rn(rm, make_float2(-2.f, -2.f), make_float2(2.f * MAGICF, 2.f * MAGICF));   // -2 round(tt)
-        const float2 g = __ffma2_rn(tt, make_float2(2.f, 2.f), k2);             // 2 (tt - round(tt)) in [-1, 1]
-        // (shift + add: LEA on the ALU pipe, not IMAD on the FMA pipe)
-        const unsigned a0 = rowbase + ((unsigned)__float_as_int(rm.x) << 3);
-        const unsigned a1 = rowbase + ((unsigned)__float_as_int(rm.y) << 3);
+        g = __ffma2_rn(tt, make_float2(2.f, 2.f), k2);                          // 2 (tt - round(tt)) in [-1, 1]
+        a0 = rowbase + ((unsigned)__float_as_int(rm.x) << 3);
+        a1 = rowbase + ((unsigned)__float_as_int(rm.y) << 3);
+    };
+#if FP_PIPE
+    unsigned a0, a1;
+    float2 g;
+    addr_g(0, a0, a1, g);
+    float s0, d0, s1, d1;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s0), "=f"(d0) : "r"(a0));
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s1), "=f"(d1) : "r"(a1 + (unsigned)(SP * 8)));
+    #pragma unroll
+    for (int i = 0; i < FP2_BL; i += 2) {
+        float ns0 = 0.f, nd0 = 0.f, ns1 = 0.f, nd1 = 0.f;
+        float2 ng = g;
+        if (i + 2 < FP2_BL) {
+            unsigned b0, b1;
+            addr_g(i + 2, b0, b1, ng);
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(ns0), "=f"(nd0) : "r"(b0 + (unsigned)((i + 2) * SP * 8)));
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(ns1), "=f"(nd1) : "r"(b1 + (unsigned)((i + 3) * SP * 8)));
+        }
+        acc = fmaf(g.x, d0, acc + s0);
+        acc = fmaf(g.y, d1, acc + s1);
+        s0 = ns0; d0 = nd0; s1 = ns1; d1 = nd1; g = ng;
+    }
+#else
+    #pragma unroll
+    for (int i = 0; i < FP2_BL; i += 2) {
+        unsigned a0, a1;
+        float2 g;
+        addr_g(i, a0, a1, g);
         float s0, d0, s1, d1;
         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s0), "=f"(d0) : "r"(a0 + (unsigned)(i * SP * 8)));
         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(s1), "=f"(d1) : "r"(a1 + (unsigned)((i + 1) * SP * 8)));
         acc = fmaf(g.x, d0, acc + s0);
         acc = fmaf(g.y, d1, acc + s1);
     }
+#endif
     return acc;
 }
 

@@ -4,4 +4,4 @@
 name=$1; shift
 mkdir -p /tmp/lt_ab
 /usr/local/cuda/bin/nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -shared \
-  "$@" -I include -o /tmp/lt_ab/$name.so paper_1604_02292_b200/csrc/loctomo.cu -lcufft -Xlinker -rpath=/usr/local/cuda/lib64
+  "$@" -I include -o /tmp/lt_ab/$name.so paper_1604_02292_b200/csrc/loctomo.cu -lcufft -Xlinker -rpath=/usr/local/cuda/lib64 > /tmp/lt_ab/$name.log 2>&1 || { echo "variant $name failed"; tail -5 /tmp/lt_ab/$name.log; }
