@@ -60,8 +60,8 @@ def test_random_geometry(lt, orc, seed):
     cfg, cen = _case(seed)
     inp = synth.make_inputs(cfg)
     h = cfg.radius + cfg.margin
-    if 2 * h > 256 and cfg.solver == "tv":
-        pytest.skip("FGP tiles are limited to 256 x 256")
+    if 2 * h > 320 and cfg.solver == "tv":
+        pytest.skip("FGP tiles are limited to 320 x 320")
     plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
     plan.filter_bank()
     sino = torch.from_numpy(inp.sino).cuda()
@@ -105,3 +105,33 @@ def test_random_geometry_large_batch(lt, orc, seed):
     for k, g in enumerate(sample):
         q = int(np.nonzero(plan.local_rois == g)[0][0])
         assert relerr(got[q], ref[k]) <= 1e-3, (cfg, int(g))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("LT_FUZZ_WIDE", "8"))))
+def test_random_geometry_wide_tiles(lt, orc, seed):
+    """Extended sides of 258..320 px (the 10-columns-per-lane FGP, the wide
+    forward projector), central and clipped ROIs, box or TV, on random
+    geometries against the oracle."""
+    rng = np.random.default_rng(3000 + seed)
+    n = int(rng.integers(300, 641))
+    na = int(rng.integers(16, 97))
+    nd = int(math.ceil(math.sqrt(2) * n)) | 1
+    side = int(rng.integers(129, 161))                      # extended half-side h in (128, 160]
+    radius = int(rng.integers(max(1, side - 64), min(side, n // 2) + 1))
+    margin = side - radius
+    n_roi = int(rng.integers(1, 4))
+    cen = np.stack([rng.integers(radius, n - radius + 1, size=n_roi),
+                    rng.integers(radius, n - radius + 1, size=n_roi)], axis=1).astype(np.int32)
+    mode = "tv" if seed % 2 == 0 else "box"
+    cfg = synth.Config(90 + seed, f"fuzzW{seed}", n, na, math.pi, nd, "gauss", 0.01, n_roi, radius, margin, "seeded",
+                       int(rng.integers(1, 4)), mode, 0.05, int(rng.integers(5, 21)), 6, 2)
+    inp = synth.make_inputs(cfg)
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, cen, cfg.radius, cfg.margin, cfg.n_iter)
+    assert 2 * plan.h > 256
+    plan.filter_bank()
+    sino = torch.from_numpy(inp.sino).cuda()
+    got = (plan.tv_solve(sino, cfg.lam, cfg.n_fgp) if mode == "tv" else plan.sirt_solve(sino, 0.0, math.inf)).cpu().numpy()
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, cen, cfg.radius, cfg.margin, cfg.n_iter,
+                       mode=mode, lam=cfg.lam, n_fgp=cfg.n_fgp)
+    for q, g in enumerate(plan.local_rois):
+        assert relerr(got[q], ref[g]) <= 1e-3, (cfg, int(g))
