@@ -53,8 +53,9 @@ def parse():
     ap.add_argument("--prior", default="config", choices=["config", "haar", "exterior"],
                     help="haar: NEXT-2 Haar-wavelet l1 prior (FISTA, 4 levels, lambda 0.02) instead of the config's; "
                          "exterior: NEXT-4(ii) exterior-subtraction box-SIRT (the prior art) for comparison")
-    ap.add_argument("--combine", default="peer", choices=["peer", "nccl"],
-                    help="N > 1: stitch reading the peers' cores over NVLink (CUDA IPC, one kernel) or NCCL all-gather + stitch")
+    ap.add_argument("--combine", default="peer", choices=["peer", "nccl", "library"],
+                    help="N > 1: stitch reading the peers' cores over NVLink (CUDA IPC, one kernel), torch's NCCL "
+                         "all-gather + stitch, or the library-owned lt_combine_rois (its own NCCL communicator)")
     ap.add_argument("--bank", default="local", choices=["local", "split"],
                     help="N > 1: every rank computes the whole filter bank (no communication), or the "
                          "angle-split cold bank (rank g owns N_theta/N angles, NCCL all-reduce of the N x N "
@@ -231,11 +232,26 @@ def run_ours(args, cfg):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    torch.cuda.set_device(local_rank)
+    # LT_BENCH_FUNCTIONAL=1: every rank on cuda:0 with gloo -- a functional check of
+    # the N > 1 code path (partition, slot tables, peer / library combine, max-over-
+    # ranks timing) on a one-GPU box; its timings are NOT measurements
+    functional = os.environ.get("LT_BENCH_FUNCTIONAL") == "1"
+    dev_index = 0 if functional else local_rank
+    torch.cuda.set_device(dev_index)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    red_dev = "cpu" if functional else "cuda"     # gloo reduces host tensors
+
+    def allreduce(vals, op_max=True, dtype=None):
+        t = torch.tensor(vals, device=red_dev, dtype=dtype or torch.float32)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op_max else dist.ReduceOp.SUM)
+        return [float(v) for v in t.cpu()]
+
     inp = synth.make_inputs(cfg)
     n_iter = cfg.n_iter
     mode = solve_mode(cfg, args)
@@ -269,6 +285,9 @@ def run_ours(args, cfg):
     image = torch.empty(cfg.n, cfg.n, device="cuda")
     gathered = torch.empty(world * spr, side, side, device="cuda") if world > 1 else None
     peer = None
+    ncomm = None
+    if world > 1 and args.combine == "library" and not functional:
+        ncomm = lt.NcclComm.from_process_group()
     if world > 1 and args.combine == "peer":
         try:
             peer = ltd.PeerCombine(plan, cores, slot_roi, spr)
@@ -308,6 +327,8 @@ def run_ours(args, cfg):
     def combine_step():
         if peer is not None:
             peer.combine(image)                            # stitch reading the peers' cores over NVLink
+        elif ncomm is not None:
+            plan.combine_rois(cores[:plan.R], ncomm, out=image)   # lt_combine_rois: in-place ncclAllGather + stitch
         elif world > 1:
             ltd.gather_cores(cores, out=gathered)          # NCCL all-gather over NVLink
             plan.combine(gathered, slot_roi, out=image)
@@ -368,14 +389,10 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         combine_ms = ec0.elapsed_time(ec1) / 5
         if dist:
-            t = torch.tensor([combine_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            combine_ms = float(t.item())
+            combine_ms = allreduce([combine_ms])[0]
     clk = clocks.stop()
     if dist:
-        t = torch.tensor([elapsed_ms, instr_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, instr_ms = float(t[0].item()), float(t[1].item())
+        elapsed_ms, instr_ms = allreduce([elapsed_ms, instr_ms])
 
     # e2e: same step through the host-buffer C-ABI entry (pinned H2D + solve + combine + D2H)
     image_host = torch.empty(cfg.n, cfg.n, dtype=torch.float32).pin_memory()
@@ -409,23 +426,26 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
     if dist:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = allreduce([e2e_ms])[0]
 
     # global counts
     upd_local, fgp_local, Ptot_local = algorithmic_counts(cfg, rects, n_iter)
     exe_local = executed_updates(cfg, rects, n_iter) if not args.xs_exact and mode in ("tv", "sirt", "haar") else None
     if dist:
-        t = torch.tensor([upd_local, fgp_local, exe_local or 0.0], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t)
-        upd, fgp_pi, exe = float(t[0]), float(t[1]), (float(t[2]) if exe_local is not None else None)
+        upd, fgp_pi, exe_sum = allreduce([upd_local, fgp_local, exe_local or 0.0], op_max=False, dtype=torch.float64)
+        exe = exe_sum if exe_local is not None else None
     else:
         upd, fgp_pi, exe = upd_local, fgp_local, exe_local
     ms_per_step = elapsed_ms / args.steps
     value = cfg.n_roi / (ms_per_step / 1e3)
     if rank != 0:
         if dist:
+            if peer is not None:
+                dist.barrier()
+                peer.close()
+                dist.barrier()
+            if ncomm is not None:
+                ncomm.close()
             dist.destroy_process_group()
         return None
 
@@ -526,6 +546,7 @@ def run_ours(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(cfg, args, world),
         "combine": ("peer-memory stitch (CUDA IPC over NVLink, one kernel)" if peer is not None else
+                    "lt_combine_rois (library-owned NCCL all-gather + stitch)" if ncomm is not None else
                     "NCCL all-gather + stitch" if world > 1 else "local stitch"),
         "gray_s": round(upd / (ms_per_step / 1e3) / 1e9, 2),
         "gray_s_note": "method-defined count: N_theta P (1 + 3 (n-1)) per ROI; gray_s_executed counts what the "
@@ -553,6 +574,12 @@ def run_ours(args, cfg):
     }
     print(json.dumps(line), flush=True)
     if dist:
+        if peer is not None:        # unmap the peers' buffers before any rank frees its own
+            dist.barrier()
+            peer.close()
+            dist.barrier()
+        if ncomm is not None:
+            ncomm.close()
         dist.destroy_process_group()
     return line
 
