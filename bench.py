@@ -640,8 +640,17 @@ def oracle_sample(cfg, n_iter_sample=2, n_conv_k=1, n_rois=16, mode=None):
 def cpu_baseline(cfg, budget_s=20.0, mode=None):
     try:
         v, sample, cores = oracle_sample(cfg, mode=mode)
-        return {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-                "nproc": os.cpu_count(), "cpu_model": cpu_model()}
+        out = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "nproc": os.cpu_count(), "cpu_model": cpu_model()}
+        if cfg.n <= 512:        # small configs also single-threaded
+            import oracle
+            oracle.set_threads(1)
+            try:
+                v1, _, _ = oracle_sample(cfg, mode=mode)
+            finally:
+                oracle.set_threads(cores)
+            out["single_thread_value"] = round(v1, 6)
+        return out
     except Exception as e:  # report, never fake
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
 
