@@ -5,6 +5,7 @@
 #include "kernels.cuh"
 
 #include <cufft.h>
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -74,6 +75,13 @@ cudaEvent_t ev_get() {
     cudaEventCreate(&e);
     return e;
 }
+// NVTX ranges around the library's phases (header-only NVTX v3: a no-op
+// unless a profiler is attached) -- SURVEY §5 tracing
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct ScopedTimer {
     int cls; cudaStream_t st; cudaEvent_t a = nullptr;
     ScopedTimer(int c, cudaStream_t s) : cls(c), st(s) {
@@ -623,6 +631,7 @@ int ensure_wd(lt_plan& p, cudaStream_t st) {
 }
 
 int disc_correct(lt_plan& p, const float* d_sino, float* d_pc, float* d_cuser, cudaStream_t st) {
+    NvtxRange nv("lt/disc");
     if (int rc = ensure_wd(p, st)) return rc;
     k_rowsum<<<p.na, 256, 0, st>>>(p.nd, d_sino, p.P<double>(p.off.psum));
     LT_LAUNCHED();
@@ -967,6 +976,7 @@ int run_local(lt_plan& p, int mode, float lo, float hi, float lam, int nfgp, con
 }
 
 int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfgp, float* d_cores, cudaStream_t st) {
+    NvtxRange nv(mode == 0 ? "lt/sirt_solve" : mode == 1 ? "lt/tv_solve" : "lt/haar_solve");
     float* pc = p.P<float>(p.off.pc);
     if (p.flags & LT_XS_EXACT) {
         LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.discc32), 0, sizeof(float), st));
@@ -976,15 +986,21 @@ int solve(lt_plan& p, int mode, const float* d_sino, float a0, float a1, int nfg
         LT_CUDA(cudaMemcpyAsync(pc, d_sino, (size_t)p.na * p.nd * sizeof(float), cudaMemcpyDeviceToDevice, st));
         LT_CUDA(cudaMemsetAsync(p.P<float>(p.off.discc32), 0, sizeof(float), st));
     }
-    if (!(p.flags & LT_XS_EXACT))
+    if (!(p.flags & LT_XS_EXACT)) {
+        NvtxRange nc("lt/conv_cache");
         if (int rc = conv_cache(p, pc, st)) return rc;
-    if (int rc = run_local(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode != 0 ? a0 : 0.f, nfgp, d_sino, st))
-        return rc;
+    }
+    {
+        NvtxRange ni("lt/iterations");
+        if (int rc = run_local(p, mode, mode == 0 ? a0 : 0.f, mode == 0 ? a1 : 0.f, mode != 0 ? a0 : 0.f, nfgp, d_sino, st))
+            return rc;
+    }
     return crop_cores(p, d_cores, st);
 }
 
 int combine(const lt_plan& p, const float* d_cores, int n_slots, const int* slot_roi, float* d_image, cudaStream_t st,
             const float* const* h_peers = nullptr, int world = 0, int spr = 1) {
+    NvtxRange nv("lt/combine");
     const int side = 2 * p.radius;
     const int nb = (p.n + 31) / 32;
     std::vector<std::vector<std::pair<int, int>>> buckets((size_t)nb * nb);
@@ -1421,6 +1437,7 @@ int lt_plan_tables(const lt_plan* p, int32_t* rects, int32_t* d0, int32_t* wwin)
 
 int lt_filter_bank(lt_plan* p, void* stream) {
     if (int rc = check_plan(p)) return rc;
+    NvtxRange nv("lt/filter_bank");
     cudaStream_t st = (cudaStream_t)stream;
     if (int rc = ensure_wd(*p, st)) return rc;
     // Alg. 1: c = e_c; for k: v = W c; u_k = u_{k-1} + alpha v; c <- c - alpha W^T v
