@@ -558,13 +558,11 @@ int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clu
     return LT_OK;
 }
 
-template <int MODE>
-int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
-    if (int rc = fgp_check(rows, cols)) return rc;
-    if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
-    // wide tiles (257..320 columns or rows): 10 columns per lane, 3 rows per warp,
-    // 24-row CTAs (clusters of up to 14 CTAs)
-    if (rows > FGP2_ROW || cols > FGP2_ROW) return launch_fgp2_t<MODE, 3, 8, false, false, 5>(A, rows, ntiles, st);
+// tiles up to 256 columns: CP = 2 / 3 / 4 column pairs per lane for tiles up to
+// 128 / 192 / 256 columns (narrow tiles use all 32 lanes: half the work per
+// warp of the 256-wide layout on a 128-wide tile)
+template <int MODE, int CP>
+int launch_fgp_cp(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     static int cfgv = -1;
     if (cfgv < 0) {
         const char* e = getenv("LT_FGP2_CFG");
@@ -584,8 +582,8 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
         int* c4 = c4_dev[dv];
         const int key = (rows + 15) / 16;
         if (!c2[key]) {
-            launch_fgp2_t<MODE, 2, 8>(A, rows, 1, st, &c2[key]);
-            launch_fgp2_t<MODE, 4, 8>(A, rows, 1, st, &c4[key]);
+            launch_fgp2_t<MODE, 2, 8, false, false, CP>(A, rows, 1, st, &c2[key]);
+            launch_fgp2_t<MODE, 4, 8, false, false, CP>(A, rows, 1, st, &c4[key]);
             if (c2[key] <= 0) c2[key] = -1;
             if (c4[key] <= 0) c4[key] = -1;
         }
@@ -595,20 +593,36 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
             use16 = w2 * 52 < w4 * 73;
         }
     }
-    if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
-    static int persist_env = -1;
-    if (persist_env < 0) { const char* e = getenv("LT_FGP_PERSIST"); persist_env = !(e && atoi(e) == 0); }
-    // persistent 8-CTA clusters (default): only the co-resident clusters are
-    // launched and each walks its tiles, prefetching the next tile's b, x_prev
-    // and x_s during the current one; the SMs the clusters cannot use stay free
-    // for the side-stream x_s backprojection for the whole FGP (C4 318 -> 331)
-    if (cfgv == 1 || use16) return launch_fgp2_t<MODE, 2, 8>(A, rows, ntiles, st);
-    if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, true>(A, rows, ntiles, st);
-    if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, true>(A, rows, ntiles, st);
-    // (many waves only: at C3's 64 tiles = 2.8 waves the dynamic wave scheduling does as well)
-    if (persist_env && clusters8 > 0 && ntiles > 3 * clusters8)
-        return launch_fgp2_t<MODE, 4, 8, false, true>(A, rows, ntiles, st);
-    return launch_fgp2_t<MODE, 4, 8>(A, rows, ntiles, st);
+    if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8, false, false, CP>(A, rows, ntiles, st);
+    if (cfgv == 1 || use16) return launch_fgp2_t<MODE, 2, 8, false, false, CP>(A, rows, ntiles, st);
+    if constexpr (CP == 4) {
+        static int persist_env = -1;
+        if (persist_env < 0) { const char* e = getenv("LT_FGP_PERSIST"); persist_env = !(e && atoi(e) == 0); }
+        if (cfgv == 2) return launch_fgp2_t<MODE, 2, 8, true>(A, rows, ntiles, st);
+        if (cfgv == 3) return launch_fgp2_t<MODE, 2, 16, true>(A, rows, ntiles, st);
+        // persistent 8-CTA clusters (many waves): only the co-resident clusters are
+        // launched and each walks its tiles, prefetching the next tile's b, x_prev
+        // and x_s during the current one; the SMs the clusters cannot use stay free
+        // for the side-stream x_s backprojection for the whole FGP (C4 318 -> 331)
+        // (at C3's 64 tiles = 2.8 waves the dynamic wave scheduling does as well)
+        if (persist_env && clusters8 > 0 && ntiles > 3 * clusters8)
+            return launch_fgp2_t<MODE, 4, 8, false, true>(A, rows, ntiles, st);
+    }
+    return launch_fgp2_t<MODE, 4, 8, false, false, CP>(A, rows, ntiles, st);
+}
+
+template <int MODE>
+int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
+    if (int rc = fgp_check(rows, cols)) return rc;
+    if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
+    // wide tiles (257..320 columns or rows): 10 columns per lane, 3 rows per warp,
+    // 24-row CTAs (clusters of up to 14 CTAs)
+    if (rows > FGP2_ROW || cols > FGP2_ROW) return launch_fgp2_t<MODE, 3, 8, false, false, 5>(A, rows, ntiles, st);
+    static int narrow_env = -1;
+    if (narrow_env < 0) { const char* e = getenv("LT_FGP_NARROW"); narrow_env = !(e && atoi(e) == 0); }
+    if (narrow_env && cols <= 128) return launch_fgp_cp<MODE, 2>(A, rows, ntiles, st);
+    if (narrow_env && cols <= 192) return launch_fgp_cp<MODE, 3>(A, rows, ntiles, st);
+    return launch_fgp_cp<MODE, 4>(A, rows, ntiles, st);
 }
 
 dim3 grid2d(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }
