@@ -280,7 +280,7 @@ __device__ __forceinline__ void st_cols(float* dst, const float* v, int x0, int 
 template <int MODE, int FR, int NW, bool BSM, bool PERSIST = false, int CP = 4>
 __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpArgs A) {
     static_assert(!(PERSIST && BSM), "persistent launch keeps b in registers");
-    static_assert(CP >= 2 && CP <= 5, "128-, 192-, 256- or 320-wide tiles");
+    static_assert(CP >= 1 && CP <= 5, "64-, 128-, 192-, 256- or 320-wide tiles");
     using SM = Fgp2Smem<FR, NW, CP>;
     constexpr int ROW = SM::ROW;
     constexpr int NC = 2 * CP;                  // columns per lane

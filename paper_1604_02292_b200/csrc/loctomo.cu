@@ -558,9 +558,9 @@ int launch_fgp2_t(FgpArgs A, int rows, int ntiles, cudaStream_t st, int* max_clu
     return LT_OK;
 }
 
-// tiles up to 256 columns: CP = 2 / 3 / 4 column pairs per lane for tiles up to
-// 128 / 192 / 256 columns (narrow tiles use all 32 lanes: half the work per
-// warp of the 256-wide layout on a 128-wide tile)
+// tiles up to 256 columns: CP = 1 / 2 / 3 / 4 column pairs per lane for tiles up
+// to 64 / 128 / 192 / 256 columns (narrow tiles use all 32 lanes: half the work
+// per warp of the 256-wide layout on a 128-wide tile)
 template <int MODE, int CP>
 int launch_fgp_cp(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
     static int cfgv = -1;
@@ -620,6 +620,7 @@ int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     if (rows > FGP2_ROW || cols > FGP2_ROW) return launch_fgp2_t<MODE, 3, 8, false, false, 5>(A, rows, ntiles, st);
     static int narrow_env = -1;
     if (narrow_env < 0) { const char* e = getenv("LT_FGP_NARROW"); narrow_env = !(e && atoi(e) == 0); }
+    if (narrow_env && cols <= 64) return launch_fgp_cp<MODE, 1>(A, rows, ntiles, st);
     if (narrow_env && cols <= 128) return launch_fgp_cp<MODE, 2>(A, rows, ntiles, st);
     if (narrow_env && cols <= 192) return launch_fgp_cp<MODE, 3>(A, rows, ntiles, st);
     return launch_fgp_cp<MODE, 4>(A, rows, ntiles, st);
