@@ -615,9 +615,16 @@ template <int MODE>
 int launch_fgp(FgpArgs A, int rows, int cols, int ntiles, cudaStream_t st) {
     if (int rc = fgp_check(rows, cols)) return rc;
     if (int rc = ensure_fgp_beta(A.nfgp, st)) return rc;
-    // wide tiles (257..320 columns or rows): 10 columns per lane, 3 rows per warp,
-    // 24-row CTAs (clusters of up to 14 CTAs)
-    if (rows > FGP2_ROW || cols > FGP2_ROW) return launch_fgp2_t<MODE, 3, 8, false, false, 5>(A, rows, ntiles, st);
+    // wide tiles (257..320 columns or rows): 10 columns per lane, 2 rows per warp,
+    // 10 warps: 20-row CTAs (clusters of up to 16 CTAs); P1 FGP 83 -> 79 us per
+    // launch against 3 rows x 8 warps (24-row CTAs, 14-CTA clusters), which
+    // LT_FGP_WIDE_CFG=3x8 keeps
+    if (rows > FGP2_ROW || cols > FGP2_ROW) {
+        static int w_env = -1;
+        if (w_env < 0) { const char* e = getenv("LT_FGP_WIDE_CFG"); w_env = (e && !strcmp(e, "3x8")) ? 1 : 0; }
+        if (w_env == 1) return launch_fgp2_t<MODE, 3, 8, false, false, 5>(A, rows, ntiles, st);
+        return launch_fgp2_t<MODE, 2, 10, false, false, 5>(A, rows, ntiles, st);
+    }
     static int narrow_env = -1;
     if (narrow_env < 0) { const char* e = getenv("LT_FGP_NARROW"); narrow_env = !(e && atoi(e) == 0); }
     if (narrow_env && cols <= 64) return launch_fgp_cp<MODE, 1>(A, rows, ntiles, st);
