@@ -532,9 +532,13 @@ def run_ours(args, cfg):
     rooflines = {c: v for c, v in rooflines.items() if v is not None}
     # dominant kernel class over the timed region (rank 0's main stream; the x_s
     # backprojection "xs" runs on a side stream, overlapped: reported per class only)
-    dom = max(rooflines, key=lambda c: ktimes[c][0])
-    roofline = {k: rooflines[dom][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
-    roofline.update({k: v for k, v in rooflines[dom].items() if k not in roofline})
+    if rooflines:
+        dom = max(rooflines, key=lambda c: ktimes[c][0])
+        roofline = {k: rooflines[dom][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+        roofline.update({k: v for k, v in rooflines[dom].items() if k not in roofline})
+    else:   # (N > 1 with fewer ROIs than ranks: rank 0 may own none and launch no roofline kernel)
+        roofline = {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
+                    "note": "rank 0 launched none of the roofline kernels (it owns no ROI)"}
     kshare = {k: {"ms_per_step": round(v[0] / args.steps, 3), "launches_per_step": v[1] // args.steps}
               for k, v in ktimes.items()}
     cpu = None
