@@ -3,7 +3,7 @@
 set -u
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/final_build.log 2>&1 || { echo BUILD FAILED; exit 1; }
-LT_PARITY_REPORT=gpurun_out/final_parity.jsonl timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/final_pytest_gpu.log 2>&1
+LT_PARITY_REPORT=gpurun_out/final_parity.jsonl timeout 2400 python -m pytest tests -m gpu -q ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/final_pytest_gpu.log 2>&1
 echo "pytest rc=$?"; tail -2 gpurun_out/final_pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/final_smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/final_bench_C4.json 2> gpurun_out/final_bench_C4.err; echo "bench C4 rc=$?"
