@@ -1209,16 +1209,41 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
         // tile centre point (x, y) = (cc - N/2, N/2 - cr)
         tile_window(*p, cc - 0.5 * n, 0.5 * n - cr, p->Wwin, &p->d0[(size_t)q * n_angles], &p->tauc[(size_t)q * n_angles]);
     }
-    // forward-projection angle groups (16 and 8 angles): one orientation per group
+    // forward-projection angle groups (16, 8 and 24 angles): one orientation per
+    // group.  Balanced (default; LT_FP_BALANCE=0: consecutive angles): an angle's
+    // work per band is ~ the rays crossing it, T c_a + 16 s_a (c_a = max(|cos|,
+    // |sin|), s_a = min); the orientation's angles sorted by it are paired
+    // largest-with-smallest for the two-angles-per-warp groups (every warp of a
+    // CTA then reaches the band barrier with about the same work) and kept in
+    // sorted order for the one-angle-per-warp groups
+    static int bal_env = -1;
+    if (bal_env < 0) { const char* e = getenv("LT_FP_BALANCE"); bal_env = !(e && atoi(e) == 0); }
     for (int ga : {16, 8, 24}) {
         std::vector<int>& grp = ga == 16 ? p->fpgroups : ga == 8 ? p->fpgroups1 : p->fpgroups24;
         for (int o = 0; o < 2; ++o) {
-            std::vector<int> cur;
+            std::vector<int> lst;
             for (int a = 0; a < n_angles; ++a)
-                if (p->angf[a].col == o) {
-                    cur.push_back(a);
-                    if ((int)cur.size() == ga) { grp.insert(grp.end(), cur.begin(), cur.end()); cur.clear(); }
+                if (p->angf[a].col == o) lst.push_back(a);
+            if (bal_env) {
+                auto work = [&](int a) {
+                    const double c = std::fabs(p->cs64[a]), sv = std::fabs(p->sn64[a]);
+                    return (double)p->T * std::max(c, sv) + 16.0 * std::min(c, sv);
+                };
+                std::stable_sort(lst.begin(), lst.end(), [&](int x, int y) { return work(x) > work(y); });
+                if (ga != 8) {   // pairs (largest, smallest), then the pairs in order
+                    std::vector<int> pr;
+                    for (size_t i = 0, j = lst.size(); i < j; ) {
+                        pr.push_back(lst[i++]);
+                        if (i < j) pr.push_back(lst[--j]);
+                    }
+                    lst.swap(pr);
                 }
+            }
+            std::vector<int> cur;
+            for (int a : lst) {
+                cur.push_back(a);
+                if ((int)cur.size() == ga) { grp.insert(grp.end(), cur.begin(), cur.end()); cur.clear(); }
+            }
             if (!cur.empty()) {
                 cur.resize(ga, -1);
                 grp.insert(grp.end(), cur.begin(), cur.end());
