@@ -217,22 +217,23 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
     for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += NWARP * 32) sacc[e] = 0.f;
 
-    // staging map (no division): thread = (line tid / 16, chunks c4 = tid % 16 + 16 u);
-    // threads 256.. of a 12-warp CTA do not stage
     const int q4 = TP / 4;                        // float4 chunks per raw line
     const int q2 = TP / 2;                        // float2 chunks per raw line
-    const int sline = threadIdx.x >> 4, sc0 = threadIdx.x & 15;
 #if FP_STAGE64
-    // thread = (line tid / 16, pixel pairs c2 = tid % 16 + 16 u): entry pair (2 c2, 2 c2 + 1)
-    // is one 16-byte store and the 16 threads of a line write 256 contiguous bytes
-    float2 raw[FP2_CPT2];
-    float nxt[FP2_CPT2];
+    // every thread stages: TPL = (threads / 16) threads per line (16 or 24),
+    // thread = (line tid / TPL, pixel pairs c2 = tid % TPL + TPL u): entry pair
+    // (2 c2, 2 c2 + 1) is one 16-byte store, a line's threads write contiguous bytes
+    constexpr int TPL = NWARP * 32 / FP2_BL;
+    constexpr int CPT2 = (FP2_P / 2 + TPL - 1) / TPL;
+    const int sline = (int)threadIdx.x / TPL, sc0 = (int)threadIdx.x - sline * TPL;
+    float2 raw[CPT2];
+    float nxt[CPT2];
     auto fetch = [&](int l0) {
         const bool lok = sline < FP2_BL && l0 + sline < T;
         const float* rp0 = src + (long long)(l0 + sline) * TP;
         #pragma unroll
-        for (int u = 0; u < FP2_CPT2; ++u) {
-            const int c2 = sc0 + 16 * u;
+        for (int u = 0; u < CPT2; ++u) {
+            const int c2 = sc0 + TPL * u;
             raw[u] = make_float2(0.f, 0.f);
             nxt[u] = 0.f;
             if (lok && c2 < q2) {
@@ -243,8 +244,8 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     };
     auto transform = [&]() {
         #pragma unroll
-        for (int u = 0; u < FP2_CPT2; ++u) {
-            const int c2 = sc0 + 16 * u;
+        for (int u = 0; u < CPT2; ++u) {
+            const int c2 = sc0 + TPL * u;
             if (sline < FP2_BL && c2 < q2) {
                 const float2 v = raw[u];
                 *reinterpret_cast<float4*>(sd + sline * FP2_P + c2 * 2) =
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
         }
     };
 #else
+    const int sline = threadIdx.x >> 4, sc0 = threadIdx.x & 15;   // (threads 256.. of a 12-warp CTA do not stage)
     float4 raw[FP2_CPT];
     float nxt[FP2_CPT];
     auto fetch = [&](int l0) {                    // raw lines l0.. of the band into registers
