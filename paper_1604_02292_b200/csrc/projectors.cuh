@@ -417,13 +417,17 @@ struct BpEpi {
     int a_lo, a_hi;        // only angles [a_lo, a_hi) (a_hi <= 0: all; angle-split filter bank)
 };
 
-template <int NS, int MODE, int SUB = BP_SUB>
+// SUBH: sub-tile height (SUB wide): 64 x 128 sub-tiles give each thread 2 x 16
+// pixels, so the per-angle setup is spread over twice the pixels
+template <int NS, int MODE, int SUB = BP_SUB, int SUBH = SUB>
 __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoView s2, BpEpi e) {
     static_assert(NS == 0 || NS == 1, "one gathered sinogram at most");
-    static_assert(SUB == 64 || SUB == 32, "64x64 (2 columns x 8 rows per thread) or 32x32 (1 x 4) sub-tiles");
+    static_assert((SUB == 64 && (SUBH == 64 || SUBH == 128)) || (SUB == 32 && SUBH == 32),
+                  "64x64 / 64x128 (2 columns x 8 / 16 rows per thread) or 32x32 (1 x 4) sub-tiles");
     constexpr int COLS = SUB / 32;                // columns per thread (32 apart)
-    constexpr int BP_PR = SUB * SUB / (256 * COLS);   // rows per thread
-    constexpr int BP_SW = SUB == 64 ? 96 : 64;        // window bins (>= (SUB-1) sqrt2 + 4, a multiple of 32)
+    constexpr int BP_PR = SUB * SUBH / (256 * COLS);  // rows per thread
+    // window bins: >= the sub-tile's projected extent ((SUB|cos| + SUBH|sin|) / c + 4), a multiple of 32
+    constexpr int BP_SW = SUB == 64 ? (SUBH == 128 ? 160 : 96) : 64;
     __shared__ float2 sw[BP_CA][BP_SW];          // (v[m], v[m+1]) / c_a, m relative to the window centre
     __shared__ float4 sa[BP_CA];                 // (cos, sin, K' = 1 - 1/(2c), 1/c)
     __shared__ float sanch[BP_CA];
@@ -444,11 +448,11 @@ __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoVie
     }
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int pj0 = stx * SUB + lane;                  // columns pj0, pj0 + 32
-    const int pi0 = sty * SUB + wq * BP_PR;            // rows pi0 .. pi0 + BP_PR - 1
+    const int pi0 = sty * SUBH + wq * BP_PR;           // rows pi0 .. pi0 + BP_PR - 1
     const double Lc = 0.5 * (T - 1);
-    const double hs = 0.5 * (SUB - 1);
-    const double dxc = stx * SUB + hs - Lc, dyc = sty * SUB + hs - Lc;
-    const float dx = (float)lane - (float)hs, dy0 = (float)(wq * BP_PR) - (float)hs;
+    const double hsx = 0.5 * (SUB - 1), hsy = 0.5 * (SUBH - 1);
+    const double dxc = stx * SUB + hsx - Lc, dyc = sty * SUBH + hsy - Lc;
+    const float dx = (float)lane - (float)hsx, dy0 = (float)(wq * BP_PR) - (float)hsy;
 
     // angles this CTA gathers (all, or one chunk of an angle-split stage 1; none in stage 2)
     const int alo = e.a_hi > 0 ? e.a_lo : 0, ahi = e.a_hi > 0 ? min(e.a_hi, na) : na;
