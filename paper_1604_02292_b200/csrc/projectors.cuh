@@ -121,6 +121,9 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 // current band is marched, then transformed into the single (S, D) buffer.
 // ---------------------------------------------------------------------------
 constexpr int FP2_BL = 16;       // lines per band
+#ifndef FP_LEAN
+#define FP_LEAN 1   // line positions by FFMA2 pairs; per-ray-group anchors by fp64 increments and magic rounding
+#endif
 constexpr int FP2_P = 272;       // (S, D) entries per staged line (>= T + PADL + PADR)
 constexpr int FP2_PW = 336;      // wide tiles (T <= 328 - PADL - PADR = 320): entries per staged line
 constexpr int FP_UW = 15;        // wide tiles: rays per lane (window W(160) = 456 <= 32 * 15)
@@ -137,8 +140,15 @@ template <bool CLAMP, int SP = FP2_P>
 __device__ __forceinline__ float fp2_band_ray(unsigned rowbase_, float f0, float Bf, float lo, float hi) {
     const unsigned rowbase = __shfl_sync(0xffffffffu, rowbase_, threadIdx.x & 31);
     float acc = 0.f;
+#if FP_LEAN
+    const float2 B2 = make_float2(Bf, Bf), f01 = make_float2(f0, f0 + Bf);
+#endif
     auto addr_g = [&](int i, unsigned& a0, unsigned& a1, float2& g) {
+#if FP_LEAN
+        float2 tt = __ffma2_rn(B2, make_float2((float)i, (float)i), f01);          // lines i, i + 1: one FFMA2
+#else
         float2 tt = make_float2(fmaf((float)i, Bf, f0), fmaf((float)(i + 1), Bf, f0));   // immediates
+#endif
         if (CLAMP) {
             tt.x = fminf(fmaxf(tt.x, lo), hi);
             tt.y = fminf(fmaxf(tt.y, lo), hi);
@@ -313,17 +323,33 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
             const int whi = min(wv1, (int)ceil(fmax(fmax(e1, e2), fmax(e3, e4))) + 2);
             const float Af = (float)A;
             const float Bl = (float)((FP2_BL - 1) * B);
+#if FP_LEAN
+            constexpr double MAGICD = 6755399441055744.0;      // 1.5 * 2^52: x + MAGICD rounds x in the low bits
+            double pc = P0 + (double)(wlo + 16) * A;           // fp64 anchor of the first group, + 32 A per group
+            const double A32 = 32.0 * A;
+#endif
             for (int wb = wlo; wb < whi; wb += 32) {
                 const int w = wb + lane;
                 const bool ray = w < whi;
                 // position (pixel index) on line l0: fp64 anchor at the group's
                 // middle ray, fp32 offset |(lane - 16) A| <= 23 px
+#if FP_LEAN
+                const double rmd = pc + MAGICD;                 // round(pc) in the low bits
+                const double frd = pc - (rmd - MAGICD);         // in [-1/2, 1/2]
+                pc += A32;
+                const float pos = fmaf((float)(lane - 16), Af, (float)frd);
+                const float rmf = pos + MAGICF;                 // a nearest integer of pos (any integer near pos will do)
+                const float fl = rmf - MAGICF;
+                const int ib = ray ? (int)__double2loint(rmd) + (__float_as_int(rmf) - MAGICI) : 0;
+                const float f0 = ray ? (pos - fl) - 0.5f : -0.5f;
+#else
                 const double pc = P0 + (double)(wb + 16) * A;
                 const double fbc = floor(pc);
                 const float pos = fmaf((float)(lane - 16), Af, (float)(pc - fbc));
                 const float fl = floorf(pos);
                 const int ib = ray ? (int)fbc + (int)fl : 0;
                 const float f0 = ray ? (pos - fl) - 0.5f : -0.5f;
+#endif
                 const float Bu = ray ? Bf : 0.f;
                 const float pa = (float)ib + f0 + 0.5f, pe = pa + Bl;
                 const bool safe = !ray || (fminf(pa, pe) >= -3.f && fmaxf(pa, pe) <= (float)T + 1.5f);
