@@ -120,7 +120,10 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 // Staging: the next band's raw lines are prefetched into registers while the
 // current band is marched, then transformed into the single (S, D) buffer.
 // ---------------------------------------------------------------------------
-constexpr int FP2_BL = 16;       // lines per band
+#ifndef FP_BLN
+#define FP_BLN 16
+#endif
+constexpr int FP2_BL = FP_BLN;   // lines per band
 #ifndef FP_LEAN
 #define FP_LEAN 1   // line positions by FFMA2 pairs; per-ray-group anchors by fp64 increments and magic rounding
 #endif
