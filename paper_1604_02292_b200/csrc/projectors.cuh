@@ -301,7 +301,11 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     const int lbeg = (lv0 / FP2_BL) * FP2_BL + (int)blockIdx.z * FP2_BL, lstep = nsplit * FP2_BL;
     if (lbeg < lv1) { fetch(lbeg); transform(); }
     __syncthreads();
+#if FP_LEAN
+    const unsigned sbase = opaque_u32((unsigned)__cvta_generic_to_shared(sd + PADL));   // entry of pixel 0 (kept in a register)
+#else
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd + PADL);     // entry of pixel 0
+#endif
     for (int l0 = lbeg; l0 < lv1; l0 += lstep) {
         const bool more = l0 + lstep < lv1;
         if (more) fetch(l0 + lstep);
@@ -314,6 +318,9 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
             const int d0 = __ldg(t.d0 + r * na + a);
             const float Bf = (float)B;
             float* acc = sacc + (warp * FP_APW + j) * (32 * FP_U);
+#if FP_LEAN
+            const unsigned acc_s = opaque_u32((unsigned)__cvta_generic_to_shared(acc));   // (no per-group address rebuild)
+#endif
             // rays with a detector bin: w in [wv0, wv1)
             const int wv0 = max(0, -d0), wv1 = min(Wwin, g.nd - d0);
             // rays meeting the valid pixels (pv0 - 1, pv1) on some line of the band
@@ -364,7 +371,15 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
                     const float lo = (float)(-3 - ib) - 0.5f, hi = (float)(T + 2 - ib) - 0.5f;
                     v = fp2_band_ray<true, FP2_P>(rowbase, f0, Bu, lo, hi);
                 }
+#if FP_LEAN
+                if (ray) {
+                    float o;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(acc_s + 4u * (unsigned)w) : "memory");
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(acc_s + 4u * (unsigned)w), "f"(o + v) : "memory");
+                }
+#else
                 if (ray) acc[w] += v;
+#endif
             }
         }
         __syncthreads();
