@@ -40,6 +40,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 #ifndef FGP_OPAQUE
 #define FGP_OPAQUE 1   // loop-invariant shared addresses kept in registers (not rematerialised from SR_CgaCtaId)
 #endif
+#ifndef FGP_KEEP4
+#define FGP_KEEP4 1    // CP = 4: 0 none, 1 the mbarrier base only (1.267 -> 1.261 ms), 2 all (1.273; tools/ab_fgpkeep4.sh)
+#endif
 // K: keep x in a register (an opaque move).  Measured (tools/ab_fgpkeep2.sh, FGP per
 // launch): C3 (CP = 3) 0.188 -> 0.178 ms, P1 (CP = 5) 0.079 -> 0.077, but C4 (CP = 4,
 // 232 -> 228 registers) 1.271 -> 1.276, so the CP = 4 kernel leaves it to ptxas
@@ -442,15 +445,15 @@ __global__ void __launch_bounds__(NW * 32, (BSM && NW <= 8) ? 2 : 1) k_fgp2(FgpA
     constexpr unsigned PS = (NW + 1) * RB;             // bytes per parity of hr / hz
     const unsigned s_hr = smem_u32(sm + SM::hr), s_hz = smem_u32(sm + SM::hz);
     // this warp's halo slots: r from above, z from below (read); r / z it publishes (written)
-    const unsigned up_slot = keep_u32<CP != 4>(s_hr + w * RB), dn_slot = keep_u32<CP != 4>(s_hz + (w + 1) * RB);
+    const unsigned up_slot = keep_u32<CP != 4 || FGP_KEEP4 >= 2>(s_hr + w * RB), dn_slot = keep_u32<CP != 4 || FGP_KEEP4 >= 2>(s_hz + (w + 1) * RB);
     const unsigned rem_rx_r = mapa(s_hr, dn_rank);                 // my last warp's r row -> slot 0 of the CTA below
     const unsigned rem_bar_r = mapa(smem_u32(bars + 0), dn_rank);
     const unsigned rem_rx_z = mapa(s_hz + NW * RB, up_rank);       // my first warp's z row -> slot NW of the CTA above
     const unsigned rem_bar_z = mapa(smem_u32(bars + 2), up_rank);
-    const unsigned my_r_slot = keep_u32<CP != 4>(s_hr + (w + 1) * RB), my_z_slot = keep_u32<CP != 4>(s_hz + w * RB);
+    const unsigned my_r_slot = keep_u32<CP != 4 || FGP_KEEP4 >= 2>(s_hr + (w + 1) * RB), my_z_slot = keep_u32<CP != 4 || FGP_KEEP4 >= 2>(s_hz + w * RB);
     constexpr unsigned row_bytes = ROW * 4;
     const int nit = lam > 0.f ? A.nfgp : 0;
-    const unsigned bar0 = keep_u32<CP != 4>(smem_u32(bars));
+    const unsigned bar0 = keep_u32<CP != 4 || FGP_KEEP4 >= 1>(smem_u32(bars));
     const float2 nl2 = f2s(-lam2);
     // p step per row of this warp (0 where p does not exist: i >= H_v - 1)
     float gp[FR];
