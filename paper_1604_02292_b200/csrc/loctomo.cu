@@ -201,6 +201,7 @@ struct lt_plan {
     // ROI-batch pipelining: the local ROIs are split into groups whose
     // iteration chains run on separate streams and overlap on the device
     int nsplit = 1;
+    int split_at = 0;               // first ROI of the second group (two-group pipelining)
     cudaStream_t gst[2] = {nullptr, nullptr};        // per group: projector work (low priority)
     cudaStream_t fst[2] = {nullptr, nullptr};        // per group: FGP (high priority)
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
@@ -923,7 +924,7 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
     } else {
         // fork: both group streams wait for the work already queued on st
         LT_CUDA(cudaEventRecord(p.gev[2], st));
-        const int half = (p.R + 1) / 2;
+        const int half = p.split_at;
         for (int g = 0; g < 2; ++g) {
             LT_CUDA(cudaStreamWaitEvent(p.gst[g], p.gev[2], 0));
             const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
@@ -1265,7 +1266,10 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     // x_s block lists: blocks meeting any valid extended rect
     {
         const int nbk = (n + BP_SUB - 1) / BP_SUB;
-        const int half = (p->R + 1) / 2;
+        const char* sb = getenv("LT_SPLIT_B");     // size of the second ROI group (LT_SPLIT=2); default half
+        const int nb2 = sb ? atoi(sb) : 0;
+        const int half = (nb2 > 0 && nb2 < p->R) ? p->R - nb2 : (p->R + 1) / 2;
+        p->split_at = half;
         const int ranges[3][2] = {{0, p->R}, {0, half}, {half, p->R}};
         for (int l = 0; l < 3; ++l) {
             std::vector<char> need((size_t)nbk * nbk, 0);
