@@ -336,8 +336,22 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
     // 16 angles per CTA share each staged band; 8 when that would leave the
     // SMs short of two waves (small ROI batches: C1-C3, T1, 8-GPU shards)
     static int one_env = -2;
-    if (one_env == -2) { const char* e = getenv("LT_FP_ONE"); one_env = e ? atoi(e) : -1; }   // diagnostics: 0 / 1 force
-    const bool one = one_env >= 0 ? one_env == 1 : (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
+    if (one_env == -2) { const char* e = getenv("LT_FP_ONE"); one_env = (e && *e) ? atoi(e) : -1; }   // diagnostics: 0 / 1 force
+    bool one = one_env >= 0 ? one_env == 1 : (long long)p.ngroups * t.ntiles < 2LL * 3 * p.num_sms;
+    // ... but the 24-angle CTAs when they pad the angles by <= 10 % and still fill
+    // >= 3/4 of a wave (a C4 shard of 32 ROIs on 8 GPUs: 256 CTAs for 296 slots,
+    // FP 0.236 -> 0.223 ms; C2 / C3 pad 32 / 64 angles to 48 / 96 and keep 8)
+    bool small24 = false;
+    if (one && one_env < 0 && fp_wide() && 10 * p.ngroups24 * 24 <= 11 * p.na && p.ngroups24 * 24 <= p.ngroups * 16) {
+        static long long r24_dev[LT_MAX_DEV] = {};
+        const int dv = std::max(0, cur_dev());
+        if (!r24_dev[dv]) {
+            const size_t smem3 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
+            LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+            r24_dev[dv] = resident_ctas(p, k_fp_roi2<2, 12>, 384, smem3);
+        }
+        if (4LL * p.ngroups24 * t.ntiles >= 3LL * r24_dev[dv]) { one = false; small24 = true; }
+    }
     const int apw = one ? 1 : 2;
     const size_t smem2 = (size_t)FP2_BL * FP2_P * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1, p.a_lo, p.a_hi};
@@ -363,7 +377,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         } else {
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
         }
-    } else if (fp_wide() && ((long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms || one_env == 0) &&
+    } else if (fp_wide() && ((long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms || one_env == 0 || small24) &&
                p.ngroups24 * 24 <= p.ngroups * 16) {
         // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM),
         // unless the 24-angle groups pad more (C5: 128 angles per orientation = 5 1/3 x 24)
