@@ -131,6 +131,16 @@ constexpr int FP2_P = 272;       // (S, D) entries per staged line (>= T + PADL 
 constexpr int FP2_PW = 336;      // wide tiles (T <= 328 - PADL - PADR = 320): entries per staged line
 constexpr int FP_UW = 15;        // wide tiles: rays per lane (window W(160) = 456 <= 32 * 15)
 constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16;  // float4 chunks per thread per band (16 threads per line)
+#ifndef FP_XPAD
+#define FP_XPAD 16     // zero (S, D) entries staged on each side of a line (0: the round-1/2 layout)
+#endif
+// With FP_XPAD >= 16 every ray the band visits stays inside its staged line
+// (positions reach at most 15 |B| + 2 A + 1 < 19 px beyond the valid pixels:
+// PADL + FP_XPAD zero pixels on the left, >= PADR + FP_XPAD on the right), so
+// the clamped ray variant (FMNMX per step) is no longer needed for the rays
+// near the tile edges; the results are bitwise the same (zeros either way).
+constexpr int FP_XP = FP_XPAD;
+__host__ __device__ constexpr int fp_line(int sp) { return sp + 2 * FP_XP; }   // staged entries per line, margins included
 #ifndef FP_STAGE64
 #define FP_STAGE64 1   // staging by 8-byte pixel pairs: each STS.128 of a half-warp covers 256 contiguous bytes
 #endif
@@ -208,10 +218,11 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
                                                                             const int* __restrict__ groups) {
     constexpr int FP_GA = NWARP * FP_APW;       // angles per CTA (they share each staged band)
     constexpr int FP2_P = SP, FP_U = SU;
+    constexpr int SPX = fp_line(SP);             // staged entries per line (FP_XP zero entries on each side)
     constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16, FP2_CPT2 = (FP2_P / 2 + 15) / 16;
     extern __shared__ float4 smf4[];
-    float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][FP2_P] (S, D), entry 0 = pixel -PADL
-    float* sacc = reinterpret_cast<float*>(sd + FP2_BL * FP2_P);  // [FP_GA][32 * FP_U] per-ray accumulators
+    float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][SPX] (S, D), entry 0 = pixel -PADL - FP_XP
+    float* sacc = reinterpret_cast<float*>(sd + FP2_BL * SPX);    // [FP_GA][32 * FP_U] per-ray accumulators
     const int r = blockIdx.y, grp = blockIdx.x;
     const int na = g.na, T = t.T, TP = t.TP, Wwin = t.Wwin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -229,6 +240,15 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     const double Lc = 0.5 * (T - 1);
     const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
     for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += NWARP * 32) sacc[e] = 0.f;
+    if constexpr (FP_XP > 0) {   // the zero margins of every staged line (never overwritten by the staging)
+        const int rb = FP_XP + TP;               // first entry after the raw line
+        for (int e = threadIdx.x; e < FP2_BL * 2 * FP_XP + FP2_BL * (SP - TP); e += NWARP * 32) {
+            int l, k;
+            if (e < FP2_BL * 2 * FP_XP) { l = e / (2 * FP_XP); k = e - l * 2 * FP_XP; k = k < FP_XP ? k : rb + (k - FP_XP); }
+            else { const int e2 = e - FP2_BL * 2 * FP_XP; l = e2 / (SP - TP); k = rb + FP_XP + (e2 - l * (SP - TP)); }
+            sd[l * SPX + k] = make_float2(0.f, 0.f);
+        }
+    }
 
     const int q4 = TP / 4;                        // float4 chunks per raw line
     const int q2 = TP / 2;                        // float2 chunks per raw line
@@ -261,7 +281,7 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
             const int c2 = sc0 + TPL * u;
             if (sline < FP2_BL && c2 < q2) {
                 const float2 v = raw[u];
-                *reinterpret_cast<float4*>(sd + sline * FP2_P + c2 * 2) =
+                *reinterpret_cast<float4*>(sd + sline * SPX + FP_XP + c2 * 2) =
                     make_float4(v.x + v.y, v.y - v.x, v.y + nxt[u], nxt[u] - v.y);
             }
         }
@@ -290,7 +310,7 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
             const int c4 = sc0 + 16 * u;
             if (sline < FP2_BL && c4 < q4) {
                 const float4 v = raw[u];
-                float4* dst = reinterpret_cast<float4*>(sd + sline * FP2_P + c4 * 4);
+                float4* dst = reinterpret_cast<float4*>(sd + sline * SPX + FP_XP + c4 * 4);
                 dst[0] = make_float4(v.x + v.y, v.y - v.x, v.y + v.z, v.z - v.y);
                 dst[1] = make_float4(v.z + v.w, v.w - v.z, v.w + nxt[u], nxt[u] - v.w);
             }
@@ -302,9 +322,9 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     if (lbeg < lv1) { fetch(lbeg); transform(); }
     __syncthreads();
 #if FP_LEAN
-    const unsigned sbase = opaque_u32((unsigned)__cvta_generic_to_shared(sd + PADL));   // entry of pixel 0 (kept in a register)
+    const unsigned sbase = opaque_u32((unsigned)__cvta_generic_to_shared(sd + FP_XP + PADL));   // entry of pixel 0 (kept in a register)
 #else
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd + PADL);     // entry of pixel 0
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd + FP_XP + PADL);     // entry of pixel 0
 #endif
     for (int l0 = lbeg; l0 < lv1; l0 += lstep) {
         const bool more = l0 + lstep < lv1;
@@ -362,14 +382,18 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
 #endif
                 const float Bu = ray ? Bf : 0.f;
                 const float pa = (float)ib + f0 + 0.5f, pe = pa + Bl;
-                const bool safe = !ray || (fminf(pa, pe) >= -3.f && fmaxf(pa, pe) <= (float)T + 1.5f);
+                // inside the staged line (entries of pixels -PADL - FP_XP .. SPX - PADL - FP_XP - 1), one pixel to spare
+                // (FP_XP = 0: the round-2 bounds, pixels -3 .. T + 1.5 of the raw line)
+                const bool safe = !ray || (FP_XP > 0 ? (fminf(pa, pe) >= (float)(1 - PADL - FP_XP) &&
+                                                        fmaxf(pa, pe) <= (float)(SPX - PADL - FP_XP - 3))
+                                                     : (fminf(pa, pe) >= -3.f && fmaxf(pa, pe) <= (float)T + 1.5f));
                 const unsigned rowbase = sbase + 8u * (unsigned)(ib - MAGICI);
                 float v;
                 if (__all_sync(0xffffffffu, safe)) {
-                    v = fp2_band_ray<false, FP2_P>(rowbase, f0, Bu, 0.f, 0.f);
+                    v = fp2_band_ray<false, SPX>(rowbase, f0, Bu, 0.f, 0.f);
                 } else {
                     const float lo = (float)(-3 - ib) - 0.5f, hi = (float)(T + 2 - ib) - 0.5f;
-                    v = fp2_band_ray<true, FP2_P>(rowbase, f0, Bu, lo, hi);
+                    v = fp2_band_ray<true, SPX>(rowbase, f0, Bu, lo, hi);
                 }
 #if FP_LEAN
                 if (ray) {
