@@ -15,6 +15,7 @@ timeout 900 python bench.py --config C5 --prior exterior --steps 3 --warmup 2 --
 timeout 900 python bench.py --xs-exact --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/final_bench_C4_xsexact.json 2>/dev/null; echo "xs-exact rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/final_bench_ref.json 2>/dev/null; echo "ref rc=$?"
 timeout 900 python tools/rank_scaling.py C4 > gpurun_out/final_rank_scaling.txt 2>&1; echo "scaling rc=$?"
+timeout 900 python tools/rank_scaling.py C5 1,8 > gpurun_out/final_rank_scaling_C5.txt 2>&1; echo "scaling C5 rc=$?"
 for c in C4 C2 C3 L1 P1 T1; do echo "$c $(KB_NITER=20 python tools/kernel_bench.py $c 2>&1 | tail -1)"; done > gpurun_out/final_kernel_bench.txt
 python - <<'PY'
 import json, glob
