@@ -310,7 +310,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         // wide tiles (up to 320: the paper's 256^2 parts with 1/8 padding): 8 warps x
         // 1 angle, 336-entry staged lines, 15 rays per lane; bands split over CTAs
         // when a launch is under one wave (as below)
-        const size_t smemw = (size_t)FP2_BL * fp_line(FP2_PW) * sizeof(float2) + (size_t)8 * 32 * FP_UW * sizeof(float);
+        const size_t smemw = (size_t)FP2_BL * fp_line(FP2_PW, 1) * sizeof(float2) + (size_t)8 * 32 * FP_UW * sizeof(float);
         auto kw = k_fp_roi2<1, 8, FP2_PW, FP_UW>;
         LT_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemw));
         FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1, p.a_lo, p.a_hi};
@@ -346,14 +346,14 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
         static long long r24_dev[LT_MAX_DEV] = {};
         const int dv = std::max(0, cur_dev());
         if (!r24_dev[dv]) {
-            const size_t smem3 = (size_t)FP2_BL * fp_line(FP2_P) * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
+            const size_t smem3 = (size_t)FP2_BL * fp_line(FP2_P, 2) * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
             LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
             r24_dev[dv] = resident_ctas(p, k_fp_roi2<2, 12>, 384, smem3);
         }
         if (4LL * p.ngroups24 * t.ntiles >= 3LL * r24_dev[dv]) { one = false; small24 = true; }
     }
     const int apw = one ? 1 : 2;
-    const size_t smem2 = (size_t)FP2_BL * fp_line(FP2_P) * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
+    const size_t smem2 = (size_t)FP2_BL * fp_line(FP2_P, apw) * sizeof(float2) + (size_t)8 * apw * 32 * FP_U * sizeof(float);
     FpArgs f{img, imgT, img_ts, out, out_ts, nullptr, nullptr, (float)p.alpha, nullptr, 1, p.a_lo, p.a_hi};
     ScopedTimer tm(TC_FP, st);
     if (one) {
@@ -381,7 +381,7 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
                p.ngroups24 * 24 <= p.ngroups * 16) {
         // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM),
         // unless the 24-angle groups pad more (C5: 128 angles per orientation = 5 1/3 x 24)
-        const size_t smem3 = (size_t)FP2_BL * fp_line(FP2_P) * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
+        const size_t smem3 = (size_t)FP2_BL * fp_line(FP2_P, 2) * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
         k_fp_roi2<2, 12><<<dim3(p.ngroups24, t.ntiles), 384, smem3, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups24));
     } else {

@@ -139,8 +139,10 @@ constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16;  // float4 chunks per thread per 
 // PADL + FP_XPAD zero pixels on the left, >= PADR + FP_XPAD on the right), so
 // the clamped ray variant (FMNMX per step) is no longer needed for the rays
 // near the tile edges; the results are bitwise the same (zeros either way).
-constexpr int FP_XP = FP_XPAD;
-__host__ __device__ constexpr int fp_line(int sp) { return sp + 2 * FP_XP; }   // staged entries per line, margins included
+// Only the two-angles-per-warp kernels (C4 / C5 batches) take the margins: the
+// one-angle-per-warp kernel of small batches measured slower with them (L1 FP
+// 0.062 -> 0.068 ms per launch) and keeps the clamped edge groups.
+__host__ __device__ constexpr int fp_line(int sp, int apw) { return sp + 2 * (apw == 2 ? FP_XPAD : 0); }   // staged entries per line
 #ifndef FP_STAGE64
 #define FP_STAGE64 1   // staging by 8-byte pixel pairs: each STS.128 of a half-warp covers 256 contiguous bytes
 #endif
@@ -218,7 +220,8 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
                                                                             const int* __restrict__ groups) {
     constexpr int FP_GA = NWARP * FP_APW;       // angles per CTA (they share each staged band)
     constexpr int FP2_P = SP, FP_U = SU;
-    constexpr int SPX = fp_line(SP);             // staged entries per line (FP_XP zero entries on each side)
+    constexpr int FP_XP = FP_APW == 2 ? FP_XPAD : 0;   // zero entries on each side of a staged line
+    constexpr int SPX = fp_line(SP, FP_APW);            // staged entries per line
     constexpr int FP2_CPT = (FP2_P / 4 + 15) / 16, FP2_CPT2 = (FP2_P / 2 + 15) / 16;
     extern __shared__ float4 smf4[];
     float2* sd = reinterpret_cast<float2*>(smf4);                 // [FP2_BL][SPX] (S, D), entry 0 = pixel -PADL - FP_XP
@@ -240,13 +243,12 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
     const double Lc = 0.5 * (T - 1);
     const float* src = (col ? f.imgT : f.img) + (long long)r * f.img_tstride;
     for (int e = threadIdx.x; e < FP_GA * 32 * FP_U; e += NWARP * 32) sacc[e] = 0.f;
-    if constexpr (FP_XP > 0) {   // the zero margins of every staged line (never overwritten by the staging)
+    if constexpr (FP_XP > 0) {   // the zero margins of every staged line (never overwritten by the staging):
+        // FP_XP entries before and after the raw line (entries past them are never read)
         const int rb = FP_XP + TP;               // first entry after the raw line
-        for (int e = threadIdx.x; e < FP2_BL * 2 * FP_XP + FP2_BL * (SP - TP); e += NWARP * 32) {
-            int l, k;
-            if (e < FP2_BL * 2 * FP_XP) { l = e / (2 * FP_XP); k = e - l * 2 * FP_XP; k = k < FP_XP ? k : rb + (k - FP_XP); }
-            else { const int e2 = e - FP2_BL * 2 * FP_XP; l = e2 / (SP - TP); k = rb + FP_XP + (e2 - l * (SP - TP)); }
-            sd[l * SPX + k] = make_float2(0.f, 0.f);
+        for (int e = threadIdx.x; e < FP2_BL * 2 * FP_XP; e += NWARP * 32) {
+            const int l = e / (2 * FP_XP), k = e - l * 2 * FP_XP;
+            sd[l * SPX + (k < FP_XP ? k : rb + (k - FP_XP))] = make_float2(0.f, 0.f);
         }
     }
 
@@ -382,10 +384,10 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP == 8 ? 3 : 2) k_fp_roi2(Geo 
 #endif
                 const float Bu = ray ? Bf : 0.f;
                 const float pa = (float)ib + f0 + 0.5f, pe = pa + Bl;
-                // inside the staged line (entries of pixels -PADL - FP_XP .. SPX - PADL - FP_XP - 1), one pixel to spare
+                // inside the zeroed / staged entries (pixels -PADL - FP_XP .. TP - PADL + FP_XP - 1), one pixel to spare
                 // (FP_XP = 0: the round-2 bounds, pixels -3 .. T + 1.5 of the raw line)
                 const bool safe = !ray || (FP_XP > 0 ? (fminf(pa, pe) >= (float)(1 - PADL - FP_XP) &&
-                                                        fmaxf(pa, pe) <= (float)(SPX - PADL - FP_XP - 3))
+                                                        fmaxf(pa, pe) <= (float)(TP - PADL + FP_XP - 3))
                                                      : (fminf(pa, pe) >= -3.f && fmaxf(pa, pe) <= (float)T + 1.5f));
                 const unsigned rowbase = sbase + 8u * (unsigned)(ib - MAGICI);
                 float v;
