@@ -205,7 +205,7 @@ struct lt_plan {
     cudaStream_t gst[2] = {nullptr, nullptr};        // per group: projector work (low priority)
     cudaStream_t fst[2] = {nullptr, nullptr};        // per group: FGP (high priority)
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t pev[2] = {nullptr, nullptr}, fev[2] = {nullptr, nullptr};
+    cudaEvent_t pev[2] = {nullptr, nullptr}, fev[2] = {nullptr, nullptr}, bpev[2] = {nullptr, nullptr};
     struct {
         size_t angf, cs64, sn64, A64, B64, tiles, d0, tauc, gtile, gd0, gtauc, fpgroups, fpgroups1, fpgroups24, bpart, fpart;
         size_t bank, conv, pc, wd, wdsum, psum, discc64, discc32, err;
@@ -795,9 +795,15 @@ int conv_cache_direct(lt_plan& p, const float* d_pc, cudaStream_t st) {
 
 // the local iteration loop (a5-a8) for every local ROI; mode 0 box, 1 TV
 // one ROI group (tiles [t0, t0 + cnt)) through all n iterations on stream st
+// (two-group pipelining with a shared x_s: the caller runs one iteration at a
+// time, [k0, k1) with the FISTA t_k in *tkp; ext_side = the caller computes
+// x_s^k on the side stream into xsg[0] for both groups and records p.xev_xs;
+// this group's ROI backprojection waits for it and records bpev when done)
 int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, float hi, float lam, int nfgp,
                      const float* d_sino, cudaStream_t st, cudaStream_t fst = nullptr, cudaEvent_t pev = nullptr,
-                     cudaEvent_t fev = nullptr) {
+                     cudaEvent_t fev = nullptr, int k0 = 0, int k1 = -1, double* tkp = nullptr, bool ext_side = false,
+                     cudaEvent_t bpev = nullptr) {
+    if (k1 < 0) k1 = p.n_iter;
     Tiles t = p.roi_tiles();
     t.tile += t0; t.d0 += (size_t)t0 * p.na; t.tauc += (size_t)t0 * p.na; t.ntiles = cnt;
     const long long yts = p.ytile();
@@ -813,14 +819,14 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
     // x_s^k = M_{L'} W^T b_k for every ROI of the group comes from one global
     // backprojection over the image blocks the group's extended ROIs cover
     // (the extended ROIs overlap, so this is ~4x less work than per ROI)
-    float* xsg = p.P<float>(p.off.xsg[gl == 2 ? 1 : 0]);
+    float* xsg = p.P<float>(p.off.xsg[(gl == 2 && !ext_side) ? 1 : 0]);
     int xsg_pitch = p.n;
     const int* blist = p.P<int>(p.off.xsblk[gl]);
     const int nbl = (int)p.xsblk[gl].size();
     if (exact) { xsg = p.P<float>(p.off.gimg) + PADL; xsg_pitch = p.GTP; }   // the global SIRT iterate
     static int overlap_env = -1;
     if (overlap_env < 0) { const char* e = getenv("LT_XS_OVERLAP"); overlap_env = !(e && atoi(e) == 0); }
-    const bool side = overlap_env && !exact && !fst && nbl > 0;
+    const bool side = overlap_env && !exact && !fst && nbl > 0 && !ext_side;
     if (side && !p.xst) {
         LT_CUDA(cudaStreamCreateWithFlags(&p.xst, cudaStreamNonBlocking));
         LT_CUDA(cudaEventCreateWithFlags(&p.xev_bp, cudaEventDisableTiming));
@@ -838,10 +844,10 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
         if (int rc = xs_bp(0, p.xst)) return rc;
         LT_CUDA(cudaEventRecord(p.xev_xs, p.xst));
     }
-    double tk = 1.0;
-    for (int k = 0; k < p.n_iter; ++k) {
+    double tk = tkp ? *tkp : 1.0;
+    for (int k = k0; k < k1; ++k) {
         const float* bk = p.P<float>(p.off.conv) + (long long)k * ns;
-        if (side) {
+        if (side || ext_side) {
             // x_s^k was queued on the side stream; its ROI BP waits for it below
         } else if (exact) {   // x^k = x^{k-1} + alpha W^T (p - W x^{k-1}) on the full grid, x^0 = 0 (eq. sirtit)
             const Tiles gt = p.glob_tiles();
@@ -865,17 +871,18 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
         e.alpha = (float)p.alpha; e.lo = lo; e.hi = hi; e.last = (k == p.n_iter - 1);
         if (k == 0) {
             // y^0 = 0: W_{L'} y^0 = 0, no gather
-            if (side) LT_CUDA(cudaStreamWaitEvent(st, p.xev_xs, 0));
+            if (side || ext_side) LT_CUDA(cudaStreamWaitEvent(st, p.xev_xs, 0));
             const SinoView v0 = view_full(bk, p.nd);
             if (mode == 0) { if (int rc = launch_bp_t<0, BP_BOX>(p, t, v0, v0, e, st)) return rc; }
             else { if (int rc = launch_bp_t<0, BP_TV>(p, t, v0, v0, e, st)) return rc; }
         } else {
             if (int rc = launch_fp_roi(p, t, y, yT, yts, s, (long long)p.na * p.Wwin, st)) return rc;
-            if (side) LT_CUDA(cudaStreamWaitEvent(st, p.xev_xs, 0));
+            if (side || ext_side) LT_CUDA(cudaStreamWaitEvent(st, p.xev_xs, 0));
             const SinoView vs = view_win(s, p.Wwin, p.na);
             if (mode == 0) { if (int rc = launch_bp_t<1, BP_BOX>(p, t, vs, vs, e, st)) return rc; }
             else { if (int rc = launch_bp_t<1, BP_TV>(p, t, vs, vs, e, st)) return rc; }
         }
+        if (ext_side && bpev) LT_CUDA(cudaEventRecord(bpev, st));
         if (side && k + 1 < p.n_iter) {   // x_s^{k+1} may overwrite x_s^k once this ROI BP has read it
             LT_CUDA(cudaEventRecord(p.xev_bp, st));
             LT_CUDA(cudaStreamWaitEvent(p.xst, p.xev_bp, 0));
@@ -915,7 +922,8 @@ int group_iterations(lt_plan& p, int gl, int t0, int cnt, int mode, float lo, fl
             LT_LAUNCHED();
         }
     }
-    if (fst && mode == 1) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));      // the group's stream ends after its last FGP
+    if (tkp) *tkp = tk;
+    if (fst && mode == 1 && k1 == p.n_iter) LT_CUDA(cudaStreamWaitEvent(st, fev, 0));   // the group's stream ends after its last FGP
     return LT_OK;
 }
 
@@ -939,14 +947,56 @@ int local_iterations(lt_plan& p, int mode, float lo, float hi, float lam, int nf
         // fork: both group streams wait for the work already queued on st
         LT_CUDA(cudaEventRecord(p.gev[2], st));
         const int half = p.split_at;
+        static int sxs_env = -1;
+        if (sxs_env < 0) { const char* e = getenv("LT_SPLIT_XS"); sxs_env = !(e && atoi(e) == 0); }
+        const bool shared_xs = sxs_env && !p.xsblk[0].empty();
         for (int g = 0; g < 2; ++g) {
             LT_CUDA(cudaStreamWaitEvent(p.gst[g], p.gev[2], 0));
-            const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
-            const bool prio = p.fst[g] && mode == 1;
-            if (prio) LT_CUDA(cudaStreamWaitEvent(p.fst[g], p.gev[2], 0));
-            if (int rc = group_iterations(p, 1 + g, t0, cnt, mode, lo, hi, lam, nfgp, d_sino, p.gst[g],
-                                          prio ? p.fst[g] : nullptr, p.pev[g], p.fev[g])) return rc;
-            LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
+            if (p.fst[g] && mode == 1) LT_CUDA(cudaStreamWaitEvent(p.fst[g], p.gev[2], 0));
+        }
+        if (!shared_xs) {   // each group computes the x_s of its own blocks on its own stream
+            for (int g = 0; g < 2; ++g) {
+                const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
+                const bool prio = p.fst[g] && mode == 1;
+                if (int rc = group_iterations(p, 1 + g, t0, cnt, mode, lo, hi, lam, nfgp, d_sino, p.gst[g],
+                                              prio ? p.fst[g] : nullptr, p.pev[g], p.fev[g])) return rc;
+                LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
+            }
+        } else {
+            // one x_s^k for both groups on the side stream (the global backprojection
+            // over all their blocks), queued as soon as both groups' ROI backprojections
+            // of iteration k - 1 have read x_s^{k-1}; the groups run one iteration at a time
+            if (!p.xst) {
+                LT_CUDA(cudaStreamCreateWithFlags(&p.xst, cudaStreamNonBlocking));
+                LT_CUDA(cudaEventCreateWithFlags(&p.xev_bp, cudaEventDisableTiming));
+                LT_CUDA(cudaEventCreateWithFlags(&p.xev_xs, cudaEventDisableTiming));
+            }
+            auto xs_full = [&](int k) -> int {
+                BpEpi ex = epi0();
+                ex.blist = p.P<int>(p.off.xsblk[0]); ex.out = p.P<float>(p.off.xsg[0]); ex.out_pitch = p.n;
+                const SinoView vb = view_full(p.P<float>(p.off.conv) + (long long)k * p.na * p.nd, p.nd);
+                return launch_bp_t<1, BP_PLAIN_GLOBAL>(p, p.glob_tiles(), vb, vb, ex, p.xst, (int)p.xsblk[0].size());
+            };
+            LT_CUDA(cudaStreamWaitEvent(p.xst, p.gev[2], 0));
+            if (int rc = xs_full(0)) return rc;
+            LT_CUDA(cudaEventRecord(p.xev_xs, p.xst));
+            double tk[2] = {1.0, 1.0};
+            for (int k = 0; k < p.n_iter; ++k) {
+                for (int g = 0; g < 2; ++g) {
+                    const int t0 = g ? half : 0, cnt = g ? p.R - half : half;
+                    const bool prio = p.fst[g] && mode == 1;
+                    if (int rc = group_iterations(p, 1 + g, t0, cnt, mode, lo, hi, lam, nfgp, d_sino, p.gst[g],
+                                                  prio ? p.fst[g] : nullptr, p.pev[g], p.fev[g], k, k + 1, &tk[g], true,
+                                                  p.bpev[g])) return rc;
+                }
+                if (k + 1 < p.n_iter) {
+                    LT_CUDA(cudaStreamWaitEvent(p.xst, p.bpev[0], 0));
+                    LT_CUDA(cudaStreamWaitEvent(p.xst, p.bpev[1], 0));
+                    if (int rc = xs_full(k + 1)) return rc;
+                    LT_CUDA(cudaEventRecord(p.xev_xs, p.xst));
+                }
+            }
+            for (int g = 0; g < 2; ++g) LT_CUDA(cudaEventRecord(p.gev[g], p.gst[g]));
         }
         // join
         LT_CUDA(cudaStreamWaitEvent(st, p.gev[0], 0));
@@ -1476,6 +1526,7 @@ int lt_plan_bind_workspace(lt_plan* p, void* d_ws, int64_t bytes, void* stream) 
             if (use_prio) LT_CUDA(cudaStreamCreateWithPriority(&p->fst[g], cudaStreamNonBlocking, hi_prio));
             LT_CUDA(cudaEventCreateWithFlags(&p->pev[g], cudaEventDisableTiming));
             LT_CUDA(cudaEventCreateWithFlags(&p->fev[g], cudaEventDisableTiming));
+            LT_CUDA(cudaEventCreateWithFlags(&p->bpev[g], cudaEventDisableTiming));
         }
         for (int g = 0; g < 3; ++g) LT_CUDA(cudaEventCreateWithFlags(&p->gev[g], cudaEventDisableTiming));
     }
@@ -2375,6 +2426,7 @@ void lt_plan_destroy(lt_plan* p) {
         if (p->fst[g]) cudaStreamDestroy(p->fst[g]);
         if (p->pev[g]) cudaEventDestroy(p->pev[g]);
         if (p->fev[g]) cudaEventDestroy(p->fev[g]);
+        if (p->bpev[g]) cudaEventDestroy(p->bpev[g]);
     }
     for (int g = 0; g < 3; ++g)
         if (p->gev[g]) cudaEventDestroy(p->gev[g]);

@@ -654,3 +654,31 @@ def test_determinism_full_size_c4(lt):
     box = [cpu(plan.sirt_solve(sino, 0.0, math.inf)) for _ in range(2)]
     assert np.array_equal(tv[0], tv[1]) and np.array_equal(tv[0], tv[2])
     assert np.array_equal(box[0], box[1])
+
+
+def test_two_group_pipelining_matches_oracle(lt, orc, monkeypatch):
+    """LT_SPLIT=2 (two ROI groups on their own streams, one shared side-stream
+    x_s^k, the second group of LT_SPLIT_B ROIs): C2's 16 ROIs as 13 + 3, TV and
+    box, against the oracle and against the one-group solve."""
+    cfg = synth.config("C2")
+    inp = synth.make_inputs("C2")
+    n_iter = 12
+    sino = gpu(inp.sino)
+    base = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter)
+    base.filter_bank()
+    bank = base.get_bank()
+    want_tv = cpu(base.tv_solve(sino, cfg.lam, 30))
+    want_box = cpu(base.sirt_solve(sino, 0.0, math.inf))
+    monkeypatch.setenv("LT_SPLIT", "2")
+    monkeypatch.setenv("LT_SPLIT_B", "3")
+    plan = lt.Plan(cfg.n, inp.angles, cfg.n_det, inp.centres, cfg.radius, cfg.margin, n_iter)
+    plan.set_bank(bank)
+    got_tv = cpu(plan.tv_solve(sino, cfg.lam, 30))
+    got_box = cpu(plan.sirt_solve(sino, 0.0, math.inf))
+    assert relerr(got_tv, want_tv) <= 1e-5 and relerr(got_box, want_box) <= 1e-5
+    sample = np.array([0, 5, 13, 15])          # both groups
+    ref = orc.pipeline(inp.sino.astype(np.float64), inp.angles, cfg.n, inp.centres[sample], cfg.radius,
+                       cfg.margin, n_iter, mode="tv", lam=cfg.lam, n_fgp=30)
+    for k, g in enumerate(sample):
+        q = int(np.nonzero(plan.local_rois == g)[0][0])
+        assert relerr(got_tv[q], ref[k]) <= 1e-3, g
