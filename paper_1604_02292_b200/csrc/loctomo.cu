@@ -476,8 +476,21 @@ int launch_bp_t(const lt_plan& p, const Tiles& t, const SinoView& s1, const Sino
         const int nsy = (t.T + 127) / 128;
         // 64 x 128 sub-tiles for the ROI backprojection when they still fill >= 4 waves
         // (128 registers: 2 CTAs per SM; C3's 64 ROIs: 0.070 vs 0.047 ms at under 2 waves)
+        // 64 x 32 sub-tiles when the 64 x 64 CTAs would load the busiest SM clearly
+        // more than the average (a C4 shard of 32 ROIs on 8 GPUs: 512 CTAs = 3.46 per
+        // SM, 4 on the busiest; 1024 half-size CTAs: 7 x 1/2), by the estimate
+        // ceil(CTAs / SMs) x work per CTA x 1.06 (staging and setup over half the pixels)
+        static int short_env = -2;
+        if (short_env == -2) { const char* v = getenv("LT_BP_SHORT"); short_env = (v && *v) ? atoi(v) : -1; }
+        const int nsyh = (t.T + 31) / 32;
+        const long long c64 = (long long)nsx * nsx * t.ntiles, c32 = (long long)nsx * nsyh * t.ntiles;
+        const double est64 = (double)((c64 + p.num_sms - 1) / p.num_sms);
+        const double est32 = 0.5 * 1.06 * (double)((c32 + p.num_sms - 1) / p.num_sms);
+        const bool shortb = !e.blist && NS > 0 && short_env != 0 && (short_env == 1 || est32 < 0.97 * est64);
         if (tall_env && !e.blist && NS > 0 && (long long)nsx * nsy * t.ntiles >= 4LL * 2 * p.num_sms) {
             k_bp<NS, MODE, BP_SUB, 128><<<dim3(nsx * nsy, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
+        } else if (shortb) {
+            if constexpr (NS > 0) k_bp<NS, MODE, BP_SUB, 32><<<dim3(nsx * nsyh, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
         } else {
             k_bp<NS, MODE, BP_SUB><<<dim3(e.blist ? nblist : nsx * nsx, t.ntiles), 256, 0, st>>>(p.geo(), t, s1, s2, e);
         }

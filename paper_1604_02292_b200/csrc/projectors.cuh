@@ -492,12 +492,13 @@ struct BpEpi {
 template <int NS, int MODE, int SUB = BP_SUB, int SUBH = SUB>
 __global__ void __launch_bounds__(256) k_bp(Geo g, Tiles t, SinoView s1, SinoView s2, BpEpi e) {
     static_assert(NS == 0 || NS == 1, "one gathered sinogram at most");
-    static_assert((SUB == 64 && (SUBH == 64 || SUBH == 128)) || (SUB == 32 && SUBH == 32),
-                  "64x64 / 64x128 (2 columns x 8 / 16 rows per thread) or 32x32 (1 x 4) sub-tiles");
+    static_assert((SUB == 64 && (SUBH == 32 || SUBH == 64 || SUBH == 128)) || (SUB == 32 && SUBH == 32),
+                  "64x32 / 64x64 / 64x128 (2 columns x 4 / 8 / 16 rows per thread) or 32x32 (1 x 4) sub-tiles");
     constexpr int COLS = SUB / 32;                // columns per thread (32 apart)
     constexpr int BP_PR = SUB * SUBH / (256 * COLS);  // rows per thread
     // window bins (unit bin spacing): centred on the sub-tile centre's projection, half-width
-    // >= max |u - u_c| + 2 = sqrt(((SUB-1)/2)^2 + ((SUBH-1)/2)^2) + 2 (46.5 / 72.9 / 23.9 of 48 / 80 / 32), a multiple of 32
+    // >= max |u - u_c| + 2 = sqrt(((SUB-1)/2)^2 + ((SUBH-1)/2)^2) + 2 (46.5 / 72.9 / 37.1 / 23.9 of 48 / 80 / 48 / 32),
+    // a multiple of 32 (64 x 32 sub-tiles take the 64 x 64 window)
     constexpr int BP_SW = SUB == 64 ? (SUBH == 128 ? 160 : 96) : 64;
     __shared__ float2 sw[BP_CA][BP_SW];          // (v[m], v[m+1]) / c_a, m relative to the window centre
     __shared__ float4 sa[BP_CA];                 // (cos, sin, K' = 1 - 1/(2c), 1/c)
