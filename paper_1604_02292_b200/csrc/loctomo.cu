@@ -1244,11 +1244,13 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     // Cost model: the FGP cluster works on the full (2h)^2 tile, the projectors on
     // the valid pixels: cost = 2 (2h)^2 + 3 * valid (measured ~40/60 split).
     std::vector<long long> cost(n_roi);
+    static int fgpw = -1;     // weight of the FGP term (LT_PART_FGPW, diagnostics; default 2)
+    if (fgpw < 0) { const char* e = getenv("LT_PART_FGPW"); fgpw = (e && *e) ? std::max(0, atoi(e)) : 2; }
     for (int r = 0; r < n_roi; ++r) {
         const int cr = p->cen[2 * r], cc = p->cen[2 * r + 1], h = p->h;
         const long long hv = std::min(n, cr + h) - std::max(0, cr - h);
         const long long wv = std::min(n, cc + h) - std::max(0, cc - h);
-        cost[r] = 2LL * (2 * h) * (2 * h) + 3LL * hv * wv;
+        cost[r] = (long long)fgpw * (2 * h) * (2 * h) + 3LL * hv * wv;
     }
     std::vector<int> order(n_roi);
     for (int r = 0; r < n_roi; ++r) order[r] = r;
