@@ -141,7 +141,7 @@ def check_full_solve(lt, name, mode):
 
 # ordered per config, so each config's plan and bank are built once
 CASES = [("C3", "bank"), ("C3", "box"), ("C3", "tv"), ("C4", "bank"), ("C4", "tv"), ("C4", "shards"),
-         ("C5", "bank"), ("C5", "box")]
+         ("C5", "bank"), ("C5", "box"), ("C5", "shards")]
 
 
 @pytest.mark.parametrize("name,what", CASES)
@@ -149,7 +149,7 @@ def test_full_size_stated_iterations(lt, name, what):
     if what == "bank":
         check_bank_conv_disc(lt, name)
     elif what == "shards":
-        check_rank_shards(lt, name)
+        check_rank_shards(lt, name, worlds=(2, 8) if name == "C4" else (8,))
     else:
         check_full_solve(lt, name, what)
 
