@@ -627,7 +627,10 @@ int launch_fgp_cp(FgpArgs A, int rows, int ntiles, cudaStream_t st) {
         clusters8 = c4[key];
         if (c2[key] > 0 && c4[key] > 0) {
             const long long w2 = (ntiles + c2[key] - 1) / c2[key], w4 = (ntiles + c4[key] - 1) / c4[key];
-            use16 = w2 * 52 < w4 * 73;
+            // (the 52 / 73 us latencies are the 256-wide CP = 4 layout's; on narrow tiles,
+            // CP <= 2, a 32-row CTA is the faster one per wave -- L1's 64 tiles of 128^2:
+            // 46 vs 52 us per wave -- so 16-row CTAs only when they save a wave)
+            use16 = CP >= 3 ? w2 * 52 < w4 * 73 : w2 < w4;
         }
     }
     if (cfgv == 4) return launch_fgp2_t<MODE, 4, 8, false, false, CP>(A, rows, ntiles, st);
