@@ -294,6 +294,12 @@ long long resident_ctas(const lt_plan& p, Kern kern, int threads, size_t smem) {
     return (long long)std::max(1, per_sm) * p.num_sms;
 }
 
+bool fp_force24() {   // diagnostics: 24-angle CTAs even where they pad more than the 16-angle ones
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("LT_FP_24"); v = (e && atoi(e) == 1) ? 1 : 0; }
+    return v != 0;
+}
+
 bool fp_wide() {
     static int v = -1;
     if (v < 0) { const char* e = getenv("LT_FP_WIDE"); v = !(e && atoi(e) == 0); }
@@ -378,9 +384,11 @@ int launch_fp_roi(const lt_plan& p, const Tiles& t, const float* img, const floa
             k_fp_roi2<1><<<dim3(p.ngroups1, t.ntiles), 256, smem2, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups1));
         }
     } else if (fp_wide() && ((long long)p.ngroups24 * t.ntiles >= 2LL * 2 * p.num_sms || one_env == 0 || small24) &&
-               p.ngroups24 * 24 <= p.ngroups * 16) {
+               (5 * p.ngroups24 * 24 <= 6 * p.na || fp_force24())) {
         // 12 warps x 2 angles: each staged band shared by 24 angles (2 CTAs per SM),
-        // unless the 24-angle groups pad more (C5: 128 angles per orientation = 5 1/3 x 24)
+        // unless the 24-angle groups pad the angles by more than 20 % (C5's 128 angles
+        // per orientation = 5 1/3 x 24: 12.5 %, measured 134.1 vs 132.4 ROI solves/s
+        // against the 16-angle CTAs since the staged lines carry zero margins)
         const size_t smem3 = (size_t)FP2_BL * fp_line(FP2_P, 2) * sizeof(float2) + (size_t)24 * 32 * FP_U * sizeof(float);
         LT_CUDA(cudaFuncSetAttribute(k_fp_roi2<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
         k_fp_roi2<2, 12><<<dim3(p.ngroups24, t.ntiles), 384, smem3, st>>>(p.geo(), t, f, p.P<int>(p.off.fpgroups24));
