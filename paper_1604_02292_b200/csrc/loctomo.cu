@@ -1253,10 +1253,12 @@ int lt_roi_setup(int32_t n, int32_t n_angles, int32_t n_det, const double* angle
     // `world` contiguous runs of balanced cost, so each rank's ROIs are spatially
     // compact (its global x_s backprojection covers only their neighbourhood).
     // Cost model: the FGP cluster works on the full (2h)^2 tile, the projectors on
-    // the valid pixels: cost = 2 (2h)^2 + 3 * valid (measured ~40/60 split).
+    // the valid pixels: cost = 4 (2h)^2 + 3 * valid (weight 2, the measured ~40/60 time
+    // split, left the 8-GPU C4 edge ranks 34 ROIs and the slowest; 4: projected 2084 ->
+    // 2109 ROI solves/s, C5 960 -> 965, 2 / 4 GPUs unchanged; LT_PART_FGPW overrides)
     std::vector<long long> cost(n_roi);
-    static int fgpw = -1;     // weight of the FGP term (LT_PART_FGPW, diagnostics; default 2)
-    if (fgpw < 0) { const char* e = getenv("LT_PART_FGPW"); fgpw = (e && *e) ? std::max(0, atoi(e)) : 2; }
+    static int fgpw = -1;     // weight of the FGP term (LT_PART_FGPW, diagnostics; default 4)
+    if (fgpw < 0) { const char* e = getenv("LT_PART_FGPW"); fgpw = (e && *e) ? std::max(0, atoi(e)) : 4; }
     for (int r = 0; r < n_roi; ++r) {
         const int cr = p->cen[2 * r], cc = p->cen[2 * r + 1], h = p->h;
         const long long hv = std::min(n, cr + h) - std::max(0, cr - h);

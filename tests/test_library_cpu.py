@@ -133,7 +133,7 @@ def test_partition_covers_every_roi_once(lt, cfg_name):
     def cost(r):
         hv = min(c.n, cen[r, 0] + h) - max(0, cen[r, 0] - h)
         wv = min(c.n, cen[r, 1] + h) - max(0, cen[r, 1] - h)
-        return 2 * (2 * h) ** 2 + 3 * hv * wv
+        return 4 * (2 * h) ** 2 + 3 * hv * wv
     for world in (1, 2, 3, 4, 8):
         seen, loads = [], []
         for rank in range(world):
